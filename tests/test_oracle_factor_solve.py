@@ -1,0 +1,111 @@
+"""Pins for oracle.cholesky, trisolve, solve_refined, backward_error -- CPU only.
+
+Pins: numpy.linalg.cholesky (library routine) on P K P^T; reconstruction <= 1e-13 ||K||;
+diagonal K -> L = sqrt(diag); first failing column on a non-SPD input (R6); exact rational
+solutions (fractions Gaussian elimination) for the refined solve (R8); S:85-86 solve examples.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import dense
+from synth.generator import make_config, tiny_random, KKTInstance
+
+
+def _dense_lower(Kp, Ki, Kv, n):
+    K = np.zeros((n, n))
+    for j in range(n):
+        for p in range(Kp[j], Kp[j + 1]):
+            K[Ki[p], j] = Kv[p]; K[j, Ki[p]] = Kv[p]
+    return K
+
+
+def _Ldense(Lp, Li, Lx, n):
+    L = np.zeros((n, n))
+    for j in range(n):
+        for p in range(Lp[j], Lp[j + 1]):
+            L[Li[p], j] = Lx[p]
+    return L
+
+
+@pytest.mark.parametrize("cfg,Xi", [("C1", 1e-8), ("C5", 1e-2), ("C5", 1e-8)])
+def test_cholesky_vs_numpy_and_reconstruction(cfg, Xi):
+    """Entrywise agreement with numpy is only meaningful when K is well conditioned; at
+    Xi = 1e-8 the two backward-stable factors differ by O(kappa u) and only the
+    reconstruction bound is pinned."""
+    inst = make_config(cfg) if cfg == "C1" else make_config("C5", batch=1, Xi=Xi)
+    R = oracle.reference_solve(inst)
+    n = inst.n
+    K = _dense_lower(*R["K"], n)
+    P = K[np.ix_(R["perm"], R["perm"])]
+    L = _Ldense(R["Lp"], R["Li"], R["Lx"], n)
+    assert np.abs(P - L @ L.T).max() <= 1e-13 * np.abs(K).max()
+    if cfg == "C5" and Xi < 1e-4:
+        return
+    Lnp = np.linalg.cholesky(P)
+    colscale = np.abs(Lnp).max(0)
+    assert (np.abs(L - Lnp) <= 1e-11 * colscale[None, :]).all()
+
+
+def test_diagonal_matrix_sqrt():
+    n = 6
+    rng = np.random.default_rng(3)
+    d = rng.uniform(0.5, 4.0, n)
+    inst = KKTInstance("diag", n, 0, 0, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                       d, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0), np.zeros(n),
+                       np.zeros(0), b=np.arange(1.0, n + 1))
+    R = oracle.reference_solve(inst)
+    assert R["perm"].tolist() == list(range(n))
+    assert np.array_equal(R["Lx"], np.sqrt(d))
+    assert np.allclose(R["x"], np.arange(1.0, n + 1) / d, rtol=1e-16, atol=0)
+
+
+def test_identity_and_diag_solves():
+    """F of I, b=(1,2,3) -> (1,2,3); F of diag(2,4), b=(2,8) -> (1,2)."""
+    for d, b, x in (([1.0, 1.0, 1.0], [1.0, 2.0, 3.0], [1.0, 2.0, 3.0]), ([2.0, 4.0], [2.0, 8.0], [1.0, 2.0])):
+        n = len(d)
+        inst = KKTInstance("d", n, 0, 0, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                           np.array(d), np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0),
+                           np.zeros(n), np.zeros(0), b=np.array(b))
+        assert oracle.reference_solve(inst)["x"].tolist() == x
+
+
+def test_not_spd_reports_first_column():
+    """R6: LL^T fails iff a pivot <= 0; the first failing column is reported."""
+    n = 3
+    inst = KKTInstance("nspd", n, 0, 0, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                       np.array([2.0, -3.0, 1.0]), np.zeros(1, np.int32), np.zeros(0, np.int32),
+                       np.zeros(0), np.zeros(n), np.zeros(0), b=np.ones(n))
+    R = oracle.reference_solve(inst)
+    assert R["perm"][R["fail"]] == 1
+
+
+@pytest.mark.parametrize("seed", [41, 42, 43, 44])
+def test_refined_solution_is_exact_rational_solution(seed):
+    """R8: x_ref equals the exact solution of the exact-input system, correctly rounded
+    (tolerance 1 ulp), here with Sigma spanning 1e-6..1e6 and gamma rows."""
+    inst = tiny_random(8, 6, 2, seed=seed, Xi=1e-6, hykkt_gamma=1e5, delta_w=1e-3, delta_c=1e-2)
+    R = oracle.reference_solve(inst)
+    xe = dense.exact_solve(dense.exact_condensed(inst), inst.b)
+    xe = np.array([float(v) for v in xe])
+    assert np.all(np.abs(R["x"] - xe) <= np.spacing(np.abs(xe)))
+
+
+def test_backward_error_of_exact_solution_is_tiny_and_of_perturbed_is_not():
+    inst = make_config("C5", batch=1)
+    R = oracle.reference_solve(inst)
+    eta, om = oracle.backward_error(inst, R["K"], inst.b, R["x"])
+    assert eta <= 1e-16 and om <= 2.3e-16      # x rounded to double: omega <= ~u
+    xp = R["x"] * (1 + 1e-9)
+    eta2, om2 = oracle.backward_error(inst, R["K"], inst.b, xp)
+    assert om2 > 1e-10
+
+
+def test_plain_fp64_solve_is_not_enough_in_stress_regime():
+    """Appendix-A probe: in the 0 < l < n regime the unrefined FP64 solve misses x_ref
+    by far more than 1e-8 -- the reason kkt_solve refines with a double-double residual."""
+    inst = make_config("C2s")
+    R = oracle.reference_solve(inst)
+    x0 = oracle.trisolve(inst.n, R["Lp"], R["Li"], R["Lx"], R["perm"], inst.b)
+    err = np.abs(x0 - R["x"]).max() / np.abs(R["x"]).max()
+    assert err > 1e-11
