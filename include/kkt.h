@@ -1,0 +1,181 @@
+/*
+ * kkt.h -- C-ABI of libkkt.so, the B200-native condensed-KKT linear solve of the
+ * condensed-space interior-point methods LiftedKKT and HyKKT (arXiv 2405.14236).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / equation named); readings
+ * R1..R17 are listed in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *   - Indices are 0-based int32.  Host pointers are marked [host], device pointers
+ *     [device] (cudaMalloc'd / torch CUDA memory on the device given to kkt_bind).
+ *   - The caller owns every buffer it passes.  Host pattern arrays are read only during
+ *     kkt_analyze.  Device value arrays must stay valid until the stream work completes.
+ *   - The handle owns the analysis plan, its device copy, the factor and all scratch.
+ *   - Calls never abort the process.  Argument/state errors are returned immediately;
+ *     numeric failures (non-SPD pivot, CG non-convergence, non-finite values) are
+ *     recorded in a device status word and surfaced by kkt_sync_info -- the only
+ *     host-blocking call besides kkt_analyze/kkt_bind/kkt_destroy and the *_host calls.
+ *   - Per-iteration calls (kkt_condense, kkt_factor, kkt_solve, hykkt_solve) are
+ *     stream-ordered on the stream given to kkt_bind and do not synchronise the host.
+ *   - One in-flight condense->factor->solve sequence per handle.  Handles are
+ *     independent; use one per GPU.
+ *   - Batch (options.batch = B > 1): B instances share the pattern ("same structure,
+ *     different parameters").  Every value array is [B][len] contiguous:
+ *     W_vals [B][nnzW], J_vals [B][nnzJ], Sigma_x [B][n], Sigma_s [B][m-m_eq],
+ *     D [B][m], b/x/dx [B][n], rbar2/dy [B][m_eq].
+ */
+#ifndef KKT_H
+#define KKT_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kkt_plan *kkt_handle;   /* opaque */
+typedef void *kkt_stream_t;            /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  KKT_OK = 0,
+  KKT_ERR_ARG = 1,            /* bad argument (null pointer, size, index out of range) */
+  KKT_ERR_PATTERN = 2,        /* pattern invalid: unsorted/duplicate/out-of-range/upper entry */
+  KKT_ERR_NOT_SPD = 3,        /* a pivot <= 0 or non-finite (R6); fail_col reports it     */
+  KKT_ERR_NOT_CONVERGED = 4,  /* HyKKT CG reached cg_maxit before rtol (R10)              */
+  KKT_ERR_NONFINITE = 5,      /* non-finite value in a solve / refinement                 */
+  KKT_ERR_CUDA = 6,           /* CUDA runtime error (message via kkt_last_error)          */
+  KKT_ERR_ALLOC = 7,          /* device or host allocation failed / workspace too small   */
+  KKT_ERR_STATE = 8           /* call out of order (e.g. kkt_solve before kkt_factor)     */
+} kkt_status;
+
+typedef struct {
+  int ordering;          /* 0 = MD-exact-v1 (default; bit-exact contract R11), 1 = natural  */
+  int factor_kind;       /* 0 = LL^T (default, R5); 1 reserved for pivot-free LDL^T        */
+  int relax_small;       /* amalgamation: merge if combined width <= relax_small (perf only) */
+  int relax_big;         /* amalgamation: never merge beyond this width                     */
+  double relax_zero_frac;/* amalgamation: max fraction of explicit zeros added               */
+  int batch;             /* instances sharing the pattern (C5), default 1                   */
+} kkt_options;
+
+typedef struct {
+  long long nnzK;        /* nnz of the lower triangle of K (diagonal included)            */
+  long long nnzL;        /* nnz(L) of the exact (non-amalgamated) factor, sum of colcounts */
+  long long nnzL_stored; /* doubles stored in supernodal panels (amalgamated)              */
+  double flops;          /* sum_j c_j^2 (SURVEY §8(d) factor work per instance)             */
+  long long nprod;       /* products in the condensation map (J^T D J terms)               */
+  int nsuper;            /* supernodes after amalgamation                                 */
+  int tree_height;       /* height of the supernodal elimination tree (levels)            */
+  int max_front;         /* largest front (rows of a supernode)                           */
+  double analyze_ms;     /* host time of kkt_analyze                                      */
+  double order_ms;       /* of which: MD-exact-v1 ordering                                */
+  long long update_doubles; /* per-instance multifrontal update-matrix storage            */
+} kkt_analysis_info;
+
+/* Fill *opt with defaults (MD-exact-v1, LL^T, relax 4/64/0.05, batch 1). */
+kkt_status kkt_default_options(kkt_options *opt);
+
+/*
+ * kkt_analyze -- once per sparsity pattern ("analysis phase", reported
+ * separately from the numeric path).  [host] inputs:
+ *   n, m, m_eq     variables; rows of J; rows [0, m_eq) of J are the equalities G whose
+ *                  weight is gamma (HyKKT); rows [m_eq, m) carry D_H.
+ *                  LiftedKKT: m_eq = 0 and J = H_tau.
+ *   W_rowptr[n+1], W_colind[nnzW]   lower triangle of the Hessian W (col <= row), sorted,
+ *                  no duplicates.  The diagonal need not be present.
+ *   J_rowptr[m+1], J_colind[nnzJ]   Jacobian J (m x n) CSR, sorted, no duplicates.
+ * Builds pattern(K) = pattern(W) U pattern(J^T J) U diag, the MD-exact-v1
+ * ordering, etree, column counts, supernodes, the condensation gather map and the
+ * multifrontal update maps.  On success *handle owns the plan; *info (optional) is filled.
+ * Errors: KKT_ERR_ARG (null/negative sizes), KKT_ERR_PATTERN, KKT_ERR_ALLOC.
+ */
+kkt_status kkt_analyze(int n, int m, int m_eq, const int *W_rowptr, const int *W_colind,
+                       const int *J_rowptr, const int *J_colind, const kkt_options *opt,
+                       kkt_handle *handle, kkt_analysis_info *info);
+
+/* [host] out: perm[n] (new -> old, MD-exact-v1 order), etree[n] (parent in the permuted
+ * numbering, -1 = root), colcount[n] (nnz of column j of L incl. diagonal).  Any may be NULL. */
+kkt_status kkt_get_symbolic(kkt_handle h, int *perm, int *etree, int *colcount);
+
+/* Device bytes kkt_bind needs in its caller-provided workspace (per-iteration numeric data
+ * for all `batch` instances; the static plan lives in handle-owned memory). */
+kkt_status kkt_workspace_size(kkt_handle h, size_t *bytes);
+
+/* Bind the handle to a CUDA device and stream; upload the plan (one H2D copy).
+ * d_workspace [device] of >= kkt_workspace_size bytes (caller-owned, e.g. a torch tensor)
+ * or NULL to let the library allocate it.  Must be called before any per-iteration call. */
+kkt_status kkt_bind(kkt_handle h, int device, void *d_workspace, size_t bytes, kkt_stream_t stream);
+
+/*
+ * kkt_condense -- K = W + D_x + delta_w I + J^T D J on the fixed pattern (K1;
+ * P:496 K_gamma; P:556 K_tau).  [device] inputs (batch-strided):
+ *   W_vals[nnzW], J_vals[nnzJ], Sigma_x[n] (= D_x = X^-1 U), Sigma_s[m - m_eq]
+ *   (= D_s = S^-1 V of the inequality rows), D[m] optional override of every row weight
+ *   (NULL -> D_r = gamma for r < m_eq, D_r = (Sigma_s+dw)/(1+dc(Sigma_s+dw)) otherwise).
+ * The value pointers are remembered by the handle and re-read by kkt_solve / hykkt_solve
+ * (the refinement residual uses the UNASSEMBLED operator, R8); keep them unchanged until
+ * the next kkt_condense.  Writes K into handle storage.  Non-blocking.
+ */
+kkt_status kkt_condense(kkt_handle h, const double *W_vals, const double *J_vals,
+                        const double *Sigma_x, const double *Sigma_s, const double *D,
+                        double delta_w, double delta_c, double gamma);
+
+/* kkt_factor -- pivot-free supernodal multifrontal Cholesky P K P^T = L L^T (P:512, P:524,
+ * P:560).  A pivot <= 0 or non-finite records KKT_ERR_NOT_SPD and the failing column
+ * (original index) in the device status word; the factor is then invalid.  Non-blocking. */
+kkt_status kkt_factor(kkt_handle h);
+
+/*
+ * kkt_solve -- x = K^-1 b by forward/backward supernodal triangular solves,
+ * then up to max_refine Richardson sweeps whose residual b - K x is evaluated
+ * with the UNASSEMBLED operator W x + (Sigma_x+dw) x + J^T(D o (J x)) in double-double
+ * (R8/R9).  A sweep stops the loop when the componentwise backward error
+ * omega <= tol_bwd (tol_bwd <= 0 -> 1e-15), when ||dx|| <= 2u ||x||, or when omega grows
+ * twice.  [device] b[n], x[n] (batch-strided; may not alias).  Non-blocking.
+ */
+kkt_status kkt_solve(kkt_handle h, const double *b, double *x, int max_refine, double tol_bwd);
+
+/*
+ * hykkt_solve -- HyKKT on K_gamma = K + gamma G^T G, requires a
+ * preceding kkt_condense with m_eq > 0 (delta_c applies to inequality rows only)
+ * and kkt_factor:
+ *   s = rbar1 + gamma G^T rbar2;  CG on S_gamma dy = G K_gamma^-1 s - rbar2 (eq. 14,
+ *   x0 = 0, stop ||r_k||_2 <= cg_rtol ||r_0||_2, R10);  dx = K_gamma^-1 (s - G^T dy);
+ * then max_outer_refine sweeps of refinement on the saddle system [K G^T; G 0]
+ * with a double-double residual.  [device] rbar1[n], rbar2[m_eq] in; dx[n], dy[m_eq] out.
+ * Non-blocking; KKT_ERR_NOT_CONVERGED is reported through kkt_sync_info.
+ */
+kkt_status hykkt_solve(kkt_handle h, const double *rbar1, const double *rbar2, double *dx,
+                       double *dy, double cg_rtol, int cg_maxit, int max_outer_refine);
+
+/* Block the host until the handle's stream is idle; report and clear the device status.
+ * Any out pointer may be NULL.  status: a kkt_status value; fail_col: original column of
+ * the first non-SPD pivot or -1; refine_iters: sweeps run by the last solve (max over the
+ * batch); cg_iters: CG iterations of the first HyKKT pass (max over the batch); bwd_err:
+ * componentwise backward error omega after the last solve (max over the batch). */
+kkt_status kkt_sync_info(kkt_handle h, int *status, int *fail_col, int *refine_iters,
+                         int *cg_iters, double *bwd_err);
+
+/* End-to-end convenience call on HOST buffers (the e2e path of bench.py): copies the
+ * values [host] W_vals, J_vals, Sigma_x, Sigma_s, (D or NULL), b to the device, runs
+ * condense -> factor -> solve and copies x [host] back.  Blocking. */
+kkt_status kkt_step_host(kkt_handle h, const double *W_vals, const double *J_vals,
+                         const double *Sigma_x, const double *Sigma_s, const double *D,
+                         double delta_w, double delta_c, double gamma, const double *b,
+                         double *x, int max_refine, double tol_bwd);
+
+/* Test/debug export of the condensed matrix of batch instance `inst`, lower CSC in ORIGINAL
+ * indices: [host] Kp[n+1], Ki[nnzK], Kv[nnzK] (any may be NULL).  Blocking. */
+kkt_status kkt_get_condensed(kkt_handle h, int inst, int *Kp, int *Ki, double *Kv);
+
+/* Number of kernel launches the last per-iteration call enqueued (evidence counter). */
+kkt_status kkt_launch_count(kkt_handle h, long long *launches);
+
+/* Last error message (static storage, thread-local). */
+const char *kkt_last_error(void);
+
+kkt_status kkt_destroy(kkt_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KKT_H */

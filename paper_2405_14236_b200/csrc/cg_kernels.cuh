@@ -1,0 +1,198 @@
+// cg_kernels.cuh -- refinement control and HyKKT CG kernels.
+// All reductions are deterministic: fixed per-block trees, partials summed in block order by
+// the last-arriving block (no floating-point atomics).
+#pragma once
+#include "kernels.cuh"
+
+namespace kkt {
+
+__device__ __forceinline__ double bits2d(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+// ---------------------------------------------------------------- refinement control
+__global__ void refine_init_kernel(int batch, DevCtrl C) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  C.done[b] = 0; C.refine_iters[b] = 0; C.grow[b] = 0;
+  C.omega[b] = 0ULL; C.omega_prev[b] = INFINITY; C.omega_last[b] = 0.0;
+  C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
+}
+
+// Stopping rules (R9): omega <= tol; ||dx|| <= 2u ||x|| after the previous correction;
+// omega grew in two consecutive sweeps; last sweep (measurement only).
+__global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep, int last) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  if (C.done[b]) return;
+  double om = bits2d(C.omega[b]);
+  C.omega[b] = 0ULL;
+  C.omega_last[b] = om;
+  bool stop = last || !(om > tol);  // NaN -> stop
+  if (sweep > 0) {
+    double dxn = bits2d(C.dxn[b]), xn = bits2d(C.xn[b]);
+    C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
+    if (dxn <= 2.0 * 1.1102230246251565e-16 * xn) stop = true;
+    if (om > C.omega_prev[b]) { if (++C.grow[b] >= 2) stop = true; }
+    else C.grow[b] = 0;
+  }
+  C.omega_prev[b] = om;
+  if (stop) C.done[b] = 1;
+  else C.refine_iters[b] += 1;
+}
+
+__global__ void refine_update_kernel(int batch, int n, double* x, const double* __restrict__ dx, DevCtrl C) {
+  long long total = (long long)batch * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(idx / n);
+    if (C.done[b]) continue;
+    double d = dx[idx], xv = x[idx] + d;
+    x[idx] = xv;
+    atomic_max_pos(C.dxn + b, fabs(d));
+    atomic_max_pos(C.xn + b, fabs(xv));
+  }
+}
+
+// ---------------------------------------------------------------- G^T and G products
+// out_i = base_i + alpha * sum_{r < m_eq} J_ri y_r   (the G^T prefix of every J^T column)
+__global__ void gt_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ y,
+                          double alpha, const double* __restrict__ base, double* out,
+                          const int* __restrict__ skip) {
+  long long total = (long long)P.batch * P.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(idx / P.n), i = (int)(idx % P.n);
+    if (skip && skip[b]) continue;
+    const double* J = Jv + (long long)b * P.nnzJ;
+    const double* yb = y + (long long)b * P.m_eq;
+    double acc = 0.0;
+    for (int p = P.Jt_p[i]; p < P.Gt_end[i]; p++) acc = fma(J[P.Jt_k[p]], yb[P.Jt_r[p]], acc);
+    out[idx] = base ? fma(alpha, acc, base[idx]) : alpha * acc;
+  }
+}
+
+// Block tree reduction (fixed order) of one double per thread; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nw; k++) s += red[k];
+  return s;
+}
+
+// Returns true in thread 0 of the last-arriving block of instance b; *sum = ordered sum.
+__device__ __forceinline__ bool finish_dot(DevCtrl C, int b, double part, double* sum) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    C.partial[b * KKT_NPART + blockIdx.x] = part;
+    __threadfence();
+    unsigned int a = atomicAdd(C.part_cnt + b, 1u);
+    last = (a == KKT_NPART - 1);
+    if (last) {
+      __threadfence();
+      double s = 0.0;
+      for (int k = 0; k < KKT_NPART; k++) s += __ldcg(C.partial + b * KKT_NPART + k);
+      *sum = s;
+      C.part_cnt[b] = 0u;
+    }
+  }
+  __syncthreads();
+  return last && threadIdx.x == 0;
+}
+
+// mode 0 (CG start):  r = G z - rbar2 ; p = r ; dy = 0 ; rr = rr0 = r.r
+// mode 1 (CG step c): q = G z ; pq = p.q ; alpha = rr / pq
+// grid (KKT_NPART, batch)
+__global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ z,
+                         const double* __restrict__ sub, double* out, double* p, double* dy,
+                         DevCtrl C, int mode) {
+  __shared__ double red[32];
+  const int b = blockIdx.y;
+  if (mode == 1 && C.cg_done[b]) return;
+  const int me = P.m_eq;
+  const double* J = Jv + (long long)b * P.nnzJ;
+  const double* zb = z + (long long)b * P.n;
+  double part = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < me; r += KKT_NPART * blockDim.x) {
+    double acc = 0.0;
+    for (int q = P.Jrp[r]; q < P.Jrp[r + 1]; q++) acc = fma(J[q], zb[P.Jci[q]], acc);
+    long long o = (long long)b * me + r;
+    if (mode == 0) {
+      acc -= sub[o];
+      out[o] = acc;
+      p[o] = acc;
+      dy[o] = 0.0;
+      part = fma(acc, acc, part);
+    } else {
+      out[o] = acc;
+      part = fma(p[o], acc, part);
+    }
+  }
+  double s = block_sum(part, red), tot;
+  if (finish_dot(C, b, s, &tot)) {
+    if (mode == 0) {
+      C.rr[b] = tot; C.rr0[b] = tot; C.cg_iters[b] = 0;
+      C.cg_done[b] = (tot == 0.0) ? 1 : 0;
+    } else {
+      C.pq[b] = tot;
+      C.alpha[b] = C.rr[b] / tot;
+    }
+  }
+}
+
+// dy += alpha p ; r -= alpha q ; rr_new = r.r ; convergence ||r|| <= rtol ||r0|| (R10)
+__global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const double* __restrict__ p,
+                                 const double* __restrict__ q, DevCtrl C, double rtol, int* status) {
+  __shared__ double red[32];
+  const int b = blockIdx.y;
+  if (C.cg_done[b]) return;
+  const double a = C.alpha[b];
+  double part = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < me; i += KKT_NPART * blockDim.x) {
+    long long o = (long long)b * me + i;
+    dy[o] = fma(a, p[o], dy[o]);
+    double rv = fma(-a, q[o], r[o]);
+    r[o] = rv;
+    part = fma(rv, rv, part);
+  }
+  double s = block_sum(part, red), tot;
+  if (finish_dot(C, b, s, &tot)) {
+    C.cg_iters[b] += 1;
+    if (!isfinite(tot) || !isfinite(a)) {
+      C.cg_done[b] = 1;
+      atomicCAS(status, 0, 5 /* KKT_ERR_NONFINITE */);
+    } else if (sqrt(tot) <= rtol * sqrt(C.rr0[b])) {
+      C.cg_done[b] = 1;
+    }
+    C.beta[b] = tot / C.rr[b];
+    C.rr[b] = tot;
+  }
+}
+
+__global__ void cg_p_kernel(int batch, int me, double* p, const double* __restrict__ r, DevCtrl C) {
+  long long total = (long long)batch * me;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(idx / me);
+    if (C.cg_done[b]) continue;
+    p[idx] = fma(C.beta[b], p[idx], r[idx]);
+  }
+}
+
+__global__ void axpy_kernel(long long total, double* y, const double* __restrict__ x) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x)
+    y[idx] += x[idx];
+}
+
+__global__ void cg_finish_kernel(int batch, DevCtrl C, int first, int* status) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  if (first) C.cg_iters_first[b] = C.cg_iters[b];
+  if (!C.cg_done[b]) atomicCAS(status, 0, 4 /* KKT_ERR_NOT_CONVERGED */);
+}
+
+}  // namespace kkt

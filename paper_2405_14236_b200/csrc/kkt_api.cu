@@ -1,0 +1,635 @@
+// kkt_api.cu -- C-ABI of libkkt.so (include/kkt.h): plan upload, workspace carving and the
+// stream-ordered launch sequences of the per-IPM-iteration hot path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kkt.h"
+#include "cg_kernels.cuh"
+#include "kernels.cuh"
+#include "plan.h"
+
+using namespace kkt;
+
+static thread_local std::string g_err;
+
+#define CUDA_TRY(x)                                                                \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess) {                                                       \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                     \
+      return e_ == cudaErrorMemoryAllocation ? KKT_ERR_ALLOC : KKT_ERR_CUDA;       \
+    }                                                                              \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                             \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess) {                                                       \
+      g_err = std::string("launch: ") + cudaGetErrorString(e_);                    \
+      return KKT_ERR_CUDA;                                                         \
+    }                                                                              \
+  } while (0)
+
+struct kkt_plan {
+  Plan P;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  bool bound = false;
+  int sms = 148;
+  // device plan
+  void* plan_mem = nullptr;
+  DevPlan dp{};
+  // workspace
+  void* ws = nullptr;
+  bool ws_owned = false;
+  size_t ws_bytes = 0;
+  double *Kv = nullptr, *Lx = nullptr, *Ub = nullptr, *uv = nullptr, *Y = nullptr, *Xp = nullptr;
+  double *Dh = nullptr, *Dl = nullptr, *A = nullptr, *res = nullptr, *dxv = nullptr, *res2 = nullptr;
+  double2* T = nullptr;
+  double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
+  double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
+  int *fcnt = nullptr, *bflag = nullptr, *facnt = nullptr, *ctl = nullptr, *fail = nullptr,
+      *status = nullptr;
+  DevCtrl C{};
+  // current values (remembered by kkt_condense for the refinement residual)
+  const double *Wv = nullptr, *Jv = nullptr, *Sx = nullptr, *Ss = nullptr, *Dov = nullptr;
+  double dw = 0, dc = 0, gamma = 0;
+  bool condensed = false, factored = false;
+  // launch configuration
+  long long factor_smem_cap = 0;
+  int factor_smem = 0, fwd_smem = 0, bwd_smem = 0;
+  int grid_factor = 1, grid_fwd = 1, grid_bwd = 1;
+  long long launches = 0;
+  // host-buffer path (kkt_step_host)
+  double *hW = nullptr, *hJ = nullptr, *hSx = nullptr, *hSs = nullptr, *hD = nullptr,
+         *hb = nullptr, *hx = nullptr;
+  int* pinned_flags = nullptr;
+};
+
+static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  bool dry;
+  template <class T>
+  T* take(size_t count) {
+    size_t o = off;
+    off = align_up(off + count * sizeof(T));
+    return dry ? nullptr : reinterpret_cast<T*>(base + o);
+  }
+};
+
+static void carve_workspace(kkt_plan* h, Carver& c) {
+  const Plan& P = h->P;
+  size_t B = P.batch, n = P.n, m = P.m, me = P.m_eq, ns = P.ns;
+  h->Kv = c.take<double>(B * P.Kp[n]);
+  h->Lx = c.take<double>(B * P.nnzL_stored);
+  h->Ub = c.take<double>(B * P.update_doubles);
+  h->uv = c.take<double>(B * P.uvec_doubles);
+  h->Y = c.take<double>(B * n);
+  h->Xp = c.take<double>(B * n);
+  h->res = c.take<double>(B * n);
+  h->dxv = c.take<double>(B * n);
+  h->Dh = c.take<double>(B * m);
+  h->Dl = c.take<double>(B * m);
+  h->A = c.take<double>(B * m);
+  h->T = c.take<double2>(B * m);
+  h->res2 = c.take<double>(B * me);
+  h->sg = c.take<double>(B * n);
+  h->zv = c.take<double>(B * n);
+  h->wv = c.take<double>(B * n);
+  h->hdx = c.take<double>(B * n);
+  h->hr1 = c.take<double>(B * n);
+  h->cr = c.take<double>(B * me);
+  h->cp = c.take<double>(B * me);
+  h->cq = c.take<double>(B * me);
+  h->hdy = c.take<double>(B * me);
+  h->hr2 = c.take<double>(B * me);
+  h->fcnt = c.take<int>(B * ns);
+  h->bflag = c.take<int>(B * ns);
+  h->facnt = c.take<int>(B * ns);
+  h->ctl = c.take<int>(8);
+  h->fail = c.take<int>(1);
+  h->status = c.take<int>(1);
+  h->C.done = c.take<int>(B);
+  h->C.refine_iters = c.take<int>(B);
+  h->C.grow = c.take<int>(B);
+  h->C.omega = c.take<unsigned long long>(B);
+  h->C.omega_prev = c.take<double>(B);
+  h->C.omega_last = c.take<double>(B);
+  h->C.dxn = c.take<unsigned long long>(B);
+  h->C.xn = c.take<unsigned long long>(B);
+  h->C.cg_done = c.take<int>(B);
+  h->C.cg_iters = c.take<int>(B);
+  h->C.cg_iters_first = c.take<int>(B);
+  h->C.rr = c.take<double>(B);
+  h->C.rr0 = c.take<double>(B);
+  h->C.pq = c.take<double>(B);
+  h->C.alpha = c.take<double>(B);
+  h->C.beta = c.take<double>(B);
+  h->C.partial = c.take<double>(B * KKT_NPART);
+  h->C.part_cnt = c.take<unsigned int>(B);
+}
+
+// ------------------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char* kkt_last_error(void) { return g_err.c_str(); }
+
+kkt_status kkt_default_options(kkt_options* o) {
+  if (!o) return KKT_ERR_ARG;
+  o->ordering = 0;
+  o->factor_kind = 0;
+  o->relax_small = 4;
+  o->relax_big = 64;
+  o->relax_zero_frac = 0.05;
+  o->batch = 1;
+  return KKT_OK;
+}
+
+kkt_status kkt_analyze(int n, int m, int m_eq, const int* W_rowptr, const int* W_colind,
+                       const int* J_rowptr, const int* J_colind, const kkt_options* opt,
+                       kkt_handle* handle, kkt_analysis_info* info) {
+  if (!handle) { g_err = "null handle"; return KKT_ERR_ARG; }
+  *handle = nullptr;
+  kkt_options o;
+  kkt_default_options(&o);
+  if (opt) o = *opt;
+  if (o.factor_kind != 0) { g_err = "factor_kind 1 (LDL^T) not available"; return KKT_ERR_ARG; }
+  if (o.batch < 1) { g_err = "batch < 1"; return KKT_ERR_ARG; }
+  kkt_plan* h = new (std::nothrow) kkt_plan();
+  if (!h) return KKT_ERR_ALLOC;
+  Options op;
+  op.ordering = o.ordering;
+  op.relax_small = o.relax_small;
+  op.relax_big = o.relax_big;
+  op.relax_zero_frac = o.relax_zero_frac;
+  op.batch = o.batch;
+  int code = 0;
+  std::string err;
+  try {
+    err = analyze(n, m, m_eq, W_rowptr, W_colind, J_rowptr, J_colind, op, h->P, &code);
+  } catch (const std::bad_alloc&) {
+    delete h;
+    g_err = "host allocation failed in analysis";
+    return KKT_ERR_ALLOC;
+  }
+  if (!err.empty()) {
+    delete h;
+    g_err = err;
+    return code == 1 ? KKT_ERR_ARG : KKT_ERR_PATTERN;
+  }
+  if (info) {
+    const Plan& P = h->P;
+    info->nnzK = P.Kp[P.n];
+    info->nnzL = P.nnzL;
+    info->nnzL_stored = P.nnzL_stored;
+    info->flops = P.flops;
+    info->nprod = P.nprod;
+    info->nsuper = P.ns;
+    info->tree_height = P.height;
+    info->max_front = P.max_front;
+    info->analyze_ms = P.analyze_ms;
+    info->order_ms = P.order_ms;
+    info->update_doubles = P.update_doubles;
+  }
+  *handle = h;
+  return KKT_OK;
+}
+
+kkt_status kkt_get_symbolic(kkt_handle h, int* perm, int* etree, int* colcount) {
+  if (!h) return KKT_ERR_ARG;
+  size_t n = h->P.n;
+  if (perm) std::memcpy(perm, h->P.perm_md.data(), n * sizeof(int));
+  if (etree) std::memcpy(etree, h->P.etree_md.data(), n * sizeof(int));
+  if (colcount) std::memcpy(colcount, h->P.colcount_md.data(), n * sizeof(int));
+  return KKT_OK;
+}
+
+kkt_status kkt_workspace_size(kkt_handle h, size_t* bytes) {
+  if (!h || !bytes) return KKT_ERR_ARG;
+  Carver c{nullptr, 0, true};
+  carve_workspace(h, c);
+  *bytes = c.off;
+  return KKT_OK;
+}
+
+}  // extern "C"
+
+// J pattern is needed on the device: analysis keeps it in Plan via jrow + these vectors.
+// (Rebuilt here from Jt maps to avoid storing the caller's arrays twice.)
+static void rebuild_J_csr(const Plan& P, std::vector<int>& Jrp, std::vector<int>& Jci) {
+  Jrp.assign(P.m + 1, 0);
+  Jci.assign(P.nnzJ, 0);
+  for (int p = 0; p < P.nnzJ; p++) Jrp[P.jrow[p] + 1]++;
+  for (int r = 0; r < P.m; r++) Jrp[r + 1] += Jrp[r];
+  for (int i = 0; i < P.n; i++)
+    for (int q = P.Jt_p[i]; q < P.Jt_p[i + 1]; q++) Jci[P.Jt_k[q]] = i;
+}
+
+template <class T>
+static size_t vbytes(const std::vector<T>& v) { return align_up(v.size() * sizeof(T) + 1); }
+
+extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size_t bytes,
+                               kkt_stream_t stream) {
+  if (!h) return KKT_ERR_ARG;
+  if (h->bound) { g_err = "already bound"; return KKT_ERR_STATE; }
+  CUDA_TRY(cudaSetDevice(device));
+  h->device = device;
+  h->stream = (cudaStream_t)stream;
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  h->sms = prop.multiProcessorCount;
+  const Plan& P = h->P;
+  std::vector<int> Jrp, Jci;
+  rebuild_J_csr(P, Jrp, Jci);
+  // ---- plan upload (one allocation, one H2D per array) ----
+  const std::vector<int>* iv[] = {&P.perm, &P.iperm, &P.Kp, &P.Ki, &P.kw, &P.kdiag, &P.pptr,
+                                  &P.pa, &P.pb, &P.jrow, &P.kpos, &P.sn_first, &P.sn_rp,
+                                  &P.sn_rows, &P.sn_rel, &P.sn_parent, &P.sn_cp, &P.sn_ch,
+                                  &P.order, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
+                                  &P.Jt_k, &P.Gt_end, &Jrp, &Jci};
+  const std::vector<long long>* lv[] = {&P.sn_Lp, &P.sn_Up, &P.sn_uvp};
+  size_t tot = 0;
+  for (auto* v : iv) tot += vbytes(*v);
+  for (auto* v : lv) tot += vbytes(*v);
+  CUDA_TRY(cudaMalloc(&h->plan_mem, tot));
+  std::vector<const void*> dptr;
+  size_t off = 0;
+  char* base = (char*)h->plan_mem;
+  for (auto* v : iv) {
+    if (!v->empty()) CUDA_TRY(cudaMemcpy(base + off, v->data(), v->size() * sizeof(int), cudaMemcpyHostToDevice));
+    dptr.push_back(base + off);
+    off += vbytes(*v);
+  }
+  for (auto* v : lv) {
+    if (!v->empty()) CUDA_TRY(cudaMemcpy(base + off, v->data(), v->size() * sizeof(long long), cudaMemcpyHostToDevice));
+    dptr.push_back(base + off);
+    off += vbytes(*v);
+  }
+  DevPlan& d = h->dp;
+  d.n = P.n; d.m = P.m; d.m_eq = P.m_eq; d.nnzW = P.nnzW; d.nnzJ = P.nnzJ; d.nnzK = P.Kp[P.n];
+  d.ns = P.ns; d.batch = P.batch; d.max_front = P.max_front;
+  d.nnzL_stored = P.nnzL_stored; d.update_doubles = P.update_doubles;
+  d.uvec_doubles = P.uvec_doubles; d.nprod = P.nprod;
+  int k = 0;
+  auto I = [&](void) { return (const int*)dptr[k++]; };
+  d.perm = I(); d.iperm = I(); d.Kp = I(); d.Ki = I(); d.kw = I(); d.kdiag = I(); d.pptr = I();
+  d.pa = I(); d.pb = I(); d.jrow = I(); d.kpos = I(); d.sn_first = I(); d.sn_rp = I();
+  d.sn_rows = I(); d.sn_rel = I(); d.sn_parent = I(); d.sn_cp = I(); d.sn_ch = I();
+  d.order = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
+  d.Jt_k = I(); d.Gt_end = I(); d.Jrp = I(); d.Jci = I();
+  d.sn_Lp = (const long long*)dptr[k++];
+  d.sn_Up = (const long long*)dptr[k++];
+  d.sn_uvp = (const long long*)dptr[k++];
+  // ---- workspace ----
+  size_t need;
+  kkt_workspace_size(h, &need);
+  if (d_workspace) {
+    if (bytes < need) { g_err = "workspace too small"; return KKT_ERR_ALLOC; }
+    h->ws = d_workspace;
+    h->ws_owned = false;
+  } else {
+    CUDA_TRY(cudaMalloc(&h->ws, need));
+    h->ws_owned = true;
+  }
+  h->ws_bytes = need;
+  Carver c{(char*)h->ws, 0, false};
+  carve_workspace(h, c);
+  CUDA_TRY(cudaMemsetAsync(h->ws, 0, need, h->stream));
+  int big = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  // ---- launch configuration ----
+  long long maxneed = 0;
+  for (int s = 0; s < P.ns; s++) {
+    long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = P.sn_first[s + 1] - P.sn_first[s], R = r - w;
+    long long need_s = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
+    maxneed = std::max(maxneed, need_s);
+  }
+  const long long cap_bytes = 96 * 1024;
+  h->factor_smem_cap = std::min(maxneed, cap_bytes / 8);
+  h->factor_smem = (int)(h->factor_smem_cap * 8);
+  h->fwd_smem = (int)((P.max_front + 64 * 64) * 8);
+  h->bwd_smem = (int)((2 * P.max_front + 64 * 64) * 8);
+  CUDA_TRY(cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(h->factor_smem, 1)));
+  CUDA_TRY(cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fwd_smem));
+  CUDA_TRY(cudaFuncSetAttribute(bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->bwd_smem));
+  int occ = 0;
+  long long tasks = (long long)P.ns * P.batch;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_kernel, KKT_NT, h->factor_smem));
+  h->grid_factor = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_kernel, KKT_NT, h->fwd_smem));
+  h->grid_fwd = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bwd_kernel, KKT_NT, h->bwd_smem));
+  h->grid_bwd = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
+  CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->bound = true;
+  return KKT_OK;
+}
+
+static int grid_for(long long total, int threads, int sms) {
+  long long g = (total + threads - 1) / threads;
+  return (int)std::max(1LL, std::min(g, (long long)sms * 16));
+}
+
+extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const double* J_vals,
+                                   const double* Sigma_x, const double* Sigma_s, const double* D,
+                                   double delta_w, double delta_c, double gamma) {
+  if (!h) return KKT_ERR_ARG;
+  if (!h->bound) { g_err = "kkt_bind first"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  if ((!W_vals && P.nnzW) || (!J_vals && P.nnzJ) || !Sigma_x || (!Sigma_s && !D && P.m > P.m_eq)) {
+    g_err = "null value pointer";
+    return KKT_ERR_ARG;
+  }
+  h->Wv = W_vals; h->Jv = J_vals; h->Sx = Sigma_x; h->Ss = Sigma_s; h->Dov = D;
+  h->dw = delta_w; h->dc = delta_c; h->gamma = gamma;
+  h->launches = 0;
+  if (P.m > 0) {
+    dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->stream>>>(
+        h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  long long tot = (long long)P.batch * P.Kp[P.n];
+  condense_kernel<<<grid_for(tot, 256, h->sms), 256, 0, h->stream>>>(h->dp, W_vals, J_vals, Sigma_x,
+                                                                     h->Dh, delta_w, h->Kv);
+  LAUNCH_CHECK();
+  h->launches++;
+  h->condensed = true;
+  h->factored = false;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_factor(kkt_handle h) {
+  if (!h) return KKT_ERR_ARG;
+  if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
+  factor_kernel<<<h->grid_factor, KKT_NT, h->factor_smem, h->stream>>>(
+      h->dp, h->Kv, h->Lx, h->Ub, h->facnt, h->ctl + 0, h->fail, h->factor_smem_cap);
+  LAUNCH_CHECK();
+  h->launches++;
+  h->factored = true;
+  return KKT_OK;
+}
+
+// forward + backward solve of all batch instances: xout = K^-1 rhs
+static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, double* xout,
+                               long long xs, const int* done) {
+  fwd_kernel<<<h->grid_fwd, KKT_NT, h->fwd_smem, h->stream>>>(h->dp, h->Lx, rhs, rs, h->Y, h->uv,
+                                                               h->fcnt, h->ctl + 2, done);
+  LAUNCH_CHECK();
+  bwd_kernel<<<h->grid_bwd, KKT_NT, h->bwd_smem, h->stream>>>(h->dp, h->Lx, h->Y, h->Xp, xout, xs,
+                                                               h->bflag, h->ctl + 4, done);
+  LAUNCH_CHECK();
+  h->launches += 2;
+  return KKT_OK;
+}
+
+static kkt_status launch_resid(kkt_plan* h, const double* x, const double* rhs, int mode,
+                               const double* dy, const double* rb2, double* res,
+                               unsigned long long* omega, const int* done) {
+  const Plan& P = h->P;
+  if (P.m > 0) {
+    resid_rows_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->stream>>>(
+        h->dp, h->Jv, h->Dh, h->Dl, x, P.n, mode, dy, rb2, h->res2, h->T, h->A, done);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  resid_cols_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->stream>>>(
+      h->dp, h->Wv, h->Jv, h->Sx, h->dw, x, P.n, rhs, P.n, h->T, h->A, res, omega, done);
+  LAUNCH_CHECK();
+  h->launches++;
+  return KKT_OK;
+}
+
+#define TRY(x) do { kkt_status s_ = (x); if (s_ != KKT_OK) return s_; } while (0)
+
+extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int max_refine, double tol_bwd) {
+  if (!h || !b || !x) return KKT_ERR_ARG;
+  if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  if (tol_bwd <= 0) tol_bwd = 1e-15;
+  max_refine = std::max(0, max_refine);
+  h->launches = 0;
+  int gb = (P.batch + 127) / 128;
+  refine_init_kernel<<<gb, 128, 0, h->stream>>>(P.batch, h->C);
+  LAUNCH_CHECK();
+  h->launches++;
+  TRY(launch_solve(h, b, P.n, x, P.n, nullptr));
+  for (int k = 0; k <= max_refine; k++) {
+    TRY(launch_resid(h, x, b, 0, nullptr, nullptr, h->res, h->C.omega, h->C.done));
+    refine_decide_kernel<<<gb, 128, 0, h->stream>>>(P.batch, h->C, tol_bwd, k, k == max_refine);
+    LAUNCH_CHECK();
+    h->launches++;
+    if (k == max_refine) break;
+    TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
+    refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->stream>>>(
+        P.batch, P.n, x, h->dxv, h->C);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  return KKT_OK;
+}
+
+// one HyKKT pass for right-hand side (r1, r2) -> (dxo, dyo)
+static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, double* dxo,
+                             double* dyo, double rtol, int maxit, bool first) {
+  const Plan& P = h->P;
+  const int gs = grid_for((long long)P.batch * P.n, 256, h->sms);
+  // s = rbar1 + gamma G^T rbar2
+  gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, nullptr);
+  LAUNCH_CHECK();
+  h->launches++;
+  // z = K_gamma^-1 s ; r = G z - rbar2 ; p = r ; dy = 0
+  TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, nullptr));
+  dim3 gg(KKT_NPART, P.batch);
+  g_kernel<<<gg, 256, 0, h->stream>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0);
+  LAUNCH_CHECK();
+  h->launches++;
+  const int chunk = 8;
+  int it = 0;
+  while (it < maxit) {
+    int todo = std::min(chunk, maxit - it);
+    for (int q = 0; q < todo; q++) {
+      gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
+      LAUNCH_CHECK();
+      TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
+      g_kernel<<<gg, 256, 0, h->stream>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1);
+      LAUNCH_CHECK();
+      cg_update_kernel<<<gg, 256, 0, h->stream>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+                                                   rtol, h->status);
+      LAUNCH_CHECK();
+      cg_p_kernel<<<grid_for((long long)P.batch * P.m_eq, 256, h->sms), 256, 0, h->stream>>>(
+          P.batch, P.m_eq, h->cp, h->cr, h->C);
+      LAUNCH_CHECK();
+      h->launches += 4;
+    }
+    it += todo;
+    // host check of the per-instance convergence flags between chunks
+    CUDA_TRY(cudaMemcpyAsync(h->pinned_flags, h->C.cg_done, P.batch * sizeof(int),
+                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    bool all = true;
+    for (int b = 0; b < P.batch; b++) all = all && h->pinned_flags[b];
+    if (all) break;
+  }
+  cg_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->stream>>>(P.batch, h->C, first ? 1 : 0, h->status);
+  LAUNCH_CHECK();
+  // dx = K_gamma^-1 (s - G^T dy)
+  gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, dyo, -1.0, h->sg, h->wv, nullptr);
+  LAUNCH_CHECK();
+  TRY(launch_solve(h, h->wv, P.n, dxo, P.n, nullptr));
+  h->launches += 2;
+  return KKT_OK;
+}
+
+extern "C" kkt_status hykkt_solve(kkt_handle h, const double* rbar1, const double* rbar2, double* dx,
+                                  double* dy, double cg_rtol, int cg_maxit, int max_outer_refine) {
+  if (!h || !rbar1 || !dx) return KKT_ERR_ARG;
+  const Plan& P = h->P;
+  if (P.m_eq > 0 && (!rbar2 || !dy)) return KKT_ERR_ARG;
+  if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
+  if (cg_rtol <= 0) cg_rtol = 1e-12;
+  if (cg_maxit <= 0) cg_maxit = std::max(1, std::min(P.m_eq, 2000));
+  h->launches = 0;
+  if (P.m_eq == 0) return kkt_solve(h, rbar1, dx, max_outer_refine, 0.0);
+  TRY(hykkt_pass(h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, true));
+  const long long nn = (long long)P.batch * P.n, mm = (long long)P.batch * P.m_eq;
+  for (int k = 0; k < max_outer_refine; k++) {
+    // rho1 = rbar1 - K dx - G^T dy ; rho2 = rbar2 - G dx   (double-double, K without gamma rows)
+    TRY(launch_resid(h, dx, rbar1, 1, dy, rbar2, h->hr1, nullptr, nullptr));
+    CUDA_TRY(cudaMemcpyAsync(h->hr2, h->res2, mm * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    TRY(hykkt_pass(h, h->hr1, h->hr2, h->hdx, h->hdy, cg_rtol, cg_maxit, false));
+    axpy_kernel<<<grid_for(nn, 256, h->sms), 256, 0, h->stream>>>(nn, dx, h->hdx);
+    axpy_kernel<<<grid_for(mm, 256, h->sms), 256, 0, h->stream>>>(mm, dy, h->hdy);
+    LAUNCH_CHECK();
+    h->launches += 2;
+  }
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_sync_info(kkt_handle h, int* status, int* fail_col, int* refine_iters,
+                                    int* cg_iters, double* bwd_err) {
+  if (!h) return KKT_ERR_ARG;
+  if (!h->bound) { g_err = "not bound"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  int st = 0, fl = INT_MAX;
+  std::vector<int> it(P.batch), cg(P.batch);
+  std::vector<double> om(P.batch);
+  CUDA_TRY(cudaMemcpyAsync(&st, h->status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(&fl, h->fail, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(it.data(), h->C.refine_iters, P.batch * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(cg.data(), h->C.cg_iters_first, P.batch * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(om.data(), h->C.omega_last, P.batch * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  int zero = 0, big = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(h->status, &zero, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (fl != INT_MAX && st == 0) st = KKT_ERR_NOT_SPD;
+  if (status) *status = st;
+  if (fail_col) *fail_col = (fl != INT_MAX) ? P.perm[fl] : -1;
+  if (refine_iters) *refine_iters = *std::max_element(it.begin(), it.end());
+  if (cg_iters) *cg_iters = *std::max_element(cg.begin(), cg.end());
+  if (bwd_err) *bwd_err = *std::max_element(om.begin(), om.end());
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_step_host(kkt_handle h, const double* W_vals, const double* J_vals,
+                                    const double* Sigma_x, const double* Sigma_s, const double* D,
+                                    double delta_w, double delta_c, double gamma, const double* b,
+                                    double* x, int max_refine, double tol_bwd) {
+  if (!h || !b || !x || !Sigma_x) return KKT_ERR_ARG;
+  if (!h->bound) { g_err = "kkt_bind first"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  size_t B = P.batch;
+  if (!h->hb) {
+    CUDA_TRY(cudaMalloc(&h->hW, std::max<size_t>(1, B * P.nnzW) * 8));
+    CUDA_TRY(cudaMalloc(&h->hJ, std::max<size_t>(1, B * P.nnzJ) * 8));
+    CUDA_TRY(cudaMalloc(&h->hSx, B * P.n * 8));
+    CUDA_TRY(cudaMalloc(&h->hSs, std::max<size_t>(1, B * (P.m - P.m_eq)) * 8));
+    CUDA_TRY(cudaMalloc(&h->hD, std::max<size_t>(1, B * P.m) * 8));
+    CUDA_TRY(cudaMalloc(&h->hb, B * P.n * 8));
+    CUDA_TRY(cudaMalloc(&h->hx, B * P.n * 8));
+  }
+  cudaStream_t s = h->stream;
+  if (P.nnzW) CUDA_TRY(cudaMemcpyAsync(h->hW, W_vals, B * P.nnzW * 8, cudaMemcpyHostToDevice, s));
+  if (P.nnzJ) CUDA_TRY(cudaMemcpyAsync(h->hJ, J_vals, B * P.nnzJ * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(h->hSx, Sigma_x, B * P.n * 8, cudaMemcpyHostToDevice, s));
+  if (Sigma_s && P.m > P.m_eq)
+    CUDA_TRY(cudaMemcpyAsync(h->hSs, Sigma_s, B * (P.m - P.m_eq) * 8, cudaMemcpyHostToDevice, s));
+  if (D && P.m) CUDA_TRY(cudaMemcpyAsync(h->hD, D, B * P.m * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(h->hb, b, B * P.n * 8, cudaMemcpyHostToDevice, s));
+  TRY(kkt_condense(h, h->hW, h->hJ, h->hSx, h->hSs, D ? h->hD : nullptr, delta_w, delta_c, gamma));
+  TRY(kkt_factor(h));
+  TRY(kkt_solve(h, h->hb, h->hx, max_refine, tol_bwd));
+  CUDA_TRY(cudaMemcpyAsync(x, h->hx, B * P.n * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_get_condensed(kkt_handle h, int inst, int* Kp, int* Ki, double* Kv) {
+  if (!h) return KKT_ERR_ARG;
+  const Plan& P = h->P;
+  if (inst < 0 || inst >= P.batch) return KKT_ERR_ARG;
+  const int n = P.n, nnz = P.Kp[n];
+  std::vector<double> v(nnz);
+  if (Kv) {
+    if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
+    CUDA_TRY(cudaMemcpyAsync(v.data(), h->Kv + (size_t)inst * nnz, nnz * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  // internal (i, j) -> original lower (max, min), CSC sorted
+  std::vector<int> cnt(n + 1, 0);
+  for (int j = 0; j < n; j++)
+    for (int p = P.Kp[j]; p < P.Kp[j + 1]; p++) {
+      int a = P.perm[P.Ki[p]], c = P.perm[j];
+      cnt[std::min(a, c) + 1]++;
+    }
+  for (int j = 0; j < n; j++) cnt[j + 1] += cnt[j];
+  std::vector<std::pair<int, int>> ent(nnz);  // (row, internal p) per orig column slot
+  std::vector<int> f(cnt.begin(), cnt.end() - 1);
+  for (int j = 0; j < n; j++)
+    for (int p = P.Kp[j]; p < P.Kp[j + 1]; p++) {
+      int a = P.perm[P.Ki[p]], c = P.perm[j];
+      ent[f[std::min(a, c)]++] = {std::max(a, c), p};
+    }
+  for (int j = 0; j < n; j++) std::sort(ent.begin() + cnt[j], ent.begin() + cnt[j + 1]);
+  if (Kp) std::memcpy(Kp, cnt.data(), (n + 1) * sizeof(int));
+  for (int q = 0; q < nnz; q++) {
+    if (Ki) Ki[q] = ent[q].first;
+    if (Kv) Kv[q] = v[ent[q].second];
+  }
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
+  if (!h || !launches) return KKT_ERR_ARG;
+  *launches = h->launches;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_destroy(kkt_handle h) {
+  if (!h) return KKT_ERR_ARG;
+  if (h->bound) {
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->plan_mem) cudaFree(h->plan_mem);
+    if (h->ws_owned && h->ws) cudaFree(h->ws);
+    for (double* p : {h->hW, h->hJ, h->hSx, h->hSs, h->hD, h->hb, h->hx})
+      if (p) cudaFree(p);
+    if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
+  }
+  delete h;
+  return KKT_OK;
+}
