@@ -167,6 +167,12 @@ kkt_status kkt_step_host(kkt_handle h, const double *W_vals, const double *J_val
  * indices: [host] Kp[n+1], Ki[nnzK], Kv[nnzK] (any may be NULL).  Blocking. */
 kkt_status kkt_get_condensed(kkt_handle h, int inst, int *Kp, int *Ki, double *Kv);
 
+/* Supernode partition (internal postordered numbering): nsuper; and when
+ * non-NULL [host] sn_first[nsuper+1] (first column), sn_nrows[nsuper] (rows of the front),
+ * sn_parent[nsuper] (-1 = root).  Call with NULL arrays first to learn nsuper. */
+kkt_status kkt_get_supernodes(kkt_handle h, int *nsuper, int *sn_first, int *sn_nrows,
+                              int *sn_parent);
+
 /* Number of kernel launches the last per-iteration call enqueued (evidence counter). */
 kkt_status kkt_launch_count(kkt_handle h, long long *launches);
 

@@ -17,7 +17,8 @@ __global__ void refine_init_kernel(int batch, DevCtrl C) {
   C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
 }
 
-// Stopping rules (R9): omega <= tol; ||dx|| <= 2u ||x|| after the previous correction;
+// Stopping rules (R9): omega <= tol (only if tol > 0); ||dx|| <= 2u ||x|| after the previous
+// correction;
 // omega grew in two consecutive sweeps; last sweep (measurement only).
 __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep, int last) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -26,7 +27,7 @@ __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep
   double om = bits2d(C.omega[b]);
   C.omega[b] = 0ULL;
   C.omega_last[b] = om;
-  bool stop = last || !(om > tol);  // NaN -> stop
+  bool stop = last || isnan(om) || (tol > 0.0 && om <= tol);
   if (sweep > 0) {
     double dxn = bits2d(C.dxn[b]), xn = bits2d(C.xn[b]);
     C.dxn[b] = 0ULL; C.xn[b] = 0ULL;

@@ -417,7 +417,7 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   if (!h || !b || !x) return KKT_ERR_ARG;
   if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
   const Plan& P = h->P;
-  if (tol_bwd <= 0) tol_bwd = 1e-15;
+  if (tol_bwd < 0) tol_bwd = 0;  // 0 disables the backward-error stop (R9)
   max_refine = std::max(0, max_refine);
   h->launches = 0;
   int gb = (P.batch + 127) / 128;
@@ -610,6 +610,20 @@ extern "C" kkt_status kkt_get_condensed(kkt_handle h, int inst, int* Kp, int* Ki
     if (Ki) Ki[q] = ent[q].first;
     if (Kv) Kv[q] = v[ent[q].second];
   }
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_get_supernodes(kkt_handle h, int* nsuper, int* sn_first, int* sn_nrows,
+                                         int* sn_parent) {
+  if (!h) return KKT_ERR_ARG;
+  const Plan& P = h->P;
+  if (nsuper) *nsuper = P.ns;
+  for (int s = 0; s < P.ns; s++) {
+    if (sn_first) sn_first[s] = P.sn_first[s];
+    if (sn_nrows) sn_nrows[s] = P.sn_rp[s + 1] - P.sn_rp[s];
+    if (sn_parent) sn_parent[s] = P.sn_parent[s];
+  }
+  if (sn_first) sn_first[P.ns] = P.n;
   return KKT_OK;
 }
 

@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve",
-           "kkt_sync_info", "kkt_step_host", "kkt_get_condensed", "kkt_launch_count",
+           "kkt_sync_info", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_launch_count",
            "kkt_last_error", "kkt_destroy"]
 
 
@@ -78,6 +78,7 @@ def lib(build_if_missing: bool = True):
             "kkt_step_host": [P, P, P, P, P, P, D, D, D, P, P, I, D],
             "kkt_get_condensed": [P, I, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
+            "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
             "kkt_destroy": [P],
         }
         for name, args in sig.items():
@@ -184,6 +185,16 @@ def kkt_get_condensed(h, inst, n, nnzK, values=True):
     return Kp, Ki[:nnzK], (Kv[:nnzK] if values else None)
 
 
+def kkt_get_supernodes(h):
+    ns = C.c_int()
+    _chk(lib().kkt_get_supernodes(h, C.byref(ns), None, None, None), "kkt_get_supernodes")
+    f = np.zeros(ns.value + 1, np.int32); r = np.zeros(max(ns.value, 1), np.int32)
+    p = np.zeros(max(ns.value, 1), np.int32)
+    _chk(lib().kkt_get_supernodes(h, C.byref(ns), f.ctypes.data, r.ctypes.data, p.ctypes.data),
+         "kkt_get_supernodes")
+    return f, r[:ns.value], p[:ns.value]
+
+
 def kkt_launch_count(h):
     v = C.c_longlong()
     _chk(lib().kkt_launch_count(h, C.byref(v)), "kkt_launch_count")
@@ -245,6 +256,9 @@ class KKTSolver:
 
     def get_condensed(self, inst=0, values=True):
         return kkt_get_condensed(self.h, inst, self.n, int(self.info["nnzK"]), values)
+
+    def supernodes(self):
+        return kkt_get_supernodes(self.h)
 
     def launch_count(self):
         return kkt_launch_count(self.h)
