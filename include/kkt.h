@@ -173,6 +173,11 @@ kkt_status kkt_get_condensed(kkt_handle h, int inst, int *Kp, int *Ki, double *K
 kkt_status kkt_get_supernodes(kkt_handle h, int *nsuper, int *sn_first, int *sn_nrows,
                               int *sn_parent);
 
+/* Tracing (environment KKT_TRACE=1 at kkt_bind): [host] stamps[3][nsuper][8] = globaltimer
+ * (ns) start, end and checkpoints 2..7 of every supernode task of instance 0 in the last factor (row 0), forward
+ * (row 1) and backward (row 2) solve.  Blocking.  KKT_ERR_STATE when tracing is off. */
+kkt_status kkt_get_trace(kkt_handle h, long long *stamps);
+
 /* Number of kernel launches the last per-iteration call enqueued (evidence counter). */
 kkt_status kkt_launch_count(kkt_handle h, long long *launches);
 

@@ -479,6 +479,7 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
     P.sn_Up[s + 1] = P.sn_Up[s] + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
     P.sn_uvp[s + 1] = P.sn_uvp[s] + R;
   }
+  if (P.sn_uvp[ns] >= (1LL << 31)) { *code = 2; return "update vectors exceed int32 offsets"; }
   P.nnzL_stored = P.sn_Lp[ns];
   P.update_doubles = P.sn_Up[ns];
   P.uvec_doubles = P.sn_uvp[ns];
@@ -526,6 +527,48 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
   std::iota(P.order.begin(), P.order.end(), 0);
   std::stable_sort(P.order.begin(), P.order.end(),
                    [&](int a, int b) { return P.sn_level[a] < P.sn_level[b]; });
+
+  // small (warp) / big (CTA) split, closed under descendants
+  {
+    std::vector<char> big(ns, 0);
+    for (int s = 0; s < ns; s++) {
+      long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = snf[s + 1] - snf[s], R = r - w;
+      long long need = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
+      if (need > KKT_SCAP) big[s] = 1;
+    }
+    for (int s = 0; s < ns; s++)  // children precede parents
+      if (big[s] && P.sn_parent[s] >= 0) big[P.sn_parent[s]] = 1;
+    P.order_s.clear(); P.order_b.clear(); P.max_r_small = 0;
+    P.up_s.clear(); P.up_b.clear(); P.dn_b.clear(); P.dn_s.clear();
+    std::vector<int> nbigch(ns, 0);
+    for (int s = 0; s < ns; s++)
+      if (big[s] && P.sn_parent[s] >= 0) nbigch[P.sn_parent[s]]++;
+    for (int s = 0; s < ns; s++) {
+      int par = P.sn_parent[s];
+      bool leaf = P.sn_cp[s + 1] == P.sn_cp[s];
+      if (!big[s] && leaf) P.up_s.push_back(s);
+      if (big[s] && nbigch[s] == 0) P.up_b.push_back(s);
+      if (big[s] && par < 0) P.dn_b.push_back(s);
+      if (!big[s] && (par < 0 || big[par])) P.dn_s.push_back(s);
+    }
+    P.sn.resize(ns);
+    for (int s = 0; s < ns; s++) {
+      SnInfo& I = P.sn[s];
+      std::memset(&I, 0, sizeof(I));
+      I.f0 = snf[s]; I.w = snf[s + 1] - snf[s];
+      I.rp0 = P.sn_rp[s]; I.r = P.sn_rp[s + 1] - P.sn_rp[s];
+      I.par = P.sn_parent[s]; I.c0 = P.sn_cp[s]; I.c1 = P.sn_cp[s + 1]; I.big = big[s];
+      I.k0 = P.Kp[snf[s]]; I.k1 = P.Kp[snf[s + 1]];
+      I.Lp = P.sn_Lp[s]; I.Up = P.sn_Up[s]; I.uvp = (int)P.sn_uvp[s];
+    }
+    for (int s : P.order) {
+      if (big[s]) P.order_b.push_back(s);
+      else {
+        P.order_s.push_back(s);
+        P.max_r_small = std::max(P.max_r_small, P.sn_rp[s + 1] - P.sn_rp[s]);
+      }
+    }
+  }
 
   // ---------------- 6. condensation gather map ------------------------------------
   P.kw.assign(P.Kp[n], -1);

@@ -2,7 +2,7 @@
 // All reductions are deterministic: fixed per-block trees, partials summed in block order by
 // the last-arriving block (no floating-point atomics).
 #pragma once
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace kkt {
 

@@ -1,0 +1,158 @@
+// common.cuh -- shared device helpers of the sm_100a kernels of the condensed-KKT hot path (arXiv 2405.14236).
+//
+//   dweights_kernel   D_r in fp64 and double-double
+//   condense_kernel   K = W + D_x + dw I + J^T D J, gather per K entry
+//   factor_kernel     persistent multifrontal supernodal Cholesky           (§8(a) a2)
+//   fwd_kernel/bwd_kernel  persistent supernodal triangular solves         (a3)
+//   resid_rows/cols   double-double residual of the unassembled operator   (R8, a4)
+//   CG kernels        HyKKT Schur-complement CG on G K_gamma^-1 G^T         (a5)
+//
+// Determinism: no floating-point atomics anywhere; every sum has a fixed order, so results
+// are bitwise reproducible run to run and independent of the GPU count.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "devplan.h"
+
+namespace kkt {
+
+#define KKT_NT 128          // threads per CTA of the persistent kernels
+#define KKT_NPART 64        // reduction partials per instance
+
+// ------------------------------------------------------------------ memory-model helpers
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int ld_volatile(const int* p) {
+  int v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace stamps (instance 0 only): kind 0 = factor, 1 = forward, 2 = backward;
+// which 0 = start, 1 = end, 2..7 = intermediate checkpoints (KKT_TRACE_SLOTS per task)
+#define KKT_TRACE_SLOTS 8
+__device__ __forceinline__ void trace_stamp(const DevPlan& P, int kind, int s, int b, int which) {
+  if (P.trace && b == 0) P.trace[((long long)kind * P.ns + s) * KKT_TRACE_SLOTS + which] = gtimer();
+}
+// Coalesced global -> shared copy with KKT_MLP loads in flight per thread (the loads are issued
+// back to back before any store, so a copy of n elements costs ~ceil(n / (nt*KKT_MLP)) memory
+// round trips instead of ceil(n / nt)).  CG = bypass L1 (data produced in the same launch).
+#define KKT_MLP 8
+template <bool CG, class T>
+__device__ __forceinline__ void copy_g2s(T* dst, const T* src, int n, int tid, int nt) {
+  for (int base = tid; base < n; base += nt * KKT_MLP) {
+    T t[KKT_MLP];
+#pragma unroll
+    for (int u = 0; u < KKT_MLP; u++) {
+      const int q = base + u * nt;
+      if (q < n) t[u] = CG ? __ldcg(src + q) : __ldg(src + q);
+    }
+#pragma unroll
+    for (int u = 0; u < KKT_MLP; u++) {
+      const int q = base + u * nt;
+      if (q < n) dst[q] = t[u];
+    }
+  }
+}
+// producer data written earlier in the same launch by another CTA: bypass L1
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* a, double v) {
+  // non-negative doubles order like their bit patterns; NaN maps above +inf
+  unsigned long long b = isnan(v) ? 0x7ff8000000000000ULL : __double_as_longlong(v);
+  atomicMax(a, b);
+}
+
+// ------------------------------------------------------------------ double-double
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+  double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi), t = two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo + a.lo * b.hi;
+  return quick_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+  dd p = two_prod(a.hi, b);
+  p.lo = fma(a.lo, b, p.lo);
+  return quick_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+  double q1 = a.hi / b.hi;
+  dd r = dd_add(a, dd_mul_d(b, -q1));
+  double q2 = r.hi / b.hi;
+  r = dd_add(r, dd_mul_d(b, -q2));
+  double q3 = r.hi / b.hi;
+  dd q = quick_two_sum(q1, q2);
+  return dd_add(q, dd{q3, 0.0});
+}
+
+// =====================================================================================
+// Persistent-kernel task protocol.  Tasks are (supernode in level order, instance) pairs,
+// dequeued in increasing order with a global ticket; a task's dependencies always carry
+// smaller ticket numbers and are therefore held by running CTAs -> no deadlock for any grid
+// size.  Dependency counters are reset by their consumer; the ticket is reset by the last
+// CTA to exit (ctl[0] = ticket, ctl[1] = exit count).
+// =====================================================================================
+__device__ __forceinline__ int next_task(int* ctl, int* s_task) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_task = atomicAdd(ctl, 1);
+  __syncthreads();
+  return *s_task;
+}
+// ctl[0] = ticket/head, ctl[1] = exit count, ctl[2] = queue tail, ctl[3] = completed tasks;
+// the last worker to exit resets all four for the next launch (stream order publishes it).
+__device__ __forceinline__ void reset_ctl(int* ctl) {
+  ctl[0] = 0; ctl[1] = 0; ctl[2] = 0; ctl[3] = 0;
+  __threadfence();
+}
+__device__ __forceinline__ void persistent_exit(int* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    int e = atomicAdd(ctl + 1, 1);
+    if (e == (int)gridDim.x - 1) reset_ctl(ctl);
+  }
+}
+
+__device__ __forceinline__ long long upk(int i, int j, int R) {  // packed lower col-major
+  return (long long)j * R - (long long)j * (j - 1) / 2 + (i - j);
+}
+
+}  // namespace kkt

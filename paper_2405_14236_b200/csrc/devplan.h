@@ -4,13 +4,39 @@
 
 namespace kkt {
 
+// Per-warp front capacity (doubles) of the warp-per-supernode kernels.  A supernode is
+// "small" when every front in its subtree needs <= KKT_SCAP doubles (panel r*w plus packed
+// update matrix R(R+1)/2); small subtrees run one warp per supernode, the remaining top of the
+// tree ("big" supernodes) runs one CTA per supernode.  Small is closed under descendants, so
+// the small phase never waits on the big phase (bottom-up) and vice versa (top-down).
+constexpr int KKT_SCAP = 2048;
+constexpr int KKT_WPB = 4;      // warps per CTA in the warp-per-supernode kernels
+constexpr int KKT_BNT = 256;    // threads per CTA in the big-supernode kernels
+
+// Per-supernode metadata packed in 64 bytes so one broadcast load fetches it.
+struct alignas(16) SnInfo {
+  int f0, w, r, rp0;     // first column, width, front rows, offset into sn_rows
+  int par, c0, c1, big;  // parent (-1 root), children [c0,c1) in sn_ch, 1 = CTA phase
+  int k0, k1, uvp, pad;  // K entries of the supernode's columns [k0, k1); update-vector offset
+  long long Lp, Up;      // panel / update-matrix offsets
+};
+static_assert(sizeof(SnInfo) == 64, "SnInfo must be 64 bytes");
+
 struct DevPlan {
   int n, m, m_eq, nnzW, nnzJ, nnzK, ns, batch;
   int max_front;
+  int ns_s, ns_b;              // small / big supernode counts
+  int max_r_small;             // largest front among small supernodes
   long long nnzL_stored, update_doubles, uvec_doubles, nprod;
   const int *perm, *iperm;
   const int *Kp, *Ki, *kw, *kdiag, *pptr, *pa, *pb, *jrow, *kpos;
   const int *sn_first, *sn_rp, *sn_rows, *sn_rel, *sn_parent, *sn_cp, *sn_ch, *order;
+  const int *order_s, *order_b;  // level order restricted to small / big supernodes
+  const SnInfo* sn;              // [ns]
+  // ready lists of the spin-free schedulers
+  const int *up_s, *up_b, *dn_b, *dn_s;   // see plan.h
+  long long* trace;              // optional [3][ns][2] globaltimer stamps (KKT_TRACE=1), else NULL
+  int n_up_s, n_up_b, n_dn_b, n_dn_s;
   const long long *sn_Lp, *sn_Up, *sn_uvp;
   const int *Wf_p, *Wf_c, *Wf_k, *Jt_p, *Jt_r, *Jt_k, *Gt_end;
   const int *Jrp, *Jci;       // J CSR pattern (caller's, copied at analysis)

@@ -1,0 +1,239 @@
+// factor.cuh -- persistent multifrontal supernodal Cholesky, P K P^T = L L^T without pivoting
+// ("factorize it using sparse Cholesky").
+//
+// Front of supernode s (columns f0..f0+w, rows R_s with r = |R_s|, R = r - w):
+//   [F | U]:  F = panel r x w column-major (becomes L's columns),  U = packed lower R x R
+//   assembly:  F <- K(R_s, cols(s)) ; U <- 0 ; then for each child c (fixed order):
+//              extend-add U_c through the relative-index map rel_c       (deterministic)
+//   partial factorisation:  F11 = L11 L11^T, L21 = F21 L11^-T, U <- U - L21 L21^T
+//   U is kept for the parent; F is written to L.
+//
+// Phase 1 (factor_small_kernel): one WARP per supernode for the subtrees whose fronts fit
+//   KKT_SCAP doubles; the front lives in a per-warp shared-memory slice.
+// Phase 2 (factor_big_kernel): one CTA per remaining (top) supernode; front in shared memory
+//   when it fits, otherwise in global memory (L2) with a 64x64 register-tiled SYRK.
+#pragma once
+#include "dense.cuh"
+
+namespace kkt {
+
+__device__ __forceinline__ int warp_ticket(int* ctl) {
+  int t = 0;
+  if ((threadIdx.x & 31) == 0) t = atomicAdd(ctl, 1);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
+__device__ __forceinline__ void warp_exit(int* ctl, int nwarps_total) {
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    int e = atomicAdd(ctl + 1, 1);
+    if (e == nwarps_total - 1) reset_ctl(ctl);
+  }
+}
+
+
+// ------------------------------------------------------------------ front assembly
+// F, U may live in shared or global memory; `nt`/`tid` describe the cooperating group
+// (a warp: nt = 32, tid = lane; a CTA: nt = blockDim, tid = threadIdx).  The caller
+// synchronises the group between the zero/scatter/extend-add stages via `sync`.
+template <class Sync>
+__device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I, double* F,
+                                               double* U, long long usz,
+                                               const double* __restrict__ Kv, const double* Ub,
+                                               int tid, int nt, Sync sync) {
+  const int w = I.w, r = I.r, R = r - w;
+  const long long pw = (long long)r * w;
+  for (long long q = tid; q < pw; q += nt) F[q] = 0.0;
+  for (long long q = tid; q < usz; q += nt) U[q] = 0.0;
+  sync();
+  // K entries of the supernode's columns: batched loads, then scatter
+  for (int base = I.k0 + tid; base < I.k1; base += nt * KKT_MLP) {
+    int pos[KKT_MLP];
+    double val[KKT_MLP];
+#pragma unroll
+    for (int u = 0; u < KKT_MLP; u++) {
+      const int k = base + u * nt;
+      if (k < I.k1) { pos[u] = __ldg(P.kpos + k); val[u] = __ldg(Kv + k); }
+    }
+#pragma unroll
+    for (int u = 0; u < KKT_MLP; u++)
+      if (base + u * nt < I.k1) F[pos[u]] = val[u];
+  }
+  sync();
+  for (int ci = I.c0; ci < I.c1; ci++) {
+    const int c = __ldg(P.sn_ch + ci);
+    const SnInfo C = P.sn[c];
+    const int Rc = C.r - C.w;
+    const int* rel = P.sn_rel + C.rp0 + C.w;
+    const double* Uc = Ub + C.Up;
+    const long long tot = (long long)Rc * (Rc + 1) / 2;
+    // each member walks the packed child matrix with stride nt (monotone q -> incremental
+    // column decode); KKT_MLP entries are loaded before any is accumulated.  Positions within
+    // one child are distinct, so there are no conflicts; children are applied in order.
+    int jc = 0;
+    long long cs = 0;  // start of column jc
+    for (long long base = tid; base < tot; base += (long long)nt * KKT_MLP) {
+      int pi[KKT_MLP], pj[KKT_MLP];
+      double v[KKT_MLP];
+#pragma unroll
+      for (int u = 0; u < KKT_MLP; u++) {
+        const long long q = base + (long long)u * nt;
+        if (q < tot) {
+          while (q >= cs + (Rc - jc)) { cs += Rc - jc; jc++; }
+          const int ic = jc + (int)(q - cs);
+          pj[u] = __ldg(rel + jc);
+          pi[u] = __ldg(rel + ic);
+          v[u] = ldcg(Uc + q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KKT_MLP; u++) {
+        if (base + (long long)u * nt < tot) {
+          if (pj[u] < w) F[(long long)pj[u] * r + pi[u]] += v[u];
+          else U[upk(pi[u] - w, pj[u] - w, R)] += v[u];
+        }
+      }
+    }
+    sync();
+  }
+}
+
+// =====================================================================================
+// Spin-free scheduling (bottom-up).  Workers take tasks only from a static ready list
+// (leaves); when a worker finishes supernode s it increments its parent's counter with an
+// acq_rel atomic, and the LAST child to finish continues with the parent itself.  No worker
+// ever waits on a dependency.  Phase 1 (small, warps) stops at a big parent (it only counts);
+// phase 2 (big, CTAs) starts from the big supernodes without big children, whose counters
+// phase 1 already completed (reset on entry).
+// =====================================================================================
+__device__ __forceinline__ bool warp_signal_parent(const SnInfo& I, const SnInfo& Ip, int* cnt,
+                                                   int lane, bool phase_small) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    if (phase_small && Ip.big) {
+      red_release_add(cnt + I.par, 1);
+    } else {
+      const int old = atom_add_acq_rel(cnt + I.par, 1);
+      last = (old == Ip.c1 - Ip.c0 - 1);
+      if (last) cnt[I.par] = 0;
+    }
+  }
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+__global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, const double* __restrict__ Kv_all,
+                                                                    double* Lx_all, double* U_all, double* Dv_all,
+                                                                    int* cnt_all, int* ctl, int* fail_all) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* region = sm + (long long)wid * KKT_SCAP;
+  const int ninit = P.n_up_s * P.batch;
+  auto wsync = [] { __syncwarp(); };
+  for (;;) {
+    const int t = warp_ticket(ctl);
+    if (t >= ninit) break;
+    const int b = t % P.batch;
+    int s = __ldg(P.up_s + t / P.batch);
+    int* cnt = cnt_all + (long long)b * P.ns;
+    double* Lx = Lx_all + (long long)b * P.nnzL_stored;
+    double* Ub = U_all + (long long)b * P.update_doubles;
+    const double* Kv = Kv_all + (long long)b * P.nnzK;
+    for (;;) {
+      if (lane == 0) trace_stamp(P, 0, s, b, 0);
+      const SnInfo I = P.sn[s];
+      const int R = I.r - I.w;
+      const long long usz = I.par >= 0 ? (long long)R * (R + 1) / 2 : 0;
+      double* F = region;
+      double* U = region + I.r * I.w;
+      assemble_front(P, I, F, U, usz, Kv, Ub, lane, 32, wsync);
+      if (lane == 0) trace_stamp(P, 0, s, b, 2);
+      int fk = -1;
+      front_factor_warp(F, U, I.r, I.w, lane, Dv_all + (long long)b * P.n + I.f0, &fk);
+      if (lane == 0) trace_stamp(P, 0, s, b, 3);
+      double* Lg = Lx + I.Lp;
+      for (int q = lane; q < I.r * I.w; q += 32) Lg[q] = F[q];
+      if (usz) {
+        double* Ug = Ub + I.Up;
+        for (int q = lane; q < usz; q += 32) Ug[q] = U[q];
+      }
+      if (lane == 0 && fk >= 0) atomicMin(fail_all, I.f0 + fk);
+      if (lane == 0) trace_stamp(P, 0, s, b, 1);
+      if (I.par < 0) break;
+      const SnInfo Ip = P.sn[I.par];
+      if (!warp_signal_parent(I, Ip, cnt, lane, true)) break;
+      s = I.par;
+    }
+  }
+  warp_exit(ctl, gridDim.x * KKT_WPB);
+}
+
+// =====================================================================================
+// Phase 2: one CTA per big supernode (continuation scheduling, see above).
+// =====================================================================================
+__global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const double* __restrict__ Kv_all,
+                                                             double* Lx_all, double* U_all, double* Dv_all,
+                                                             int* cnt_all, int* ctl, int* fail_all,
+                                                             long long smem_cap) {
+  extern __shared__ double sm[];
+  __shared__ int s_task, s_fail, s_last;
+  const int tid = threadIdx.x;
+  const int ninit = P.n_up_b * P.batch;
+  auto bsync = [] { __syncthreads(); };
+  for (;;) {
+    const int t = next_task(ctl, &s_task);
+    if (t >= ninit) break;
+    const int b = t % P.batch;
+    int s = __ldg(P.up_b + t / P.batch);
+    int* cnt = cnt_all + (long long)b * P.ns;
+    double* Lx = Lx_all + (long long)b * P.nnzL_stored;
+    double* Ub = U_all + (long long)b * P.update_doubles;
+    const double* Kv = Kv_all + (long long)b * P.nnzK;
+    if (tid == 0) cnt[s] = 0;  // completed by phase-1 children
+    for (;;) {
+      if (tid == 0) trace_stamp(P, 0, s, b, 0);
+      const SnInfo I = P.sn[s];
+      const int r = I.r, w = I.w, R = r - w;
+      if (tid == 0) s_fail = -1;
+      __syncthreads();
+      const long long pw = (long long)r * w;
+      const long long usz = (I.par >= 0) ? (long long)R * (R + 1) / 2 : 0;
+      const bool in_smem = (pw + usz) <= smem_cap;
+      double* F = in_smem ? sm : Lx + I.Lp;
+      double* U = in_smem ? sm + pw : (usz ? Ub + I.Up : nullptr);
+      assemble_front(P, I, F, U, usz, Kv, Ub, tid, blockDim.x, bsync);
+      if (tid == 0) trace_stamp(P, 0, s, b, 2);
+      double* dv = Dv_all + (long long)b * P.n + I.f0;
+      if (in_smem) front_factor_cta<8>(F, U, r, w, dv, &s_fail);
+      else front_factor_cta<8>(F, U, r, w, dv, &s_fail);
+      __syncthreads();
+      if (tid == 0) trace_stamp(P, 0, s, b, 3);
+      if (tid == 0) trace_stamp(P, 0, s, b, 4);
+      if (in_smem) {
+        double* Lg = Lx + I.Lp;
+        for (long long q = tid; q < pw; q += blockDim.x) Lg[q] = F[q];
+        if (usz) {
+          double* Ug = Ub + I.Up;
+          for (long long q = tid; q < usz; q += blockDim.x) Ug[q] = U[q];
+        }
+      }
+      if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
+      if (tid == 0) trace_stamp(P, 0, s, b, 1);
+      if (I.par < 0) break;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const SnInfo Ip = P.sn[I.par];
+        const int old = atom_add_acq_rel(cnt + I.par, 1);
+        s_last = (old == Ip.c1 - Ip.c0 - 1);
+        if (s_last) cnt[I.par] = 0;
+      }
+      __syncthreads();
+      if (!s_last) break;
+      s = I.par;
+    }
+  }
+  persistent_exit(ctl);
+}
+
+}  // namespace kkt

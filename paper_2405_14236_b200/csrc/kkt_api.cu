@@ -6,13 +6,17 @@
 #include <chrono>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/kkt.h"
 #include "cg_kernels.cuh"
-#include "kernels.cuh"
+#include "condense.cuh"
+#include "factor.cuh"
+#include "resid.cuh"
+#include "trsv.cuh"
 #include "plan.h"
 
 using namespace kkt;
@@ -50,12 +54,14 @@ struct kkt_plan {
   void* ws = nullptr;
   bool ws_owned = false;
   size_t ws_bytes = 0;
+  double *Dv = nullptr;
   double *Kv = nullptr, *Lx = nullptr, *Ub = nullptr, *uv = nullptr, *Y = nullptr, *Xp = nullptr;
   double *Dh = nullptr, *Dl = nullptr, *A = nullptr, *res = nullptr, *dxv = nullptr, *res2 = nullptr;
   double2* T = nullptr;
   double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
-  int *fcnt = nullptr, *bflag = nullptr, *facnt = nullptr, *ctl = nullptr, *fail = nullptr,
+  TaskQueue TQ{};
+  int *fcnt = nullptr, *facnt = nullptr, *ctl = nullptr, *fail = nullptr,
       *status = nullptr;
   DevCtrl C{};
   // current values (remembered by kkt_condense for the refinement residual)
@@ -64,13 +70,14 @@ struct kkt_plan {
   bool condensed = false, factored = false;
   // launch configuration
   long long factor_smem_cap = 0;
-  int factor_smem = 0, fwd_smem = 0, bwd_smem = 0;
-  int grid_factor = 1, grid_fwd = 1, grid_bwd = 1;
+  int fsmall_smem = 0, fbig_smem = 0, tsmall_smem = 0, tbig_smem = 0, pcap = 0;
+  int g_fsmall = 1, g_fbig = 1, g_tsmall = 1, g_tbig = 1, g_bsmall = 1, g_bbig = 1;
   long long launches = 0;
   // host-buffer path (kkt_step_host)
   double *hW = nullptr, *hJ = nullptr, *hSx = nullptr, *hSs = nullptr, *hD = nullptr,
          *hb = nullptr, *hx = nullptr;
   int* pinned_flags = nullptr;
+  long long* trace_buf = nullptr;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -95,6 +102,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->Ub = c.take<double>(B * P.update_doubles);
   h->uv = c.take<double>(B * P.uvec_doubles);
   h->Y = c.take<double>(B * n);
+  h->Dv = c.take<double>(B * n);
   h->Xp = c.take<double>(B * n);
   h->res = c.take<double>(B * n);
   h->dxv = c.take<double>(B * n);
@@ -114,9 +122,10 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->hdy = c.take<double>(B * me);
   h->hr2 = c.take<double>(B * me);
   h->fcnt = c.take<int>(B * ns);
-  h->bflag = c.take<int>(B * ns);
+  h->TQ.q = c.take<int>(B * ns);
+  h->TQ.flag = c.take<int>(B * ns);
   h->facnt = c.take<int>(B * ns);
-  h->ctl = c.take<int>(8);
+  h->ctl = c.take<int>(32);
   h->fail = c.take<int>(1);
   h->status = c.take<int>(1);
   h->C.done = c.take<int>(B);
@@ -255,12 +264,14 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   const std::vector<int>* iv[] = {&P.perm, &P.iperm, &P.Kp, &P.Ki, &P.kw, &P.kdiag, &P.pptr,
                                   &P.pa, &P.pb, &P.jrow, &P.kpos, &P.sn_first, &P.sn_rp,
                                   &P.sn_rows, &P.sn_rel, &P.sn_parent, &P.sn_cp, &P.sn_ch,
-                                  &P.order, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
+                                  &P.order, &P.order_s, &P.order_b, &P.up_s, &P.up_b,
+                                  &P.dn_b, &P.dn_s, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
                                   &P.Jt_k, &P.Gt_end, &Jrp, &Jci};
   const std::vector<long long>* lv[] = {&P.sn_Lp, &P.sn_Up, &P.sn_uvp};
   size_t tot = 0;
   for (auto* v : iv) tot += vbytes(*v);
   for (auto* v : lv) tot += vbytes(*v);
+  tot += vbytes(P.sn);
   CUDA_TRY(cudaMalloc(&h->plan_mem, tot));
   std::vector<const void*> dptr;
   size_t off = 0;
@@ -275,9 +286,15 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     dptr.push_back(base + off);
     off += vbytes(*v);
   }
+  if (!P.sn.empty()) CUDA_TRY(cudaMemcpy(base + off, P.sn.data(), P.sn.size() * sizeof(SnInfo), cudaMemcpyHostToDevice));
+  const SnInfo* d_sn = (const SnInfo*)(base + off);
+  off += vbytes(P.sn);
   DevPlan& d = h->dp;
   d.n = P.n; d.m = P.m; d.m_eq = P.m_eq; d.nnzW = P.nnzW; d.nnzJ = P.nnzJ; d.nnzK = P.Kp[P.n];
   d.ns = P.ns; d.batch = P.batch; d.max_front = P.max_front;
+  d.ns_s = (int)P.order_s.size(); d.ns_b = (int)P.order_b.size(); d.max_r_small = P.max_r_small;
+  d.n_up_s = (int)P.up_s.size(); d.n_up_b = (int)P.up_b.size();
+  d.n_dn_b = (int)P.dn_b.size(); d.n_dn_s = (int)P.dn_s.size();
   d.nnzL_stored = P.nnzL_stored; d.update_doubles = P.update_doubles;
   d.uvec_doubles = P.uvec_doubles; d.nprod = P.nprod;
   int k = 0;
@@ -285,11 +302,19 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   d.perm = I(); d.iperm = I(); d.Kp = I(); d.Ki = I(); d.kw = I(); d.kdiag = I(); d.pptr = I();
   d.pa = I(); d.pb = I(); d.jrow = I(); d.kpos = I(); d.sn_first = I(); d.sn_rp = I();
   d.sn_rows = I(); d.sn_rel = I(); d.sn_parent = I(); d.sn_cp = I(); d.sn_ch = I();
-  d.order = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
+  d.order = I(); d.order_s = I(); d.order_b = I(); d.up_s = I(); d.up_b = I(); d.dn_b = I();
+  d.dn_s = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
   d.Jt_k = I(); d.Gt_end = I(); d.Jrp = I(); d.Jci = I();
   d.sn_Lp = (const long long*)dptr[k++];
   d.sn_Up = (const long long*)dptr[k++];
   d.sn_uvp = (const long long*)dptr[k++];
+  d.sn = d_sn;
+  d.trace = nullptr;
+  if (getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
+    CUDA_TRY(cudaMalloc(&h->trace_buf, (size_t)3 * std::max(P.ns, 1) * KKT_TRACE_SLOTS * sizeof(long long)));
+    CUDA_TRY(cudaMemset(h->trace_buf, 0, (size_t)3 * std::max(P.ns, 1) * KKT_TRACE_SLOTS * sizeof(long long)));
+    d.trace = h->trace_buf;
+  }
   // ---- workspace ----
   size_t need;
   kkt_workspace_size(h, &need);
@@ -309,27 +334,42 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   // ---- launch configuration ----
   long long maxneed = 0;
-  for (int s = 0; s < P.ns; s++) {
+  for (int s : P.order_b) {
     long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = P.sn_first[s + 1] - P.sn_first[s], R = r - w;
     long long need_s = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
     maxneed = std::max(maxneed, need_s);
   }
-  const long long cap_bytes = 96 * 1024;
+  const long long cap_bytes = 200 * 1024;
   h->factor_smem_cap = std::min(maxneed, cap_bytes / 8);
-  h->factor_smem = (int)(h->factor_smem_cap * 8);
-  h->fwd_smem = (int)((P.max_front + 64 * 64) * 8);
-  h->bwd_smem = (int)((2 * P.max_front + 64 * 64) * 8);
-  CUDA_TRY(cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(h->factor_smem, 1)));
-  CUDA_TRY(cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fwd_smem));
-  CUDA_TRY(cudaFuncSetAttribute(bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->bwd_smem));
-  int occ = 0;
-  long long tasks = (long long)P.ns * P.batch;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_kernel, KKT_NT, h->factor_smem));
-  h->grid_factor = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_kernel, KKT_NT, h->fwd_smem));
-  h->grid_fwd = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bwd_kernel, KKT_NT, h->bwd_smem));
-  h->grid_bwd = (int)std::max(1LL, std::min(tasks, (long long)occ * h->sms));
+  h->fbig_smem = (int)(std::max<long long>(h->factor_smem_cap, 1) * 8);
+  h->fsmall_smem = KKT_WPB * KKT_SCAP * 8;
+  h->tsmall_smem = KKT_WPB * (KKT_SCAP + P.max_r_small) * 8;
+  long long maxpanel = 0;
+  for (int s : P.order_b)
+    maxpanel = std::max(maxpanel, (long long)(P.sn_rp[s + 1] - P.sn_rp[s]) * (P.sn_first[s + 1] - P.sn_first[s]));
+  h->pcap = (int)std::min<long long>(maxpanel, 20000);
+  h->tbig_smem = (int)((P.max_front + 64 * 64 + h->pcap) * 8);
+  CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fsmall_smem));
+  CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
+  CUDA_TRY(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
+  CUDA_TRY(cudaFuncSetAttribute(bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
+  CUDA_TRY(cudaFuncSetAttribute(fwd_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tbig_smem));
+  CUDA_TRY(cudaFuncSetAttribute(bwd_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tbig_smem));
+  auto grid_of = [&](auto kern, int threads, int smem, long long tasks_, int per_cta, int* out) -> cudaError_t {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    long long ctas = (tasks_ + per_cta - 1) / per_cta;
+    *out = (int)std::max(1LL, std::min(ctas, (long long)std::max(occ, 1) * h->sms));
+    return e;
+  };
+  const long long us = (long long)P.up_s.size() * P.batch, ub = (long long)P.up_b.size() * P.batch;
+  const long long ts = (long long)P.order_s.size() * P.batch, tb = (long long)P.order_b.size() * P.batch;
+  CUDA_TRY(grid_of(factor_small_kernel, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
+  CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
+  CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
+  CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, ub, 1, &h->g_tbig));
+  CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
+  CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->bound = true;
@@ -373,10 +413,19 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
 extern "C" kkt_status kkt_factor(kkt_handle h) {
   if (!h) return KKT_ERR_ARG;
   if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
-  factor_kernel<<<h->grid_factor, KKT_NT, h->factor_smem, h->stream>>>(
-      h->dp, h->Kv, h->Lx, h->Ub, h->facnt, h->ctl + 0, h->fail, h->factor_smem_cap);
-  LAUNCH_CHECK();
-  h->launches++;
+  const Plan& P = h->P;
+  if (!P.order_s.empty()) {
+    factor_small_kernel<<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->stream>>>(
+        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0, h->fail);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  if (!P.order_b.empty()) {
+    factor_big_kernel<<<h->g_fbig, KKT_BNT, h->fbig_smem, h->stream>>>(
+        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 4, h->fail, h->factor_smem_cap);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
   h->factored = true;
   return KKT_OK;
 }
@@ -384,13 +433,28 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
 // forward + backward solve of all batch instances: xout = K^-1 rhs
 static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, double* xout,
                                long long xs, const int* done) {
-  fwd_kernel<<<h->grid_fwd, KKT_NT, h->fwd_smem, h->stream>>>(h->dp, h->Lx, rhs, rs, h->Y, h->uv,
-                                                               h->fcnt, h->ctl + 2, done);
-  LAUNCH_CHECK();
-  bwd_kernel<<<h->grid_bwd, KKT_NT, h->bwd_smem, h->stream>>>(h->dp, h->Lx, h->Y, h->Xp, xout, xs,
-                                                               h->bflag, h->ctl + 4, done);
-  LAUNCH_CHECK();
-  h->launches += 2;
+  const Plan& P = h->P;
+  if (!P.order_s.empty()) {
+    fwd_small_kernel<<<h->g_tsmall, KKT_WPB * 32, h->tsmall_smem, h->stream>>>(
+        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 8, done);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  if (!P.order_b.empty()) {
+    fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->stream>>>(
+        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 12, done, h->pcap);
+    LAUNCH_CHECK();
+    bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->stream>>>(
+        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 16, done, h->pcap);
+    LAUNCH_CHECK();
+    h->launches += 2;
+  }
+  if (!P.order_s.empty()) {
+    bwd_small_kernel<<<h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->stream>>>(
+        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 20, done);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
   return KKT_OK;
 }
 
@@ -627,6 +691,14 @@ extern "C" kkt_status kkt_get_supernodes(kkt_handle h, int* nsuper, int* sn_firs
   return KKT_OK;
 }
 
+extern "C" kkt_status kkt_get_trace(kkt_handle h, long long* stamps) {
+  if (!h || !stamps) return KKT_ERR_ARG;
+  if (!h->trace_buf) { g_err = "tracing disabled: set KKT_TRACE=1 before kkt_bind"; return KKT_ERR_STATE; }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaMemcpy(stamps, h->trace_buf, (size_t)3 * h->P.ns * KKT_TRACE_SLOTS * sizeof(long long), cudaMemcpyDeviceToHost));
+  return KKT_OK;
+}
+
 extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
   if (!h || !launches) return KKT_ERR_ARG;
   *launches = h->launches;
@@ -643,6 +715,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
     for (double* p : {h->hW, h->hJ, h->hSx, h->hSs, h->hD, h->hb, h->hx})
       if (p) cudaFree(p);
     if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
+    if (h->trace_buf) cudaFree(h->trace_buf);
   }
   delete h;
   return KKT_OK;

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include "devplan.h"
+
 namespace kkt {
 
 struct Plan {
@@ -49,6 +51,13 @@ struct Plan {
   std::vector<int> sn_cp, sn_ch; // children lists (CSR)
   std::vector<int> sn_level;     // 0 = leaf
   std::vector<int> order;        // task order: (level, s) ascending
+  std::vector<int> order_s, order_b;  // small / big supernodes (devplan.h KKT_SCAP), level order
+  int max_r_small = 0;
+  // Ready lists (spin-free scheduling, see factor.cuh):
+  //   up_s: small leaves (phase-1 bottom-up start);  up_b: big supernodes with no big child
+  //   dn_b: big roots (phase-1 top-down start);      dn_s: small roots + small children of big
+  std::vector<int> up_s, up_b, dn_b, dn_s;
+  std::vector<SnInfo> sn;
   std::vector<int> kpos;         // per K entry: offset inside its supernode's panel
   std::vector<int> col_sn;       // internal column -> supernode
   int height = 0, max_front = 0;

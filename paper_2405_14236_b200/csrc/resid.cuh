@@ -1,0 +1,92 @@
+// resid.cuh -- double-double residual of the unassembled operator (R8).
+#pragma once
+#include "common.cuh"
+
+namespace kkt {
+
+// =====================================================================================
+// Double-double residual of the unassembled operator (R8), two passes.
+//   rows:  t_r = D_r (J_r x)  (dd)          [mode 1 (saddle): rows r < m_eq carry t_r = dy_r
+//                                             and res2_r = rbar2_r - J_r x]
+//          a_r = |D_r| (|J_r| |x|)           (fp64, for the componentwise denominator)
+//   cols:  y_i = (W x)_i + (Sx_i + dw) x_i + sum_r J_ri t_r   (dd);  res_i = b_i - y_i
+//          omega = max_i |res_i| / (|W||x| + |Sx+dw||x| + |J|^T a + |b|)_i
+// =====================================================================================
+__global__ void resid_rows_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ Dh,
+                                  const double* __restrict__ Dl, const double* __restrict__ x,
+                                  long long xs, int mode, const double* __restrict__ dy,
+                                  const double* __restrict__ rb2, double* res2, double2* T,
+                                  double* A, const int* __restrict__ done) {
+  long long total = (long long)P.batch * P.m;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(idx / P.m), r = (int)(idx % P.m);
+    if (done && done[b]) continue;
+    const double* J = Jv + (long long)b * P.nnzJ;
+    const double* xb = x + (long long)b * xs;
+    int p0 = P.Jrp[r], p1 = P.Jrp[r + 1];
+    dd acc = {0.0, 0.0};
+    double aa = 0.0;
+    for (int p = p0; p < p1; p++) {
+      double jv = J[p], xv = xb[P.Jci[p]];
+      acc = dd_add(acc, two_prod(jv, xv));
+      aa = fma(fabs(jv), fabs(xv), aa);
+    }
+    if (mode == 1 && r < P.m_eq) {
+      T[idx] = make_double2(dy[(long long)b * P.m_eq + r], 0.0);
+      A[idx] = fabs(dy[(long long)b * P.m_eq + r]);
+      dd rr = dd_add(dd{rb2[(long long)b * P.m_eq + r], 0.0}, dd{-acc.hi, -acc.lo});
+      res2[(long long)b * P.m_eq + r] = rr.hi + rr.lo;
+    } else {
+      dd D = {Dh[idx], Dl[idx]};
+      dd t = dd_mul(acc, D);
+      T[idx] = make_double2(t.hi, t.lo);
+      A[idx] = fabs(D.hi) * aa;
+    }
+  }
+}
+
+__global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, const double* __restrict__ Jv,
+                                  const double* __restrict__ Sx, double dw, const double* __restrict__ x,
+                                  long long xs, const double* __restrict__ rhs, long long rs,
+                                  const double2* __restrict__ T, const double* __restrict__ A,
+                                  double* res, unsigned long long* omega, const int* __restrict__ done) {
+  long long total = (long long)P.batch * P.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(idx / P.n), i = (int)(idx % P.n);
+    if (done && done[b]) continue;
+    const double* W = Wv + (long long)b * P.nnzW;
+    const double* J = Jv + (long long)b * P.nnzJ;
+    const double* xb = x + (long long)b * xs;
+    const double2* Tb = T + (long long)b * P.m;
+    const double* Ab = A + (long long)b * P.m;
+    double xi = xb[i];
+    dd s = two_sum(Sx[idx], dw);
+    dd y = dd_mul_d(s, xi);
+    double den = fabs(s.hi) * fabs(xi);
+    for (int p = P.Wf_p[i]; p < P.Wf_p[i + 1]; p++) {
+      double wv = W[P.Wf_k[p]], xv = xb[P.Wf_c[p]];
+      y = dd_add(y, two_prod(wv, xv));
+      den = fma(fabs(wv), fabs(xv), den);
+    }
+    for (int p = P.Jt_p[i]; p < P.Jt_p[i + 1]; p++) {
+      int r = P.Jt_r[p];
+      double jv = J[P.Jt_k[p]];
+      double2 t = Tb[r];
+      y = dd_add(y, dd_mul_d(dd{t.x, t.y}, jv));
+      den = fma(fabs(jv), Ab[r], den);
+    }
+    double bi = rhs[(long long)b * rs + i];
+    dd rr = dd_add(dd{bi, 0.0}, dd{-y.hi, -y.lo});
+    double rv = rr.hi + rr.lo;
+    res[idx] = rv;
+    den += fabs(bi);
+    if (omega) {
+      double om = (den > 0.0) ? fabs(rv) / den : (rv != 0.0 ? INFINITY : 0.0);
+      atomic_max_pos(omega + b, om);
+    }
+  }
+}
+
+}  // namespace kkt

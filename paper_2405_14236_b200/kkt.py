@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve",
-           "kkt_sync_info", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_launch_count",
+           "kkt_sync_info", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
            "kkt_last_error", "kkt_destroy"]
 
 
@@ -79,6 +79,7 @@ def lib(build_if_missing: bool = True):
             "kkt_get_condensed": [P, I, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
+            "kkt_get_trace": [P, P],
             "kkt_destroy": [P],
         }
         for name, args in sig.items():
@@ -195,6 +196,12 @@ def kkt_get_supernodes(h):
     return f, r[:ns.value], p[:ns.value]
 
 
+def kkt_get_trace(h, ns):
+    t = np.zeros((3, max(ns, 1), 8), np.int64)
+    _chk(lib().kkt_get_trace(h, t.ctypes.data), "kkt_get_trace")
+    return t[:, :ns]
+
+
 def kkt_launch_count(h):
     v = C.c_longlong()
     _chk(lib().kkt_launch_count(h, C.byref(v)), "kkt_launch_count")
@@ -259,6 +266,9 @@ class KKTSolver:
 
     def supernodes(self):
         return kkt_get_supernodes(self.h)
+
+    def trace(self):
+        return kkt_get_trace(self.h, int(self.info["nsuper"]))
 
     def launch_count(self):
         return kkt_launch_count(self.h)
