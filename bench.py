@@ -9,6 +9,8 @@ are re-drawn every step (successive IPM iterations on a fixed pattern, SURVEY §
 Inputs are resident in HBM; L2 is flushed (256 MiB write) before every timed step and the
 flush is outside the per-step CUDA-event window.  N > 1 (torchrun): every rank solves its own
 instance (weak scaling, no data-path collective); value = max-over-ranks time / (N * K).
+--workload C5: the 512-instance batch is partitioned over the ranks (strong scaling) and x is
+gathered with NCCL at the end of every step; value = max-over-ranks time per batch iteration.
 
 --impl reference times the CPU oracle (oracle/, plain C, __float128) on the same workload --
 there is no installable reference implementation for this paper.
@@ -46,9 +48,18 @@ def parse():
     return ap.parse_args()
 
 
-def workload(name, rank=0, redraw=0):
-    from synth.generator import make_config, redraw_values
-    inst = make_config(name, instance=0)
+C5_TOTAL = 512
+
+
+def workload(name, rank=0, redraw=0, world=1):
+    """Instance(s) of rank `rank`.  C5: the rank's contiguous block of the 512-instance batch
+    (instance k draws its values from seed 5000 + k (+1000 per redraw), so every partition
+    reproduces the same instances).  Others: one instance per rank (weak scaling)."""
+    from synth.generator import make_config, redraw_values, partition
+    if name == "C5":
+        a, b = partition(C5_TOTAL, world, rank)
+        return make_config("C5", instance=a + 1000 * redraw, batch=b - a)
+    inst = make_config(name, instance=rank)
     if redraw:
         inst = redraw_values(inst, 100000 * (rank + 1) + redraw)
     return inst
@@ -142,15 +153,21 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     inst = workload(args.workload)
+    if inst.batch > 1:
+        inst = inst.instance(0)
     import oracle  # noqa: F401
     _, _, sym = oracle_time(inst, 0.0)         # analysis once (untimed)
     for _ in range(args.warmup):
         pass
     t0 = time.perf_counter()
     ms_each = []
+    nb = C5_TOTAL if args.workload == "C5" else 1
     for k in range(args.steps):
-        ms, cnt, _ = oracle_time(workload(args.workload, 0, 1 + k % args.nvalues), 0.0, sym)
-        ms_each.append(ms)
+        it = workload(args.workload, 0, 1 + k % args.nvalues)
+        if it.batch > 1:
+            it = it.instance(k % it.batch)
+        ms, cnt, _ = oracle_time(it, 0.0, sym)
+        ms_each.append(ms * nb)        # C5: one batch iteration = 512 instance solves
     total = time.perf_counter() - t0
     v = float(np.mean(ms_each))
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -161,12 +178,26 @@ def run_reference(args, rank, world):
            "impl": "reference",
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                             "sample": f"{args.steps} full oracle IPM iterations (condense + "
-                                      f"Cholesky + __float128-refined solve), {total:.1f} s"},
+                                      f"Cholesky + __float128-refined solve){' x 512 (one instance timed per step, scaled)' if nb > 1 else ''}, {total:.1f} s"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 # ------------------------------------------------------------------------------ ours
+def algorithmic_work(S, inst, refine_iters):
+    """SURVEY §8(d) algorithmic work per instance."""
+    n, m, nnzW, nnzJ = inst.n, inst.m, inst.nnzW, inst.nnzJ
+    nnzK, nnzL = int(S.info["nnzK"]), int(S.info["nnzL"])
+    condense_bytes = 8 * (nnzW + nnzJ + n + m) + 8 * nnzK
+    trsv_bytes = 16 * nnzL + 24 * n
+    resid_bytes = 24 * nnzW + 24 * nnzJ + 8 * (2 * n + m)
+    pairs = 1 + refine_iters
+    solve_bytes = pairs * trsv_bytes + (refine_iters + 1) * resid_bytes
+    return dict(condense_bytes=condense_bytes, factor_flops=float(S.info["flops"]),
+                trsv_bytes=trsv_bytes, resid_bytes=resid_bytes, solve_bytes=solve_bytes,
+                trsv_pairs=pairs)
+
+
 def run_ours(args, rank, world):
     import torch
     import paper_2405_14236_b200 as K
@@ -178,21 +209,29 @@ def run_ours(args, rank, world):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    inst = workload(args.workload, rank)
+    batched = args.workload == "C5"
+    inst = workload(args.workload, rank, 0, world)
+    B = inst.batch
     hykkt = inst.m_eq > 0
     S = K.KKTSolver.from_instance(inst)
     S.bind(local)
     stream = torch.cuda.current_stream(dev)
     d = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
-    # value sets cycled over steps (re-drawn values = successive IPM iterations)
+    # value sets cycled over steps (re-drawn values = successive IPM iterations, same pattern)
     sets = []
     for k in range(args.nvalues):
-        it = workload(args.workload, rank, 1 + k)
+        it = workload(args.workload, rank, 1 + k, world)
         sets.append(dict(W=d(it.W_vals), J=d(it.J_vals), Sx=d(it.Sigma_x), Ss=d(it.Sigma_s),
                          b=d(it.b), r1=d(it.rbar1) if hykkt else None,
                          r2=d(it.rbar2) if hykkt else None, inst=it))
-    x = torch.zeros(inst.n, dtype=torch.float64, device=dev)
+    x = torch.zeros((B, inst.n) if B > 1 else (inst.n,), dtype=torch.float64, device=dev)
     dy = torch.zeros(max(inst.m_eq, 1), dtype=torch.float64, device=dev)
+    gathered = None
+    if dist is not None and batched:
+        from synth.generator import partition
+        counts = [partition(C5_TOTAL, world, r)[1] - partition(C5_TOTAL, world, r)[0] for r in range(world)]
+        assert len(set(counts)) == 1, "C5 multi-GPU run needs world | 512"
+        gathered = torch.empty((C5_TOTAL, inst.n), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
@@ -208,8 +247,10 @@ def run_ours(args, rank, world):
         else:
             S.solve(v["b"], x, args.max_refine, 0.0)
         n3 = S.launch_count()
+        if gathered is not None:     # the only cross-GPU step: final gather of x (NCCL)
+            dist.all_gather_into_tensor(gathered, x)
         if evs: evs[3].record(stream)
-        return n1 + 1 + n3
+        return n1 + 2 + n3
 
     for k in range(args.warmup):
         step(sets[k % len(sets)])
@@ -239,24 +280,27 @@ def run_ours(args, rank, world):
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    ms_per_solve = total_ms / (args.steps * world)
+    # batch: one step = one IPM iteration of the whole 512-instance batch (strong scaling);
+    # otherwise every rank solves its own instance (weak scaling)
+    value = total_ms / args.steps if batched else total_ms / (args.steps * world)
     # ---------------- e2e through host buffers (pinned) ----------------
     v0 = sets[0]["inst"]
     pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
-    hW, hJ, hSx, hSs, hb = (pin(v0.W_vals), pin(v0.J_vals), pin(v0.Sigma_x), pin(v0.Sigma_s), pin(v0.b))
-    hx = torch.zeros(inst.n, dtype=torch.float64).pin_memory()
     e2e_ms = None
+    h2d = d2h = 0
     if not hykkt:
+        hW, hJ, hSx, hSs, hb = (pin(v0.W_vals), pin(v0.J_vals), pin(v0.Sigma_x), pin(v0.Sigma_s), pin(v0.b))
+        hx = torch.zeros(tuple(x.shape), dtype=torch.float64).pin_memory()
+        call = lambda: K.kkt_step_host(S.h, hW, hJ, hSx, hSs, None, inst.delta_w, inst.delta_c,
+                                       inst.gamma, hb, hx, args.max_refine, 0.0)
         for _ in range(2):
-            K.kkt_step_host(S.h, hW, hJ, hSx, hSs, None, inst.delta_w, inst.delta_c, inst.gamma, hb, hx,
-                            args.max_refine, 0.0)
+            call()
         e0, e1 = ev(), ev()
         ts = []
         for k in range(args.steps):
             flush.fill_(float(k))
             e0.record(stream)
-            K.kkt_step_host(S.h, hW, hJ, hSx, hSs, None, inst.delta_w, inst.delta_c, inst.gamma, hb, hx,
-                            args.max_refine, 0.0)
+            call()
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
@@ -265,59 +309,62 @@ def run_ours(args, rank, world):
             t = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
-        e2e_ms = e2e_tot / (args.steps * world)
-    h2d = 8 * (inst.nnzW + inst.nnzJ + inst.n + (inst.m - inst.m_eq) + inst.n)
-    d2h = 8 * inst.n
-    # ---------------- roofline of the dominant phase ----------------
+        e2e_ms = e2e_tot / args.steps if batched else e2e_tot / (args.steps * world)
+        h2d = 8 * B * (inst.nnzW + inst.nnzJ + inst.n + (inst.m - inst.m_eq) + inst.n)
+        d2h = 8 * B * inst.n
+    # ---------------- roofline ----------------
     ph_mean = ph.mean(0)
-    names = ["condense", "factor", "solve"]
-    dom = int(np.argmax(ph_mean))
-    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    work = algorithmic_work(S, inst, max(info["refine_iters"], 0))
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    pk = json.load(open(pk_path)) if os.path.exists(pk_path) else {}
     fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    nnzK = int(S.info["nnzK"])
-    if names[dom] == "factor":
-        achieved = S.info["flops"] / (ph_mean[1] * 1e-3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": fp64["dfma_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / fp64["dfma_tflops"], "traffic": None, "kernel": "factor_kernel",
-                "note": "FP64 DFMA peak measured by tools/fp64_peaks.cu (profiles/r01_fp64_peaks.json)"}
-    elif names[dom] == "condense":
-        byts = 8 * (inst.nnzW + inst.nnzJ + inst.n + inst.m) + 8 * nnzK
-        achieved = byts / (ph_mean[0] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "kernel": "condense_kernel"}
-    else:
-        sweeps = 1 + 2 * max(info["refine_iters"], 0) if not hykkt else None
-        byts = 16 * S.info["nnzL"] + 24 * inst.n
-        achieved = byts / (ph_mean[2] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "kernel": "solve (fwd+bwd+refine)",
-                "note": "algorithmic bytes of ONE trsv pair over the whole solve phase"}
-    out = {"metric": METRIC, "value": ms_per_solve, "unit": UNIT, "n_gpus": world,
+    hbm_note = "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback 6650 GB/s"
+    f_ach = B * work["factor_flops"] / (ph_mean[1] * 1e-3) / 1e12
+    roof_factor = {"bound": "tensor", "achieved": f_ach, "peak": fp64["dmma_tflops"], "unit": "TFLOP/s",
+                   "frac": f_ach / fp64["dmma_tflops"], "traffic": None,
+                   "kernel": "kkt_factor (factor_small_kernel + factor_big_kernel)",
+                   "work": "B x sum_j c_j^2 flops per call",
+                   "peak_note": "FP64 DMMA (mma.sync m8n8k4) measured by tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json"}
+    s_ach = B * work["solve_bytes"] / (ph_mean[2] * 1e-3) / 1e9
+    roof_solve = {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak, "unit": "GB/s",
+                  "frac": s_ach / hbm_peak, "traffic": None,
+                  "kernel": ("hykkt_solve" if hykkt else "kkt_solve") + " (fwd/bwd trsv kernels + dd residual)",
+                  "work": f"B x [{work['trsv_pairs']} trsv pairs x 16 nnz(L) + residual passes] bytes",
+                  "peak_note": hbm_note}
+    c_ach = B * work["condense_bytes"] / (ph_mean[0] * 1e-3) / 1e9
+    roof_cond = {"bound": "hbm", "achieved": c_ach, "peak": hbm_peak, "unit": "GB/s", "frac": c_ach / hbm_peak,
+                 "traffic": None, "kernel": "condense_kernel (+dweights_kernel)"}
+    roofs = {"condense": roof_cond, "factor": roof_factor, "solve": roof_solve}
+    dom = ["condense", "factor", "solve"][int(np.argmax(ph_mean))]
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic",
+           "higher_is_better": False, "scaling": "strong" if batched else "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, synth/)",
            "config": {"workload": f"{args.workload}: {describe(args.workload)}", "n": inst.n,
-                      "m": inst.m, "m_eq": inst.m_eq, "nnzK": nnzK, "nnzL": int(S.info["nnzL"]),
+                      "m": inst.m, "m_eq": inst.m_eq, "batch_per_gpu": B,
+                      "nnzK": int(S.info["nnzK"]), "nnzL": int(S.info["nnzL"]),
                       "flops": S.info["flops"], "nsuper": S.info["nsuper"],
+                      "tree_height": S.info["tree_height"],
                       "l2": "flushed (256 MiB write) before every step, outside the event window",
-                      "max_refine": args.max_refine, "parallelism": f"instances x{world}"},
-           "phases_ms": {n_: float(v) for n_, v in zip(names, ph_mean)},
+                      "max_refine": args.max_refine,
+                      "parallelism": f"{'batch partition' if batched else 'instance per GPU'} x{world}"},
+           "phases_ms": {n_: float(v_) for n_, v_ in zip(["condense", "factor", "solve"], ph_mean)},
            "refine_iters": info["refine_iters"], "cg_iters": info["cg_iters"],
            "bwd_err": info["bwd_err"], "analyze_ms": S.info["analyze_ms"],
            "wall_s_timed": t_wall,
-           "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d if e2e_ms else 0,
-                   "d2h_bytes_per_step": d2h if e2e_ms else 0},
+           "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
            "gpu_launches": launches,
-           "roofline": roof,
+           "roofline": dict(roofs[dom], phase=dom),
+           "roofline_phases": roofs,
            "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ms, cnt, _ = oracle_time(inst, args.cpu_sample_s)
-        out["cpu_baseline"] = {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle",
-                               "sample": f"{cnt} oracle IPM iterations of {args.workload} "
+        one = inst.instance(0) if B > 1 else inst
+        ms, cnt, _ = oracle_time(one, args.cpu_sample_s)
+        out["cpu_baseline"] = {"value": ms * B, "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"{cnt} oracle IPM iterations of one {args.workload} instance "
                                          f"(condense + Cholesky + __float128 refined solve), "
-                                         f"~{args.cpu_sample_s:.0f} s budget"}
+                                         f"~{args.cpu_sample_s:.0f} s budget" + (f"; x{B} for the batch" if B > 1 else "")}
     if rank == 0:
         print(json.dumps(out), flush=True)
     S.close()

@@ -445,6 +445,18 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
     std::vector<int> f(P.sn_cp.begin(), P.sn_cp.end() - 1);
     for (int s = 0; s < ns; s++) if (P.sn_parent[s] >= 0) P.sn_ch[f[P.sn_parent[s]]++] = s;
   }
+  // children ordered by subtree height (descending): the top-down solve continues with the
+  // child on the longest remaining chain and queues the others (critical path first)
+  {
+    std::vector<int> hsub(ns, 0);
+    for (int s = 0; s < ns; s++)
+      if (P.sn_parent[s] >= 0) hsub[P.sn_parent[s]] = std::max(hsub[P.sn_parent[s]], hsub[s] + 1);
+    for (int s = 0; s < ns; s++)
+      std::sort(P.sn_ch.begin() + P.sn_cp[s], P.sn_ch.begin() + P.sn_cp[s + 1], [&](int a, int b) {
+        return hsub[a] != hsub[b] ? hsub[a] > hsub[b] : a < b;
+      });
+    P.sn_hsub = hsub;
+  }
   std::vector<std::vector<int>> rows(ns);
   std::vector<int> smark(n, -1);
   P.max_front = 0;
@@ -551,6 +563,17 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       if (big[s] && par < 0) P.dn_b.push_back(s);
       if (!big[s] && (par < 0 || big[par])) P.dn_s.push_back(s);
     }
+    auto by_height = [&](int a, int b) {
+      return P.sn_hsub[a] != P.sn_hsub[b] ? P.sn_hsub[a] > P.sn_hsub[b] : a < b;
+    };
+    std::sort(P.dn_b.begin(), P.dn_b.end(), by_height);
+    std::sort(P.dn_s.begin(), P.dn_s.end(), by_height);
+    std::sort(P.up_s.begin(), P.up_s.end(), [&](int a, int b) {  // deepest chains first
+      int ha = 0, hb = 0;
+      for (int x = a; x >= 0 && !big[x]; x = P.sn_parent[x]) ha++;
+      for (int x = b; x >= 0 && !big[x]; x = P.sn_parent[x]) hb++;
+      return ha != hb ? ha > hb : a < b;
+    });
     P.sn.resize(ns);
     for (int s = 0; s < ns; s++) {
       SnInfo& I = P.sn[s];
@@ -561,6 +584,8 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       I.k0 = P.Kp[snf[s]]; I.k1 = P.Kp[snf[s + 1]];
       I.Lp = P.sn_Lp[s]; I.Up = P.sn_Up[s]; I.uvp = (int)P.sn_uvp[s];
     }
+    P.chinfo.resize(P.sn_ch.size());
+    for (size_t t = 0; t < P.sn_ch.size(); t++) P.chinfo[t] = P.sn[P.sn_ch[t]];
     for (int s : P.order) {
       if (big[s]) P.order_b.push_back(s);
       else {

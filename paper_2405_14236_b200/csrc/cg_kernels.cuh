@@ -14,7 +14,7 @@ __global__ void refine_init_kernel(int batch, DevCtrl C) {
   if (b >= batch) return;
   C.done[b] = 0; C.refine_iters[b] = 0; C.grow[b] = 0;
   C.omega[b] = 0ULL; C.omega_prev[b] = INFINITY; C.omega_last[b] = 0.0;
-  C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
+  C.dxn[b] = 0ULL; C.xn[b] = 0ULL; C.dxprev[b] = INFINITY;
 }
 
 // Stopping rules (R9): omega <= tol (only if tol > 0); ||dx|| <= 2u ||x|| after the previous
@@ -31,7 +31,12 @@ __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep
   if (sweep > 0) {
     double dxn = bits2d(C.dxn[b]), xn = bits2d(C.xn[b]);
     C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
-    if (dxn <= 2.0 * 1.1102230246251565e-16 * xn) stop = true;
+    // the last correction was negligible, or (geometric convergence, rate rho = ||dx_k|| /
+    // ||dx_k-1|| < 1/2) the next one would be: rho ||dx_k|| / (1 - rho) <= 1e-14 ||x||   (R9)
+    const double rho = dxn / C.dxprev[b];
+    C.dxprev[b] = dxn;
+    if (dxn <= 1e-14 * xn) stop = true;
+    if (rho < 0.5 && rho * dxn / (1.0 - rho) <= 1e-14 * xn) stop = true;
     if (om > C.omega_prev[b]) { if (++C.grow[b] >= 2) stop = true; }
     else C.grow[b] = 0;
   }

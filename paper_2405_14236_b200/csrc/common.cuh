@@ -136,10 +136,13 @@ __device__ __forceinline__ int next_task(int* ctl, int* s_task) {
   __syncthreads();
   return *s_task;
 }
-// ctl[0] = ticket/head, ctl[1] = exit count, ctl[2] = queue tail, ctl[3] = completed tasks;
-// the last worker to exit resets all four for the next launch (stream order publishes it).
+// Control block of one persistent launch (KKT_CTL ints, the all-done flag on its own 32-byte
+// sector so that pollers do not contend with the completion atomics):
+//   ctl[0] = ticket/head, ctl[1] = exit count, ctl[2] = queue tail, ctl[3] = completed tasks,
+//   ctl[8] = all tasks done.  The last worker to exit resets it for the next launch.
+#define KKT_CTL 16
 __device__ __forceinline__ void reset_ctl(int* ctl) {
-  ctl[0] = 0; ctl[1] = 0; ctl[2] = 0; ctl[3] = 0;
+  ctl[0] = 0; ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[8] = 0;
   __threadfence();
 }
 __device__ __forceinline__ void persistent_exit(int* ctl) {

@@ -33,6 +33,7 @@ struct DevPlan {
   const int *sn_first, *sn_rp, *sn_rows, *sn_rel, *sn_parent, *sn_cp, *sn_ch, *order;
   const int *order_s, *order_b;  // level order restricted to small / big supernodes
   const SnInfo* sn;              // [ns]
+  const SnInfo* chinfo;          // parallel to sn_ch
   // ready lists of the spin-free schedulers
   const int *up_s, *up_b, *dn_b, *dn_s;   // see plan.h
   long long* trace;              // optional [3][ns][2] globaltimer stamps (KKT_TRACE=1), else NULL
@@ -56,6 +57,7 @@ struct DevCtrl {
   unsigned long long* omega; // bits of current omega (atomicMax)
   double* omega_prev;        // previous sweep's omega
   double* omega_last;        // reported omega
+  double* dxprev;            // ||dx|| of the previous correction
   unsigned long long* dxn;   // bits of ||dx||_inf
   unsigned long long* xn;    // bits of ||x||_inf
   // CG

@@ -59,9 +59,11 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I
       if (base + u * nt < I.k1) F[pos[u]] = val[u];
   }
   sync();
+  SnInfo Cn;
+  if (I.c0 < I.c1) Cn = P.chinfo[I.c0];
   for (int ci = I.c0; ci < I.c1; ci++) {
-    const int c = __ldg(P.sn_ch + ci);
-    const SnInfo C = P.sn[c];
+    const SnInfo C = Cn;
+    if (ci + 1 < I.c1) Cn = P.chinfo[ci + 1];  // prefetch the next child's metadata
     const int Rc = C.r - C.w;
     const int* rel = P.sn_rel + C.rp0 + C.w;
     const double* Uc = Ub + C.Up;

@@ -41,11 +41,23 @@ static thread_local std::string g_err;
     }                                                                              \
   } while (0)
 
+#define TRY(x) do { kkt_status s_ = (x); if (s_ != KKT_OK) return s_; } while (0)
+
 struct kkt_plan {
   Plan P;
   int device = -1;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // caller's stream (all work is ordered on it)
+  cudaStream_t ls = nullptr;       // kernel-launch stream: == stream, or the capture stream
+  cudaStream_t cap = nullptr;      // private stream used only to record CUDA graphs
   bool bound = false;
+  // CUDA graph of the whole refined solve (fixed internal b / x buffers)
+  bool use_graph = true;
+  cudaGraphExec_t solve_exec = nullptr;
+  int g_max_refine = -1;
+  double g_tol = -1.0, g_dw = 0.0;
+  const void *g_W = nullptr, *g_J = nullptr, *g_Sx = nullptr;
+  long long g_launches = 0;
+  double *gb = nullptr, *gx = nullptr;
   int sms = 148;
   // device plan
   void* plan_mem = nullptr;
@@ -105,6 +117,8 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->Dv = c.take<double>(B * n);
   h->Xp = c.take<double>(B * n);
   h->res = c.take<double>(B * n);
+  h->gb = c.take<double>(B * n);
+  h->gx = c.take<double>(B * n);
   h->dxv = c.take<double>(B * n);
   h->Dh = c.take<double>(B * m);
   h->Dl = c.take<double>(B * m);
@@ -125,7 +139,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->TQ.q = c.take<int>(B * ns);
   h->TQ.flag = c.take<int>(B * ns);
   h->facnt = c.take<int>(B * ns);
-  h->ctl = c.take<int>(32);
+  h->ctl = c.take<int>(8 * KKT_CTL);
   h->fail = c.take<int>(1);
   h->status = c.take<int>(1);
   h->C.done = c.take<int>(B);
@@ -134,6 +148,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.omega = c.take<unsigned long long>(B);
   h->C.omega_prev = c.take<double>(B);
   h->C.omega_last = c.take<double>(B);
+  h->C.dxprev = c.take<double>(B);
   h->C.dxn = c.take<unsigned long long>(B);
   h->C.xn = c.take<unsigned long long>(B);
   h->C.cg_done = c.take<int>(B);
@@ -254,6 +269,9 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(cudaSetDevice(device));
   h->device = device;
   h->stream = (cudaStream_t)stream;
+  h->ls = h->stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+  h->use_graph = !(getenv("KKT_NO_GRAPH") && atoi(getenv("KKT_NO_GRAPH")) > 0);
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   h->sms = prop.multiProcessorCount;
@@ -271,7 +289,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   size_t tot = 0;
   for (auto* v : iv) tot += vbytes(*v);
   for (auto* v : lv) tot += vbytes(*v);
-  tot += vbytes(P.sn);
+  tot += vbytes(P.sn) + vbytes(P.chinfo);
   CUDA_TRY(cudaMalloc(&h->plan_mem, tot));
   std::vector<const void*> dptr;
   size_t off = 0;
@@ -289,6 +307,9 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   if (!P.sn.empty()) CUDA_TRY(cudaMemcpy(base + off, P.sn.data(), P.sn.size() * sizeof(SnInfo), cudaMemcpyHostToDevice));
   const SnInfo* d_sn = (const SnInfo*)(base + off);
   off += vbytes(P.sn);
+  if (!P.chinfo.empty()) CUDA_TRY(cudaMemcpy(base + off, P.chinfo.data(), P.chinfo.size() * sizeof(SnInfo), cudaMemcpyHostToDevice));
+  const SnInfo* d_ch = (const SnInfo*)(base + off);
+  off += vbytes(P.chinfo);
   DevPlan& d = h->dp;
   d.n = P.n; d.m = P.m; d.m_eq = P.m_eq; d.nnzW = P.nnzW; d.nnzJ = P.nnzJ; d.nnzK = P.Kp[P.n];
   d.ns = P.ns; d.batch = P.batch; d.max_front = P.max_front;
@@ -309,6 +330,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   d.sn_Up = (const long long*)dptr[k++];
   d.sn_uvp = (const long long*)dptr[k++];
   d.sn = d_sn;
+  d.chinfo = d_ch;
   d.trace = nullptr;
   if (getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
     CUDA_TRY(cudaMalloc(&h->trace_buf, (size_t)3 * std::max(P.ns, 1) * KKT_TRACE_SLOTS * sizeof(long long)));
@@ -395,13 +417,13 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
   h->dw = delta_w; h->dc = delta_c; h->gamma = gamma;
   h->launches = 0;
   if (P.m > 0) {
-    dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->stream>>>(
+    dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
     LAUNCH_CHECK();
     h->launches++;
   }
   long long tot = (long long)P.batch * P.Kp[P.n];
-  condense_kernel<<<grid_for(tot, 256, h->sms), 256, 0, h->stream>>>(h->dp, W_vals, J_vals, Sigma_x,
+  condense_kernel<<<grid_for(tot, 256, h->sms), 256, 0, h->ls>>>(h->dp, W_vals, J_vals, Sigma_x,
                                                                      h->Dh, delta_w, h->Kv);
   LAUNCH_CHECK();
   h->launches++;
@@ -415,14 +437,14 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
   if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
   const Plan& P = h->P;
   if (!P.order_s.empty()) {
-    factor_small_kernel<<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->stream>>>(
-        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0, h->fail);
+    factor_small_kernel<<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
+        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0 * KKT_CTL, h->fail);
     LAUNCH_CHECK();
     h->launches++;
   }
   if (!P.order_b.empty()) {
-    factor_big_kernel<<<h->g_fbig, KKT_BNT, h->fbig_smem, h->stream>>>(
-        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 4, h->fail, h->factor_smem_cap);
+    factor_big_kernel<<<h->g_fbig, KKT_BNT, h->fbig_smem, h->ls>>>(
+        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 1 * KKT_CTL, h->fail, h->factor_smem_cap);
     LAUNCH_CHECK();
     h->launches++;
   }
@@ -435,23 +457,23 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
                                long long xs, const int* done) {
   const Plan& P = h->P;
   if (!P.order_s.empty()) {
-    fwd_small_kernel<<<h->g_tsmall, KKT_WPB * 32, h->tsmall_smem, h->stream>>>(
-        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 8, done);
+    fwd_small_kernel<<<h->g_tsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
+        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done);
     LAUNCH_CHECK();
     h->launches++;
   }
   if (!P.order_b.empty()) {
-    fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->stream>>>(
-        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 12, done, h->pcap);
+    fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->ls>>>(
+        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 3 * KKT_CTL, done, h->pcap);
     LAUNCH_CHECK();
-    bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->stream>>>(
-        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 16, done, h->pcap);
+    bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
+        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap);
     LAUNCH_CHECK();
     h->launches += 2;
   }
   if (!P.order_s.empty()) {
-    bwd_small_kernel<<<h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->stream>>>(
-        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 20, done);
+    bwd_small_kernel<<<h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
+        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 5 * KKT_CTL, done);
     LAUNCH_CHECK();
     h->launches++;
   }
@@ -463,19 +485,40 @@ static kkt_status launch_resid(kkt_plan* h, const double* x, const double* rhs, 
                                unsigned long long* omega, const int* done) {
   const Plan& P = h->P;
   if (P.m > 0) {
-    resid_rows_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->stream>>>(
+    resid_rows_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, h->Jv, h->Dh, h->Dl, x, P.n, mode, dy, rb2, h->res2, h->T, h->A, done);
     LAUNCH_CHECK();
     h->launches++;
   }
-  resid_cols_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->stream>>>(
+  resid_cols_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
       h->dp, h->Wv, h->Jv, h->Sx, h->dw, x, P.n, rhs, P.n, h->T, h->A, res, omega, done);
   LAUNCH_CHECK();
   h->launches++;
   return KKT_OK;
 }
 
-#define TRY(x) do { kkt_status s_ = (x); if (s_ != KKT_OK) return s_; } while (0)
+
+static kkt_status enqueue_solve(kkt_plan* h, const double* b, double* x, int max_refine, double tol_bwd) {
+  const Plan& P = h->P;
+  int gb = (P.batch + 127) / 128;
+  refine_init_kernel<<<gb, 128, 0, h->ls>>>(P.batch, h->C);
+  LAUNCH_CHECK();
+  h->launches++;
+  TRY(launch_solve(h, b, P.n, x, P.n, nullptr));
+  for (int k = 0; k <= max_refine; k++) {
+    TRY(launch_resid(h, x, b, 0, nullptr, nullptr, h->res, h->C.omega, h->C.done));
+    refine_decide_kernel<<<gb, 128, 0, h->ls>>>(P.batch, h->C, tol_bwd, k, k == max_refine);
+    LAUNCH_CHECK();
+    h->launches++;
+    if (k == max_refine) break;
+    TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
+    refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
+        P.batch, P.n, x, h->dxv, h->C);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
+  return KKT_OK;
+}
 
 extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int max_refine, double tol_bwd) {
   if (!h || !b || !x) return KKT_ERR_ARG;
@@ -484,23 +527,32 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   if (tol_bwd < 0) tol_bwd = 0;  // 0 disables the backward-error stop (R9)
   max_refine = std::max(0, max_refine);
   h->launches = 0;
-  int gb = (P.batch + 127) / 128;
-  refine_init_kernel<<<gb, 128, 0, h->stream>>>(P.batch, h->C);
-  LAUNCH_CHECK();
-  h->launches++;
-  TRY(launch_solve(h, b, P.n, x, P.n, nullptr));
-  for (int k = 0; k <= max_refine; k++) {
-    TRY(launch_resid(h, x, b, 0, nullptr, nullptr, h->res, h->C.omega, h->C.done));
-    refine_decide_kernel<<<gb, 128, 0, h->stream>>>(P.batch, h->C, tol_bwd, k, k == max_refine);
-    LAUNCH_CHECK();
-    h->launches++;
-    if (k == max_refine) break;
-    TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
-    refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->stream>>>(
-        P.batch, P.n, x, h->dxv, h->C);
-    LAUNCH_CHECK();
-    h->launches++;
+  if (!h->use_graph) return enqueue_solve(h, b, x, max_refine, tol_bwd);
+  // The refined solve is one CUDA graph (all sweeps; finished instances early-exit on device),
+  // recorded once per (max_refine, tol, value pointers, delta_w) on a private stream.
+  const bool stale = !h->solve_exec || h->g_max_refine != max_refine || h->g_tol != tol_bwd ||
+                     h->g_W != h->Wv || h->g_J != h->Jv || h->g_Sx != h->Sx || h->g_dw != h->dw;
+  if (stale) {
+    if (h->solve_exec) { cudaGraphExecDestroy(h->solve_exec); h->solve_exec = nullptr; }
+    h->ls = h->cap;
+    CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    kkt_status st = enqueue_solve(h, h->gb, h->gx, max_refine, tol_bwd);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    h->ls = h->stream;
+    if (st != KKT_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) { g_err = std::string("graph capture: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    e = cudaGraphInstantiate(&h->solve_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { g_err = std::string("graph instantiate: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    h->g_max_refine = max_refine; h->g_tol = tol_bwd; h->g_W = h->Wv; h->g_J = h->Jv;
+    h->g_Sx = h->Sx; h->g_dw = h->dw; h->g_launches = h->launches;
   }
+  const size_t bytes = (size_t)P.batch * P.n * sizeof(double);
+  CUDA_TRY(cudaMemcpyAsync(h->gb, b, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaGraphLaunch(h->solve_exec, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(x, h->gx, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  h->launches = h->g_launches;
   return KKT_OK;
 }
 
@@ -510,13 +562,13 @@ static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, do
   const Plan& P = h->P;
   const int gs = grid_for((long long)P.batch * P.n, 256, h->sms);
   // s = rbar1 + gamma G^T rbar2
-  gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, nullptr);
+  gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, nullptr);
   LAUNCH_CHECK();
   h->launches++;
   // z = K_gamma^-1 s ; r = G z - rbar2 ; p = r ; dy = 0
   TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, nullptr));
   dim3 gg(KKT_NPART, P.batch);
-  g_kernel<<<gg, 256, 0, h->stream>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0);
+  g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0);
   LAUNCH_CHECK();
   h->launches++;
   const int chunk = 8;
@@ -524,15 +576,15 @@ static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, do
   while (it < maxit) {
     int todo = std::min(chunk, maxit - it);
     for (int q = 0; q < todo; q++) {
-      gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
+      gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
       LAUNCH_CHECK();
       TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->stream>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1);
+      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1);
       LAUNCH_CHECK();
-      cg_update_kernel<<<gg, 256, 0, h->stream>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
                                                    rtol, h->status);
       LAUNCH_CHECK();
-      cg_p_kernel<<<grid_for((long long)P.batch * P.m_eq, 256, h->sms), 256, 0, h->stream>>>(
+      cg_p_kernel<<<grid_for((long long)P.batch * P.m_eq, 256, h->sms), 256, 0, h->ls>>>(
           P.batch, P.m_eq, h->cp, h->cr, h->C);
       LAUNCH_CHECK();
       h->launches += 4;
@@ -546,10 +598,10 @@ static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, do
     for (int b = 0; b < P.batch; b++) all = all && h->pinned_flags[b];
     if (all) break;
   }
-  cg_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->stream>>>(P.batch, h->C, first ? 1 : 0, h->status);
+  cg_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C, first ? 1 : 0, h->status);
   LAUNCH_CHECK();
   // dx = K_gamma^-1 (s - G^T dy)
-  gt_kernel<<<gs, 256, 0, h->stream>>>(h->dp, h->Jv, dyo, -1.0, h->sg, h->wv, nullptr);
+  gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, dyo, -1.0, h->sg, h->wv, nullptr);
   LAUNCH_CHECK();
   TRY(launch_solve(h, h->wv, P.n, dxo, P.n, nullptr));
   h->launches += 2;
@@ -573,8 +625,8 @@ extern "C" kkt_status hykkt_solve(kkt_handle h, const double* rbar1, const doubl
     TRY(launch_resid(h, dx, rbar1, 1, dy, rbar2, h->hr1, nullptr, nullptr));
     CUDA_TRY(cudaMemcpyAsync(h->hr2, h->res2, mm * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
     TRY(hykkt_pass(h, h->hr1, h->hr2, h->hdx, h->hdy, cg_rtol, cg_maxit, false));
-    axpy_kernel<<<grid_for(nn, 256, h->sms), 256, 0, h->stream>>>(nn, dx, h->hdx);
-    axpy_kernel<<<grid_for(mm, 256, h->sms), 256, 0, h->stream>>>(mm, dy, h->hdy);
+    axpy_kernel<<<grid_for(nn, 256, h->sms), 256, 0, h->ls>>>(nn, dx, h->hdx);
+    axpy_kernel<<<grid_for(mm, 256, h->sms), 256, 0, h->ls>>>(mm, dy, h->hdy);
     LAUNCH_CHECK();
     h->launches += 2;
   }
@@ -716,6 +768,8 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
       if (p) cudaFree(p);
     if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
     if (h->trace_buf) cudaFree(h->trace_buf);
+    if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
+    if (h->cap) cudaStreamDestroy(h->cap);
   }
   delete h;
   return KKT_OK;

@@ -58,6 +58,8 @@ struct Plan {
   //   dn_b: big roots (phase-1 top-down start);      dn_s: small roots + small children of big
   std::vector<int> up_s, up_b, dn_b, dn_s;
   std::vector<SnInfo> sn;
+  std::vector<SnInfo> chinfo;    // parallel to sn_ch: SnInfo of each child (one hop less)
+  std::vector<int> sn_hsub;      // subtree height
   std::vector<int> kpos;         // per K entry: offset inside its supernode's panel
   std::vector<int> col_sn;       // internal column -> supernode
   int height = 0, max_front = 0;

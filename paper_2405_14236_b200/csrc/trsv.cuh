@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, cons
       for (int q = lane; q < r; q += 32) v[q] = (q < w) ? bb[__ldg(P.perm + I.f0 + q)] : 0.0;
       __syncwarp();
       for (int ci = I.c0; ci < I.c1; ci++) {
-        const SnInfo C = P.sn[__ldg(P.sn_ch + ci)];
+        const SnInfo C = P.chinfo[ci];
         const int Rc = C.r - C.w;
         const int* rel = P.sn_rel + C.rp0 + C.w;
         const double* u = uv + C.uvp;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       }
       __syncthreads();
       for (int ci = I.c0; ci < I.c1; ci++) {
-        const SnInfo C = P.sn[__ldg(P.sn_ch + ci)];
+        const SnInfo C = P.chinfo[ci];
         const int Rc = C.r - C.w;
         const int* rel = P.sn_rel + C.rp0 + C.w;
         const double* u = uv + C.uvp;
@@ -215,12 +215,10 @@ __device__ __forceinline__ int pop_task(int* ctl, const int* init, int ninit_nod
   if (h < ninit) return __ldg(init + h / batch) * batch + h % batch;
   const int slot = h - ninit;
   if (slot >= total) return -1;
-  int ns = 64;
   for (;;) {
     if (ld_volatile(Q.flag + slot)) break;
-    if (ld_volatile(ctl + 3) >= total) return -1;
-    __nanosleep(ns);
-    if (ns < 1024) ns *= 2;
+    if (ld_volatile(ctl + 8)) return -1;  // every task of the phase is done
+    __nanosleep(64);
   }
   __threadfence();
   const int task = ld_volatile(Q.q + slot);
@@ -231,7 +229,7 @@ __device__ __forceinline__ int pop_task(int* ctl, const int* init, int ninit_nod
 // Continue with the first eligible child, push the others.  Called by one lane / thread after
 // the supernode's results are globally visible.
 __device__ __forceinline__ int spawn_children(const DevPlan& P, const SnInfo& I, int b, int* ctl,
-                                              TaskQueue Q, bool big_phase) {
+                                              TaskQueue Q, bool big_phase, int total) {
   int next = -1;
   for (int ci = I.c0; ci < I.c1; ci++) {
     const int c = __ldg(P.sn_ch + ci);
@@ -245,7 +243,8 @@ __device__ __forceinline__ int spawn_children(const DevPlan& P, const SnInfo& I,
       st_release(Q.flag + slot, 1);
     }
   }
-  atomicAdd(ctl + 3, 1);  // completed
+  __threadfence();
+  if (atomicAdd(ctl + 3, 1) == total - 1) st_release(ctl + 8, 1);  // completed -> all done
   return next;
 }
 
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     }
     const int s = task / P.batch, b = task % P.batch;
     if (done && done[b]) {  // finished instance: account for its whole subtree without work
-      if (tid == 0) s_task = spawn_children(P, P.sn[s], b, ctl, Q, true);
+      if (tid == 0) s_task = spawn_children(P, P.sn[s], b, ctl, Q, true, total);
       __syncthreads();
       task = s_task;
       __syncthreads();
@@ -328,7 +327,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     if (tid == 0) trace_stamp(P, 2, s, b, 1);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_task = spawn_children(P, I, b, ctl, Q, true);
+    if (tid == 0) s_task = spawn_children(P, I, b, ctl, Q, true, total);
     __syncthreads();
     task = s_task;
     __syncthreads();
@@ -360,7 +359,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
     const SnInfo I = P.sn[s];
     if (done && done[b]) {
       int t = 0;
-      if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false);
+      if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false, total);
       task = __shfl_sync(0xffffffffu, t, 0);
       continue;
     }
@@ -395,7 +394,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
     __threadfence();
     __syncwarp();
     int t = 0;
-    if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false);
+    if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false, total);
     task = __shfl_sync(0xffffffffu, t, 0);
   }
   warp_exit(ctl, gridDim.x * KKT_WPB);

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = ["KKTInstance", "bearing", "acopf", "make_config", "tiny_random", "CONFIGS",
-           "acopf_sizes", "redraw_values"]
+           "acopf_sizes", "redraw_values", "partition"]
 
 
 @dataclass
@@ -139,13 +139,18 @@ def bearing(nx=50, ny=50, seed=1000, Xi=1e-8, band=(0.5, 0.8), ecc=0.1, b_len=10
     Wp, Wc, Wv = _csr_from_coo(n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
     frac = (I / nx)
     active = (frac >= band[0]) & (frac < band[1])
-    Sx = np.empty(n)
-    Sx[p] = _two_level(rng, n, active, Xi)
+
+    def draw(rng):
+        Sx = np.empty(n)
+        Sx[p] = _two_level(rng, n, active, Xi)
+        return np.zeros(0), Wv, Sx, np.zeros(0), rng.standard_normal(n), None, None
+
+    _, _, Sx, _, b, _, _ = draw(rng)
     Jp = np.zeros(1, dtype=np.int32)
     inst = KKTInstance("C1-bearing-%dx%d" % (nx, ny), n, 0, 0, Wp, Wc, Wv, Jp,
-                       np.zeros(0, np.int32), np.zeros(0), Sx, np.zeros(0),
-                       b=rng.standard_normal(n),
+                       np.zeros(0, np.int32), np.zeros(0), Sx, np.zeros(0), b=b,
                        meta=dict(kind="bearing", nx=nx, ny=ny, Xi=Xi, seed=seed, band=band))
+    inst.meta["_draw"] = draw
     return inst
 
 
@@ -319,7 +324,8 @@ def acopf(nb, seed, hykkt=False, gamma=1e7, Xi=None, relaxed_active=1.0,
         r2 = rng.standard_normal(m_eq)
         return v, wv, Sx, Ss, b, r1, r2
 
-    outs = [draw(np.random.default_rng(seed + k if batch > 1 else seed + 7919)) for k in range(batch)]
+    family = batch > 1 or _pattern_rng_seed is not None   # batch family: instance k <- seed + k
+    outs = [draw(np.random.default_rng(seed + k if family else seed + 7919)) for k in range(batch)]
     stack = (lambda i: outs[0][i]) if batch == 1 else (lambda i: np.stack([o[i] for o in outs]))
     inst = KKTInstance(name or ("acopf-%d%s" % (nb, "-hykkt" if hykkt else "")), n, m, m_eq,
                        Wp, Wcol, stack(1), Jp, Jc, stack(0), stack(2), stack(3),
@@ -385,6 +391,12 @@ CONFIGS = {
 }
 
 
+def partition(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block partition of `total` batch instances over `world` ranks:
+    rank k gets [k*total//world, (k+1)*total//world)."""
+    return rank * total // world, (rank + 1) * total // world
+
+
 def make_config(name: str, instance: int = 0, gamma: float = 1e7, batch: int | None = None,
                 **kw) -> KKTInstance:
     """Build configuration C1..C5; seed = config_number*1000 + instance."""
@@ -401,6 +413,8 @@ def make_config(name: str, instance: int = 0, gamma: float = 1e7, batch: int | N
     if name == "C4":
         return acopf(78484, seed, name="C4-acopf78484", **kw)
     if name == "C5":
+        # instance k of the batch draws its values from seed 5000 + instance + k, so any block of
+        # a partition reproduces the same instances as the full batch (bitwise)
         return acopf(500, seed, batch=512 if batch is None else batch, name="C5-acopf500-batch",
                      _pattern_rng_seed=5000, **kw)
     raise KeyError(name)
