@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -574,6 +575,27 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       for (int x = b; x >= 0 && !big[x]; x = P.sn_parent[x]) hb++;
       return ha != hb ? ha > hb : a < b;
     });
+    // huge: fronts beyond one CTA's shared memory (KKT_HCAP doubles), closed upward
+    std::vector<char> huge(ns, 0);
+    long long hcap = KKT_HCAP;  // test hook: KKT_HCAP=<doubles> moves smaller fronts to the GPU-wide path
+    if (const char* e = getenv("KKT_HCAP")) hcap = std::min<long long>(hcap, std::max(0LL, atoll(e)));
+    for (int s = 0; s < ns; s++) {
+      long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = snf[s + 1] - snf[s], R = r - w;
+      long long need = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
+      if (need > hcap && big[s]) huge[s] = 1;
+    }
+    for (int s = 0; s < ns; s++)
+      if (huge[s] && P.sn_parent[s] >= 0) huge[P.sn_parent[s]] = 1;
+    P.up_bf.clear(); P.order_h.clear();
+    {
+      std::vector<int> nbn(ns, 0);  // big non-huge children
+      for (int s = 0; s < ns; s++)
+        if (big[s] && !huge[s] && P.sn_parent[s] >= 0) nbn[P.sn_parent[s]]++;
+      for (int s = 0; s < ns; s++) {
+        if (big[s] && !huge[s] && nbn[s] == 0) P.up_bf.push_back(s);
+        if (huge[s]) P.order_h.push_back(s);  // postorder = topological
+      }
+    }
     P.sn.resize(ns);
     for (int s = 0; s < ns; s++) {
       SnInfo& I = P.sn[s];
@@ -582,7 +604,7 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       I.rp0 = P.sn_rp[s]; I.r = P.sn_rp[s + 1] - P.sn_rp[s];
       I.par = P.sn_parent[s]; I.c0 = P.sn_cp[s]; I.c1 = P.sn_cp[s + 1]; I.big = big[s];
       I.k0 = P.Kp[snf[s]]; I.k1 = P.Kp[snf[s + 1]];
-      I.Lp = P.sn_Lp[s]; I.Up = P.sn_Up[s]; I.uvp = (int)P.sn_uvp[s];
+      I.Lp = P.sn_Lp[s]; I.Up = P.sn_Up[s]; I.uvp = (int)P.sn_uvp[s]; I.huge = huge[s];
     }
     P.chinfo.resize(P.sn_ch.size());
     for (size_t t = 0; t < P.sn_ch.size(); t++) P.chinfo[t] = P.sn[P.sn_ch[t]];

@@ -12,12 +12,16 @@ namespace kkt {
 constexpr int KKT_SCAP = 2048;
 constexpr int KKT_WPB = 4;      // warps per CTA in the warp-per-supernode kernels
 constexpr int KKT_BNT = 256;    // threads per CTA in the big-supernode kernels
+// Fronts needing more than KKT_HCAP doubles (and their ancestors) are factorised by the
+// whole-GPU cooperative kernel (huge.cuh); the rest of the big ones by one CTA in shared memory.
+constexpr int KKT_HCAP = 25600;
 
 // Per-supernode metadata packed in 64 bytes so one broadcast load fetches it.
 struct alignas(16) SnInfo {
   int f0, w, r, rp0;     // first column, width, front rows, offset into sn_rows
   int par, c0, c1, big;  // parent (-1 root), children [c0,c1) in sn_ch, 1 = CTA phase
-  int k0, k1, uvp, pad;  // K entries of the supernode's columns [k0, k1); update-vector offset
+  int k0, k1, uvp, huge; // K entries of the supernode's columns [k0, k1); update-vector offset;
+                         // 1 = factorised by the whole-GPU kernel (huge.cuh)
   long long Lp, Up;      // panel / update-matrix offsets
 };
 static_assert(sizeof(SnInfo) == 64, "SnInfo must be 64 bytes");
@@ -38,6 +42,8 @@ struct DevPlan {
   const int *up_s, *up_b, *dn_b, *dn_s;   // see plan.h
   long long* trace;              // optional [3][ns][2] globaltimer stamps (KKT_TRACE=1), else NULL
   int n_up_s, n_up_b, n_dn_b, n_dn_s;
+  const int *up_bf, *order_h;    // factor-only: big non-huge start list; huge supernodes in order
+  int n_up_bf, n_h;
   const long long *sn_Lp, *sn_Up, *sn_uvp;
   const int *Wf_p, *Wf_c, *Wf_k, *Jt_p, *Jt_r, *Jt_k, *Gt_end;
   const int *Jrp, *Jci;       // J CSR pattern (caller's, copied at analysis)

@@ -180,13 +180,13 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
   extern __shared__ double sm[];
   __shared__ int s_task, s_fail, s_last;
   const int tid = threadIdx.x;
-  const int ninit = P.n_up_b * P.batch;
+  const int ninit = P.n_up_bf * P.batch;
   auto bsync = [] { __syncthreads(); };
   for (;;) {
     const int t = next_task(ctl, &s_task);
     if (t >= ninit) break;
     const int b = t % P.batch;
-    int s = __ldg(P.up_b + t / P.batch);
+    int s = __ldg(P.up_bf + t / P.batch);
     int* cnt = cnt_all + (long long)b * P.ns;
     double* Lx = Lx_all + (long long)b * P.nnzL_stored;
     double* Ub = U_all + (long long)b * P.update_doubles;
@@ -226,9 +226,14 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
       __syncthreads();
       if (tid == 0) {
         const SnInfo Ip = P.sn[I.par];
-        const int old = atom_add_acq_rel(cnt + I.par, 1);
-        s_last = (old == Ip.c1 - Ip.c0 - 1);
-        if (s_last) cnt[I.par] = 0;
+        if (Ip.huge) {            // the whole-GPU phase takes it from here
+          red_release_add(cnt + I.par, 1);
+          s_last = 0;
+        } else {
+          const int old = atom_add_acq_rel(cnt + I.par, 1);
+          s_last = (old == Ip.c1 - Ip.c0 - 1);
+          if (s_last) cnt[I.par] = 0;
+        }
       }
       __syncthreads();
       if (!s_last) break;

@@ -1,0 +1,199 @@
+// huge.cuh -- whole-GPU factorisation of the top fronts ("huge": front > one CTA's shared
+// memory), one front at a time in topological order, by a cooperative persistent kernel:
+//
+//   assemble    grid-stride zero / K scatter / extend-add of every child's update matrix
+//               (children in fixed order, grid barrier between children: deterministic)
+//   for each column block [k0, k0+kb), kb <= 32:
+//     a. every CTA factors the kb x kb diagonal block in one warp's registers (redundantly,
+//        saving a barrier); CTA 0 writes L_kk and the inverse pivots
+//     b. TRSM: rows below the block, one thread per row, column-oriented sweep
+//     -- grid barrier --
+//     c. trailing update of the lower triangle of rows/cols [k0+kb, r) in 64 x 64 tiles over
+//        all CTAs: operands staged in shared memory, 8 warps x 8 DMMA (m8n8k4.f64) tiles
+//     -- grid barrier --
+#pragma once
+#include <cooperative_groups.h>
+
+#include "dense.cuh"
+
+namespace kkt {
+
+#define HB 32          // column block of the huge path (diagonal block held in registers)
+#define HT 64          // trailing-update tile edge
+#define HT_LD (HT + 1) // padded leading dimension of staged operands (bank spread)
+
+// shared memory layout of factor_huge_kernel (doubles)
+constexpr int HUGE_SMEM_DOUBLES = HB * HB + HB + 2 * HB * HT_LD;
+
+__global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const double* __restrict__ Kv_all,
+                                                          double* Lx_all, double* U_all, double* Dv_all,
+                                                          int* cnt_all, int* fail_all) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  double* Dg = sm;                  // [HB][HB] diagonal block, column-major (ld HB)
+  double* dsh = Dg + HB * HB;       // [HB] inverse pivots
+  double* As = dsh + HB;            // [HB][HT_LD] rows of tile i (k-major)
+  double* Bs = As + HB * HT_LD;     // [HB][HT_LD] rows of tile j
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const long long gtid = (long long)blockIdx.x * nt + tid, gnt = (long long)gridDim.x * nt;
+
+  for (int hi = 0; hi < P.n_h; hi++) {
+    const int s = __ldg(P.order_h + hi);
+    const SnInfo I = P.sn[s];
+    const int r = I.r, w = I.w, R = r - w;
+    const long long pw = (long long)r * w;
+    const long long usz = I.par >= 0 ? (long long)R * (R + 1) / 2 : 0;
+    for (int b = 0; b < P.batch; b++) {
+      if (gtid == 0) trace_stamp(P, 0, s, b, 0);
+      double* F = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
+      double* U = U_all + (long long)b * P.update_doubles + I.Up;
+      const double* Ub = U_all + (long long)b * P.update_doubles;
+      const double* Kv = Kv_all + (long long)b * P.nnzK;
+      double* dinv = Dv_all + (long long)b * P.n + I.f0;
+      if (gtid == 0) cnt_all[(long long)b * P.ns + s] = 0;  // children are complete
+      // ---------------- assemble ----------------
+      for (long long q = gtid; q < pw; q += gnt) F[q] = 0.0;
+      for (long long q = gtid; q < usz; q += gnt) U[q] = 0.0;
+      grid.sync();
+      for (long long k = I.k0 + gtid; k < I.k1; k += gnt) F[__ldg(P.kpos + k)] = __ldg(Kv + k);
+      for (int ci = I.c0; ci < I.c1; ci++) {
+        const SnInfo C = P.chinfo[ci];
+        const int Rc = C.r - C.w;
+        const int* rel = P.sn_rel + C.rp0 + C.w;
+        const double* Uc = Ub + C.Up;
+        const long long tot = (long long)Rc * (Rc + 1) / 2;
+        grid.sync();
+        for (long long q = gtid; q < tot; q += gnt) {
+          // decode packed (column-major lower) index q -> (ic, jc)
+          const double tR = 2.0 * Rc + 1.0;
+          int jc = (int)((tR - sqrt(tR * tR - 8.0 * (double)q)) * 0.5);
+          if (jc < 0) jc = 0;
+          if (jc > Rc - 1) jc = Rc - 1;
+          while (jc > 0 && upk(jc, jc, Rc) > q) jc--;
+          while (jc + 1 < Rc && upk(jc + 1, jc + 1, Rc) <= q) jc++;
+          const int ic = jc + (int)(q - upk(jc, jc, Rc));
+          const int pj = __ldg(rel + jc), pi = __ldg(rel + ic);
+          const double v = ldcg(Uc + q);
+          double* dst = (pj < w) ? F + (long long)pj * r + pi : U + upk(pi - w, pj - w, R);
+          *dst = ldcg(dst) + v;  // L1 is not coherent across CTAs: read through L2
+        }
+      }
+      grid.sync();
+      // ---------------- blocked factorisation ----------------
+      if (tid == 0) s_fail = -1;
+      for (int k0 = 0; k0 < w; k0 += HB) {
+        const int kb = (w - k0) < HB ? (w - k0) : HB;
+        // a. diagonal block in warp 0's registers (every CTA)
+        if (warp == 0) {
+          double a[HB];
+          const int row = k0 + lane;
+#pragma unroll
+          for (int c = 0; c < HB; c++)
+            a[c] = (lane < kb && c < kb && c <= lane) ? ldcg(F + (long long)(k0 + c) * r + row) : 0.0;
+#pragma unroll
+          for (int c = 0; c < HB; c++) {
+            if (c < kb) {
+              double lc[HB];
+#pragma unroll
+              for (int cc = 0; cc < HB; cc++) lc[cc] = __shfl_sync(0xffffffffu, a[c], cc);
+              const double d = lc[c];
+              const bool bad = !(d > 0.0) || !isfinite(d);
+              const double inv = bad ? nan_d() : rsqrt(d);
+              if (lane == 0) {
+                dsh[c] = inv;
+                if (bad && s_fail < 0) s_fail = k0 + c;
+              }
+              if (lane > c) {
+                const double l = a[c] * inv;
+                a[c] = l;
+#pragma unroll
+                for (int cc = c + 1; cc < HB; cc++) a[cc] = fma(-l, lc[cc] * inv, a[cc]);
+              } else if (lane == c) {
+                a[c] = d * inv;
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < HB; c++) Dg[c * HB + lane] = (c <= lane && lane < kb && c < kb) ? a[c] : 0.0;
+        }
+        __syncthreads();
+        // b. TRSM: rows i in [k0+kb, r), x = f L_kk^-T, column-oriented sweep per row
+        for (long long i = k0 + kb + gtid; i < r; i += gnt) {
+          double x[HB];
+#pragma unroll
+          for (int c = 0; c < HB; c++) x[c] = (c < kb) ? ldcg(F + (long long)(k0 + c) * r + i) : 0.0;
+#pragma unroll
+          for (int c = 0; c < HB; c++) {
+            if (c < kb) {
+              x[c] *= dsh[c];
+#pragma unroll
+              for (int t = c + 1; t < HB; t++) x[t] = fma(-x[c], Dg[c * HB + t], x[t]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < HB; c++)
+            if (c < kb) F[(long long)(k0 + c) * r + i] = x[c];
+        }
+        grid.sync();
+        // every CTA has finished reading the unfactored diagonal block: CTA 0 stores L_kk
+        if (blockIdx.x == 0) {
+          for (int q = tid; q < kb * kb; q += nt) {
+            const int c = q / kb, i = q % kb;
+            if (i >= c) F[(long long)(k0 + c) * r + k0 + i] = Dg[c * HB + i];
+          }
+          for (int q = tid; q < kb; q += nt) dinv[k0 + q] = dsh[q];
+        }
+        // c. trailing update in HT x HT tiles
+        const int j0 = k0 + kb, m = r - j0;
+        if (m > 0) {
+          const int ntl = (m + HT - 1) / HT;
+          const long long ntiles = (long long)ntl * (ntl + 1) / 2;
+          for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int tj = 0;
+            long long rem = t;
+            while (rem >= ntl - tj) { rem -= ntl - tj; tj++; }
+            const int ti = tj + (int)rem;
+            const int i0 = j0 + ti * HT, jj0 = j0 + tj * HT;
+            __syncthreads();
+            for (int q = tid; q < HB * HT; q += nt) {
+              const int k = q / HT, i = q % HT;
+              const bool kin = k < kb;
+              As[k * HT_LD + i] = (kin && i0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + i0 + i) : 0.0;
+              Bs[k * HT_LD + i] = (kin && jj0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + jj0 + i) : 0.0;
+            }
+            __syncthreads();
+            // 64 x 64 = 8 x 8 DMMA tiles; warp w owns tile row w x all 8 tile columns
+            double c0[8], c1[8];
+#pragma unroll
+            for (int y = 0; y < 8; y++) { c0[y] = 0.0; c1[y] = 0.0; }
+            for (int kk = 0; kk < kb; kk += 4) {
+              const int k = kk + (lane & 3);
+              const double a = As[k * HT_LD + warp * 8 + (lane >> 2)];
+              double bb[8];
+#pragma unroll
+              for (int y = 0; y < 8; y++) bb[y] = Bs[k * HT_LD + y * 8 + (lane >> 2)];
+#pragma unroll
+              for (int y = 0; y < 8; y++) dmma8x8x4(c0[y], c1[y], a, bb[y]);
+            }
+            const int i = i0 + warp * 8 + (lane >> 2);
+#pragma unroll
+            for (int y = 0; y < 8; y++) {
+              const int jb = jj0 + y * 8 + (lane & 3) * 2;
+              if (i < r) {
+                if (jb <= i) { double* p = front_at(F, U, r, w, i, jb); *p = ldcg(p) - c0[y]; }
+                if (jb + 1 <= i) { double* p = front_at(F, U, r, w, i, jb + 1); *p = ldcg(p) - c1[y]; }
+              }
+            }
+          }
+        }
+        grid.sync();
+      }
+      if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
+      if (gtid == 0) trace_stamp(P, 0, s, b, 1);
+    }
+  }
+}
+
+}  // namespace kkt

@@ -15,6 +15,7 @@
 #include "cg_kernels.cuh"
 #include "condense.cuh"
 #include "factor.cuh"
+#include "huge.cuh"
 #include "resid.cuh"
 #include "trsv.cuh"
 #include "plan.h"
@@ -84,6 +85,7 @@ struct kkt_plan {
   long long factor_smem_cap = 0;
   int fsmall_smem = 0, fbig_smem = 0, tsmall_smem = 0, tbig_smem = 0, pcap = 0;
   int g_fsmall = 1, g_fbig = 1, g_tsmall = 1, g_tbig = 1, g_bsmall = 1, g_bbig = 1;
+  int g_huge = 1, huge_smem = 0;
   long long launches = 0;
   // host-buffer path (kkt_step_host)
   double *hW = nullptr, *hJ = nullptr, *hSx = nullptr, *hSs = nullptr, *hD = nullptr,
@@ -283,7 +285,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
                                   &P.pa, &P.pb, &P.jrow, &P.kpos, &P.sn_first, &P.sn_rp,
                                   &P.sn_rows, &P.sn_rel, &P.sn_parent, &P.sn_cp, &P.sn_ch,
                                   &P.order, &P.order_s, &P.order_b, &P.up_s, &P.up_b,
-                                  &P.dn_b, &P.dn_s, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
+                                  &P.dn_b, &P.dn_s, &P.up_bf, &P.order_h, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
                                   &P.Jt_k, &P.Gt_end, &Jrp, &Jci};
   const std::vector<long long>* lv[] = {&P.sn_Lp, &P.sn_Up, &P.sn_uvp};
   size_t tot = 0;
@@ -316,6 +318,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   d.ns_s = (int)P.order_s.size(); d.ns_b = (int)P.order_b.size(); d.max_r_small = P.max_r_small;
   d.n_up_s = (int)P.up_s.size(); d.n_up_b = (int)P.up_b.size();
   d.n_dn_b = (int)P.dn_b.size(); d.n_dn_s = (int)P.dn_s.size();
+  d.n_up_bf = (int)P.up_bf.size(); d.n_h = (int)P.order_h.size();
   d.nnzL_stored = P.nnzL_stored; d.update_doubles = P.update_doubles;
   d.uvec_doubles = P.uvec_doubles; d.nprod = P.nprod;
   int k = 0;
@@ -324,7 +327,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   d.pa = I(); d.pb = I(); d.jrow = I(); d.kpos = I(); d.sn_first = I(); d.sn_rp = I();
   d.sn_rows = I(); d.sn_rel = I(); d.sn_parent = I(); d.sn_cp = I(); d.sn_ch = I();
   d.order = I(); d.order_s = I(); d.order_b = I(); d.up_s = I(); d.up_b = I(); d.dn_b = I();
-  d.dn_s = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
+  d.dn_s = I(); d.up_bf = I(); d.order_h = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
   d.Jt_k = I(); d.Gt_end = I(); d.Jrp = I(); d.Jci = I();
   d.sn_Lp = (const long long*)dptr[k++];
   d.sn_Up = (const long long*)dptr[k++];
@@ -357,6 +360,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   // ---- launch configuration ----
   long long maxneed = 0;
   for (int s : P.order_b) {
+    if (P.sn[s].huge) continue;
     long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = P.sn_first[s + 1] - P.sn_first[s], R = r - w;
     long long need_s = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
     maxneed = std::max(maxneed, need_s);
@@ -392,6 +396,15 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, ub, 1, &h->g_tbig));
   CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
   CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
+  {
+    const long long ubf = (long long)P.up_bf.size() * P.batch;
+    CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
+    h->huge_smem = HUGE_SMEM_DOUBLES * 8;
+    CUDA_TRY(cudaFuncSetAttribute(factor_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->huge_smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_huge_kernel, 256, h->huge_smem));
+    h->g_huge = std::max(1, occ) * h->sms;
+  }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->bound = true;
@@ -442,10 +455,20 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     LAUNCH_CHECK();
     h->launches++;
   }
-  if (!P.order_b.empty()) {
+  if (!P.up_bf.empty()) {
     factor_big_kernel<<<h->g_fbig, KKT_BNT, h->fbig_smem, h->ls>>>(
         h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 1 * KKT_CTL, h->fail, h->factor_smem_cap);
     LAUNCH_CHECK();
+    h->launches++;
+  }
+  if (!P.order_h.empty()) {
+    DevPlan dp = h->dp;
+    const double* kv = h->Kv;
+    double *lx = h->Lx, *ub = h->Ub, *dv = h->Dv;
+    int *cnt = h->facnt, *fail = h->fail;
+    void* args[] = {&dp, &kv, &lx, &ub, &dv, &cnt, &fail};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)factor_huge_kernel, dim3(h->g_huge), dim3(256), args,
+                                         (size_t)h->huge_smem, h->ls));
     h->launches++;
   }
   h->factored = true;

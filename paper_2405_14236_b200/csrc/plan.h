@@ -57,6 +57,7 @@ struct Plan {
   //   up_s: small leaves (phase-1 bottom-up start);  up_b: big supernodes with no big child
   //   dn_b: big roots (phase-1 top-down start);      dn_s: small roots + small children of big
   std::vector<int> up_s, up_b, dn_b, dn_s;
+  std::vector<int> up_bf, order_h;  // factor: big non-huge supernodes with no big non-huge child; huge list
   std::vector<SnInfo> sn;
   std::vector<SnInfo> chinfo;    // parallel to sn_ch: SnInfo of each child (one hop less)
   std::vector<int> sn_hsub;      // subtree height

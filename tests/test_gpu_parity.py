@@ -188,3 +188,41 @@ def test_step_host_matches_device_path():
                     inst.delta_w, inst.delta_c, inst.gamma, np.ascontiguousarray(inst.b), x, 10, 0.0)
     assert np.array_equal(x, x_dev)
     S.close()
+
+
+@pytest.mark.parametrize("hcap", ["1500", "4000"])
+def test_gpu_wide_front_path_parity(hcap, monkeypatch):
+    """Force medium fronts onto the whole-GPU cooperative path (huge.cuh) via the KKT_HCAP test
+    hook and check the solve against the oracle (C2 and the C2 stress variant)."""
+    from kkt_gpu import run_lifted, relerr
+    monkeypatch.setenv("KKT_HCAP", hcap)
+    for cfg in ("C2", "C2s"):
+        inst = make_config(cfg)
+        R = oracle.reference_solve(inst)
+        x, info, S = run_lifted(inst, max_refine=10)
+        assert info["status"] == 0, info
+        assert relerr(x, R["x"]) <= 1e-8, (cfg, relerr(x, R["x"]))
+        S.close()
+
+
+def test_lifted_acopf10000_parity():
+    """C3 pattern solved as LiftedKKT: exercises big fronts beyond one CTA's shared memory."""
+    from kkt_gpu import run_lifted, relerr
+    inst = acopf(10000, 3000, name="acopf10000-lifted")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, relerr(x, R["x"])
+    eta, _ = oracle.backward_error(inst, R["K"], inst.b, x)
+    assert eta <= 1e-10
+    S.close()
+
+
+def test_hykkt_parity_C3():
+    from kkt_gpu import run_hykkt, relerr
+    inst = make_config("C3", gamma=1e7)
+    R = oracle.reference_hykkt(inst)
+    dx, dy, info, S = run_hykkt(inst, max_outer=3)
+    assert info["status"] == 0, info
+    assert relerr(dx, R["dx"]) <= 1e-8 and relerr(dy, R["dy"]) <= 1e-8, (relerr(dx, R["dx"]), relerr(dy, R["dy"]))
+    S.close()
