@@ -544,10 +544,14 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
   // small (warp) / big (CTA) split, closed under descendants
   {
     std::vector<char> big(ns, 0);
+    // warp-per-supernode class threshold (<= KKT_SCAP, the per-warp shared-memory slice);
+    // KKT_SCLASS=<doubles> overrides it (tuning hook)
+    long long sclass = KKT_SCAP;
+    if (const char* e = getenv("KKT_SCLASS")) sclass = std::min<long long>(KKT_SCAP, std::max(0LL, atoll(e)));
     for (int s = 0; s < ns; s++) {
       long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = snf[s + 1] - snf[s], R = r - w;
       long long need = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);
-      if (need > KKT_SCAP) big[s] = 1;
+      if (need > sclass) big[s] = 1;
     }
     for (int s = 0; s < ns; s++)  // children precede parents
       if (big[s] && P.sn_parent[s] >= 0) big[P.sn_parent[s]] = 1;

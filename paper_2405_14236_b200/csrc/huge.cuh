@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
         }
       }
       grid.sync();
+      if (gtid == 0) trace_stamp(P, 0, s, b, 2);
       // ---------------- blocked factorisation ----------------
       if (tid == 0) s_fail = -1;
       for (int k0 = 0; k0 < w; k0 += HB) {
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
 #pragma unroll
           for (int c = 0; c < HB; c++) {
             if (c < kb) {
+              __syncwarp();
               double lc[HB];
 #pragma unroll
               for (int cc = 0; cc < HB; cc++) lc[cc] = __shfl_sync(0xffffffffu, a[c], cc);
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
           for (int c = 0; c < HB; c++) Dg[c * HB + lane] = (c <= lane && lane < kb && c < kb) ? a[c] : 0.0;
         }
         __syncthreads();
+        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 3);
         // b. TRSM: rows i in [k0+kb, r), x = f L_kk^-T, column-oriented sweep per row
         for (long long i = k0 + kb + gtid; i < r; i += gnt) {
           double x[HB];
@@ -137,6 +140,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
             if (c < kb) F[(long long)(k0 + c) * r + i] = x[c];
         }
         grid.sync();
+        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 4);
         // every CTA has finished reading the unfactored diagonal block: CTA 0 stores L_kk
         if (blockIdx.x == 0) {
           for (int q = tid; q < kb * kb; q += nt) {
@@ -168,6 +172,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
             double c0[8], c1[8];
 #pragma unroll
             for (int y = 0; y < 8; y++) { c0[y] = 0.0; c1[y] = 0.0; }
+            __syncwarp();
             for (int kk = 0; kk < kb; kk += 4) {
               const int k = kk + (lane & 3);
               const double a = As[k * HT_LD + warp * 8 + (lane >> 2)];
@@ -189,6 +194,8 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
           }
         }
         grid.sync();
+        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 5);
+        if (gtid == 0 && k0 == HB) trace_stamp(P, 0, s, b, 6);
       }
       if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
       if (gtid == 0) trace_stamp(P, 0, s, b, 1);
