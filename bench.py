@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--nvalues", type=int, default=4, help="distinct value sets cycled over steps")
+    ap.add_argument("--relax", default=None, help="amalgamation 'small,big,zero_frac' (perf tuning)")
     return ap.parse_args()
 
 
@@ -213,7 +214,11 @@ def run_ours(args, rank, world):
     inst = workload(args.workload, rank, 0, world)
     B = inst.batch
     hykkt = inst.m_eq > 0
-    S = K.KKTSolver.from_instance(inst)
+    kw = {}
+    if args.relax:
+        a_, b_, c_ = args.relax.split(",")
+        kw = dict(relax_small=int(a_), relax_big=int(b_), relax_zero_frac=float(c_))
+    S = K.KKTSolver.from_instance(inst, **kw)
     S.bind(local)
     stream = torch.cuda.current_stream(dev)
     d = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)

@@ -25,9 +25,40 @@ namespace kkt {
 // shared memory layout of factor_huge_kernel (doubles)
 constexpr int HUGE_SMEM_DOUBLES = HB * HB + HB + 2 * HB * HT_LD;
 
+// Group of CTAs cooperating on one front (contiguous blockIdx range); a group barrier is an
+// arrival counter in its own slot (targets grow with the generation), or __syncthreads for 1 CTA.
+struct CtaGroup {
+  int rank, size;
+  int* ctr;
+  int gen;
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    if (size > 1) {
+      if (threadIdx.x == 0) {
+        __threadfence();
+        gen++;
+        atomicAdd(ctr, 1);
+        while (ld_acquire(ctr) < gen * size) { }
+      }
+      __syncthreads();
+    }
+  }
+};
+
+// Level schedule of the huge fronts (built at kkt_bind for the launch grid G):
+//   hl_ptr[L]..hl_ptr[L+1]: entries of level L; entry e = {front s, first CTA, #CTAs, counter slot}
+// Fronts of one level are independent; a level with more fronts than CTAs is run round-robin by
+// single-CTA groups (ncta = 0 marks that mode: CTA c takes entries c, c+G, ...).
+struct HugeSched {
+  const int* lvl_ptr;   // [nlev+1]
+  const int4* ent;      // [nent]
+  int nlev;
+  int* ctr;             // [nent] group barrier counters (zeroed by the kernel)
+};
+
 __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const double* __restrict__ Kv_all,
                                                           double* Lx_all, double* U_all, double* Dv_all,
-                                                          int* cnt_all, int* fail_all) {
+                                                          int* cnt_all, int* fail_all, HugeSched H) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
@@ -37,10 +68,23 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
   double* Bs = As + HB * HT_LD;     // [HB][HT_LD] rows of tile j
   __shared__ int s_fail;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const long long gtid = (long long)blockIdx.x * nt + tid, gnt = (long long)gridDim.x * nt;
 
-  for (int hi = 0; hi < P.n_h; hi++) {
-    const int s = __ldg(P.order_h + hi);
+  for (int e = blockIdx.x; e < H.lvl_ptr[H.nlev]; e += gridDim.x) H.ctr[e] = 0;
+  grid.sync();
+  for (int L = 0; L < H.nlev; L++) {
+   const int e0 = H.lvl_ptr[L], e1 = H.lvl_ptr[L + 1];
+   const bool rr = (H.ent[e0].z == 0);  // round-robin singletons
+   for (int e = rr ? e0 + (int)blockIdx.x : e0; e < e1; e += rr ? (int)gridDim.x : 1) {
+    const int4 E = H.ent[e];
+    CtaGroup G;
+    if (rr) { G.rank = 0; G.size = 1; }
+    else {
+      if ((int)blockIdx.x < E.y || (int)blockIdx.x >= E.y + E.z) continue;
+      G.rank = blockIdx.x - E.y; G.size = E.z;
+    }
+    G.ctr = H.ctr + e; G.gen = 0;
+    const long long gtid = (long long)G.rank * nt + tid, gnt = (long long)G.size * nt;
+    const int s = E.x;
     const SnInfo I = P.sn[s];
     const int r = I.r, w = I.w, R = r - w;
     const long long pw = (long long)r * w;
@@ -56,7 +100,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
       // ---------------- assemble ----------------
       for (long long q = gtid; q < pw; q += gnt) F[q] = 0.0;
       for (long long q = gtid; q < usz; q += gnt) U[q] = 0.0;
-      grid.sync();
+      G.sync();
       for (long long k = I.k0 + gtid; k < I.k1; k += gnt) F[__ldg(P.kpos + k)] = __ldg(Kv + k);
       for (int ci = I.c0; ci < I.c1; ci++) {
         const SnInfo C = P.chinfo[ci];
@@ -64,7 +108,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
         const int* rel = P.sn_rel + C.rp0 + C.w;
         const double* Uc = Ub + C.Up;
         const long long tot = (long long)Rc * (Rc + 1) / 2;
-        grid.sync();
+        G.sync();
         for (long long q = gtid; q < tot; q += gnt) {
           // decode packed (column-major lower) index q -> (ic, jc)
           const double tR = 2.0 * Rc + 1.0;
@@ -80,7 +124,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
           *dst = ldcg(dst) + v;  // L1 is not coherent across CTAs: read through L2
         }
       }
-      grid.sync();
+      G.sync();
       if (gtid == 0) trace_stamp(P, 0, s, b, 2);
       // ---------------- blocked factorisation ----------------
       if (tid == 0) s_fail = -1;
@@ -139,10 +183,10 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
           for (int c = 0; c < HB; c++)
             if (c < kb) F[(long long)(k0 + c) * r + i] = x[c];
         }
-        grid.sync();
+        G.sync();
         if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 4);
         // every CTA has finished reading the unfactored diagonal block: CTA 0 stores L_kk
-        if (blockIdx.x == 0) {
+        if (G.rank == 0) {
           for (int q = tid; q < kb * kb; q += nt) {
             const int c = q / kb, i = q % kb;
             if (i >= c) F[(long long)(k0 + c) * r + k0 + i] = Dg[c * HB + i];
@@ -154,7 +198,7 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
         if (m > 0) {
           const int ntl = (m + HT - 1) / HT;
           const long long ntiles = (long long)ntl * (ntl + 1) / 2;
-          for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          for (long long t = G.rank; t < ntiles; t += G.size) {
             int tj = 0;
             long long rem = t;
             while (rem >= ntl - tj) { rem -= ntl - tj; tj++; }
@@ -193,13 +237,15 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
             }
           }
         }
-        grid.sync();
+        G.sync();
         if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 5);
         if (gtid == 0 && k0 == HB) trace_stamp(P, 0, s, b, 6);
       }
       if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
       if (gtid == 0) trace_stamp(P, 0, s, b, 1);
     }
+   }
+   grid.sync();  // level done: the next level's fronts may read these update matrices
   }
 }
 

@@ -92,6 +92,8 @@ struct kkt_plan {
          *hb = nullptr, *hx = nullptr;
   int* pinned_flags = nullptr;
   long long* trace_buf = nullptr;
+  void* huge_mem = nullptr;
+  HugeSched hsched{};
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -404,6 +406,58 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_huge_kernel, 256, h->huge_smem));
     h->g_huge = std::max(1, occ) * h->sms;
+    // level schedule of the huge fronts for this grid (see HugeSched in huge.cuh)
+    if (!P.order_h.empty()) {
+      const int G = h->g_huge;
+      std::vector<int> hl(P.ns, -1);
+      int nlev = 0;
+      for (int s : P.order_h) {  // postorder: children first
+        int l = 0;
+        for (int q = P.sn_cp[s]; q < P.sn_cp[s + 1]; q++) {
+          int c = P.sn_ch[q];
+          if (hl[c] >= 0) l = std::max(l, hl[c] + 1);
+        }
+        hl[s] = l;
+        nlev = std::max(nlev, l + 1);
+      }
+      std::vector<std::vector<int>> lv(nlev);
+      for (int s : P.order_h) lv[hl[s]].push_back(s);
+      std::vector<int> lptr(1, 0);
+      std::vector<int4> ent;
+      for (int L = 0; L < nlev; L++) {
+        const auto& F = lv[L];
+        const int k = (int)F.size();
+        if (k > G) {
+          for (int s : F) ent.push_back(make_int4(s, 0, 0, 0));
+        } else {
+          std::vector<double> wgt(k);
+          double tot = 0;
+          for (int i = 0; i < k; i++) {
+            double r = P.sn_rp[F[i] + 1] - P.sn_rp[F[i]], w = P.sn_first[F[i] + 1] - P.sn_first[F[i]];
+            wgt[i] = r * r * (w + 2.0);
+            tot += wgt[i];
+          }
+          std::vector<int> g(k);
+          int sum = 0;
+          for (int i = 0; i < k; i++) { g[i] = std::max(1, (int)(G * wgt[i] / tot)); sum += g[i]; }
+          while (sum > G) {  // trim the largest groups
+            int im = (int)(std::max_element(g.begin(), g.end()) - g.begin());
+            g[im]--; sum--;
+          }
+          int c0 = 0;
+          for (int i = 0; i < k; i++) { ent.push_back(make_int4(F[i], c0, g[i], 0)); c0 += g[i]; }
+        }
+        lptr.push_back((int)ent.size());
+      }
+      CUDA_TRY(cudaMalloc(&h->huge_mem, lptr.size() * sizeof(int) + ent.size() * sizeof(int4) * 2 + 256));
+      char* hb = (char*)h->huge_mem;
+      int4* d_ent = (int4*)hb;
+      CUDA_TRY(cudaMemcpy(d_ent, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      int* d_ctr = (int*)(hb + ent.size() * sizeof(int4));
+      int* d_lptr = (int*)(hb + ent.size() * sizeof(int4) * 2);
+      CUDA_TRY(cudaMemcpy(d_lptr, lptr.data(), lptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      h->hsched.lvl_ptr = d_lptr; h->hsched.ent = d_ent; h->hsched.nlev = nlev; h->hsched.ctr = d_ctr;
+    }
   }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -466,7 +520,8 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     const double* kv = h->Kv;
     double *lx = h->Lx, *ub = h->Ub, *dv = h->Dv;
     int *cnt = h->facnt, *fail = h->fail;
-    void* args[] = {&dp, &kv, &lx, &ub, &dv, &cnt, &fail};
+    HugeSched hs = h->hsched;
+    void* args[] = {&dp, &kv, &lx, &ub, &dv, &cnt, &fail, &hs};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)factor_huge_kernel, dim3(h->g_huge), dim3(256), args,
                                          (size_t)h->huge_smem, h->ls));
     h->launches++;
@@ -791,6 +846,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
       if (p) cudaFree(p);
     if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
     if (h->trace_buf) cudaFree(h->trace_buf);
+    if (h->huge_mem) cudaFree(h->huge_mem);
     if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
     if (h->cap) cudaStreamDestroy(h->cap);
   }
