@@ -114,7 +114,7 @@ __device__ __forceinline__ bool finish_dot(DevCtrl C, int b, double part, double
 // grid (KKT_NPART, batch)
 __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ z,
                          const double* __restrict__ sub, double* out, double* p, double* dy,
-                         DevCtrl C, int mode) {
+                         DevCtrl C, int mode, int first) {
   __shared__ double red[32];
   const int b = blockIdx.y;
   if (mode == 1 && C.cg_done[b]) return;
@@ -141,6 +141,7 @@ __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double*
   if (finish_dot(C, b, s, &tot)) {
     if (mode == 0) {
       C.rr[b] = tot; C.rr0[b] = tot; C.cg_iters[b] = 0;
+      if (first) C.rr0_first[b] = tot;
       C.cg_done[b] = (tot == 0.0) ? 1 : 0;
     } else {
       C.pq[b] = tot;
@@ -149,9 +150,12 @@ __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double*
   }
 }
 
-// dy += alpha p ; r -= alpha q ; rr_new = r.r ; convergence ||r|| <= rtol ||r0|| (R10)
+// dy += alpha p ; r -= alpha q ; rr_new = r.r ; convergence ||r|| <= rtol ||r0|| (R10).
+// Correction passes of the outer refinement (first == 0) stop at the absolute level
+// rtol ||r0 of the first pass|| -- the correction only has to be accurate relative to the
+// solution it corrects, not relative to its own (small) right-hand side.
 __global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const double* __restrict__ p,
-                                 const double* __restrict__ q, DevCtrl C, double rtol, int* status) {
+                                 const double* __restrict__ q, DevCtrl C, double rtol, int* status, int first) {
   __shared__ double red[32];
   const int b = blockIdx.y;
   if (C.cg_done[b]) return;
@@ -170,7 +174,7 @@ __global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const
     if (!isfinite(tot) || !isfinite(a)) {
       C.cg_done[b] = 1;
       atomicCAS(status, 0, 5 /* KKT_ERR_NONFINITE */);
-    } else if (sqrt(tot) <= rtol * sqrt(C.rr0[b])) {
+    } else if (sqrt(tot) <= rtol * sqrt(first ? C.rr0[b] : fmax(C.rr0[b], C.rr0_first[b]))) {
       C.cg_done[b] = 1;
     }
     C.beta[b] = tot / C.rr[b];

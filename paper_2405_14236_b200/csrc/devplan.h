@@ -72,6 +72,7 @@ struct DevCtrl {
   int* cg_iters_first;
   double* rr;                // r.r
   double* rr0;               // ||r_0||^2
+  double* rr0_first;         // ||r_0||^2 of the first HyKKT pass (absolute target of corrections)
   double* pq;                // p.q
   double* alpha;
   double* beta;

@@ -160,6 +160,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.cg_iters_first = c.take<int>(B);
   h->C.rr = c.take<double>(B);
   h->C.rr0 = c.take<double>(B);
+  h->C.rr0_first = c.take<double>(B);
   h->C.pq = c.take<double>(B);
   h->C.alpha = c.take<double>(B);
   h->C.beta = c.take<double>(B);
@@ -646,7 +647,7 @@ static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, do
   // z = K_gamma^-1 s ; r = G z - rbar2 ; p = r ; dy = 0
   TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, nullptr));
   dim3 gg(KKT_NPART, P.batch);
-  g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0);
+  g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0, first ? 1 : 0);
   LAUNCH_CHECK();
   h->launches++;
   const int chunk = 8;
@@ -657,10 +658,10 @@ static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, do
       gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
       LAUNCH_CHECK();
       TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1);
+      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1, 0);
       LAUNCH_CHECK();
       cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
-                                                   rtol, h->status);
+                                                   rtol, h->status, first ? 1 : 0);
       LAUNCH_CHECK();
       cg_p_kernel<<<grid_for((long long)P.batch * P.m_eq, 256, h->sms), 256, 0, h->ls>>>(
           P.batch, P.m_eq, h->cp, h->cr, h->C);

@@ -215,10 +215,11 @@ __device__ __forceinline__ int pop_task(int* ctl, const int* init, int ninit_nod
   if (h < ninit) return __ldg(init + h / batch) * batch + h % batch;
   const int slot = h - ninit;
   if (slot >= total) return -1;
-  for (;;) {
+  for (int polls = 1;; polls++) {
     if (ld_volatile(Q.flag + slot)) break;
-    if (ld_volatile(ctl + 8)) return -1;  // every task of the phase is done
-    __nanosleep(64);
+    // every task of the phase done?  (checked every 16th poll: one hot word for all pollers)
+    if ((polls & 15) == 0 && ld_volatile(ctl + 8)) return -1;
+    __nanosleep(32);
   }
   __threadfence();
   const int task = ld_volatile(Q.q + slot);
