@@ -341,6 +341,12 @@ def run_ours(args, rank, world):
     roof_cond = {"bound": "hbm", "achieved": c_ach, "peak": hbm_peak, "unit": "GB/s", "frac": c_ach / hbm_peak,
                  "traffic": None, "kernel": "condense_kernel (+dweights_kernel)"}
     roofs = {"condense": roof_cond, "factor": roof_factor, "solve": roof_solve}
+    tpath = os.path.join(ROOT, "profiles", f"r01_traffic_{args.workload}.json")
+    if os.path.exists(tpath):  # DRAM bytes per phase from one ncu capture (cold caches per launch)
+        tr = json.load(open(tpath))
+        for k_, r_ in roofs.items():
+            r_["traffic"] = tr["dram_bytes_per_step"].get(k_) / max(B, 1) if tr["dram_bytes_per_step"].get(k_) else None
+            r_["traffic_note"] = "ncu dram__bytes_read+write per step of this phase (" + tr["source"] + ")"
     dom = ["condense", "factor", "solve"][int(np.argmax(ph_mean))]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
