@@ -163,6 +163,29 @@ kkt_status kkt_step_host(kkt_handle h, const double *W_vals, const double *J_val
                          double delta_w, double delta_c, double gamma, const double *b,
                          double *x, int max_refine, double tol_bwd);
 
+/*
+ * kkt_recover -- directions of the eliminated blocks after the condensed solve (P:421-423,
+ * SURVEY §8(f) NEXT-1), for the inequality rows [m_eq, m) of J (= H), with the values of the
+ * last kkt_condense:
+ *   dz = -C r2 + D_H (H dx + r4),  ds = -(D_s + dw I)^-1 (r2 + dz),
+ *   C = (I + dc (D_s + dw I))^-1,  D_H = (D_s + dw I) C.
+ * [device] r2, r4 [m - m_eq] (K2 right-hand-side blocks), dx [n] (the condensed
+ * solution) in; dz, ds [m - m_eq] out (batch-strided).  D overrides are not supported here
+ * (KKT_ERR_STATE if kkt_condense was given D).  Non-blocking.
+ */
+kkt_status kkt_recover(kkt_handle h, const double *r2, const double *r4, const double *dx,
+                       double *dz, double *ds);
+
+/*
+ * kkt_recover_bounds -- bound-multiplier directions:
+ *   du = -X^-1 (U dx - mu e) - u   [n],   dv = -S^-1 (V ds - mu e) - v   [m - m_eq].
+ * [device] x, u, dx [n]; s, v, ds [m - m_eq] in; du [n], dv [m - m_eq] out (batch-strided;
+ * s/v/ds/dv may be NULL when m == m_eq).  Non-blocking.
+ */
+kkt_status kkt_recover_bounds(kkt_handle h, const double *x, const double *u, const double *s,
+                              const double *v, double mu, const double *dx, const double *ds,
+                              double *du, double *dv);
+
 /* Test/debug export of the condensed matrix of batch instance `inst`, lower CSC in ORIGINAL
  * indices: [host] Kp[n+1], Ki[nnzK], Kv[nnzK] (any may be NULL).  Blocking. */
 kkt_status kkt_get_condensed(kkt_handle h, int inst, int *Kp, int *Ki, double *Kv);

@@ -205,4 +205,44 @@ __global__ void cg_finish_kernel(int batch, DevCtrl C, int first, int* status) {
   if (!C.cg_done[b]) atomicCAS(status, 0, 4 /* KKT_ERR_NOT_CONVERGED */);
 }
 
+// ---------------------------------------------------------------- NEXT-1 recovery
+// dz = -C r2 + D_H (H dx + r4), ds = -(D_s + dw)^-1 (r2 + dz), one thread per row
+__global__ void recover_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ Ss,
+                               double dw, double dc, const double* __restrict__ r2,
+                               const double* __restrict__ r4, const double* __restrict__ dx, double* dz,
+                               double* ds) {
+  const int mi = P.m - P.m_eq;
+  long long total = (long long)P.batch * mi;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / mi), q = (int)(idx % mi), row = P.m_eq + q;
+    const double* J = Jv + (long long)b * P.nnzJ;
+    const double* x = dx + (long long)b * P.n;
+    double hx = 0.0;
+    for (int p = P.Jrp[row]; p < P.Jrp[row + 1]; p++) hx = fma(J[p], x[P.Jci[p]], hx);
+    const double t = Ss[idx] + dw;               // D_s + dw
+    const double Cr = 1.0 / fma(dc, t, 1.0);     // C
+    const double DH = t * Cr;                    // D_H
+    const double z = fma(DH, hx + r4[idx], -Cr * r2[idx]);
+    dz[idx] = z;
+    ds[idx] = -(r2[idx] + z) / t;
+  }
+}
+
+// du = -(U dx - mu)/X - u ;  dv = -(V ds - mu)/S - v
+__global__ void recover_bounds_kernel(long long nx, long long ns, const double* __restrict__ x,
+                                      const double* __restrict__ u, const double* __restrict__ s,
+                                      const double* __restrict__ v, double mu,
+                                      const double* __restrict__ dx, const double* __restrict__ ds,
+                                      double* du, double* dv) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nx + ns;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (idx < nx) du[idx] = -fma(u[idx], dx[idx], -mu) / x[idx] - u[idx];
+    else {
+      const long long k = idx - nx;
+      dv[k] = -fma(v[k], ds[k], -mu) / s[k] - v[k];
+    }
+  }
+}
+
 }  // namespace kkt

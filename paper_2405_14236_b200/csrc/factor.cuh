@@ -109,8 +109,7 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I
 // =====================================================================================
 __device__ __forceinline__ bool warp_signal_parent(const SnInfo& I, const SnInfo& Ip, int* cnt,
                                                    int lane, bool phase_small) {
-  __threadfence();
-  __syncwarp();
+  __syncwarp();  // lanes' writes are ordered before lane 0's release (acq_rel / release atomic)
   int last = 0;
   if (lane == 0) {
     if (phase_small && Ip.big) {

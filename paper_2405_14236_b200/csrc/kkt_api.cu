@@ -398,6 +398,11 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
   CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, ub, 1, &h->g_tbig));
   CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
+  {  // top-down workers mostly wait on the queue: cap them so idle pollers do not crowd the SMs
+    int cap = h->sms;
+    if (const char* e = getenv("KKT_BWD_CTAS")) cap = std::max(1, atoi(e));
+    h->g_bsmall = std::min(h->g_bsmall, cap);
+  }
   CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
@@ -769,6 +774,37 @@ extern "C" kkt_status kkt_step_host(kkt_handle h, const double* W_vals, const do
   TRY(kkt_solve(h, h->hb, h->hx, max_refine, tol_bwd));
   CUDA_TRY(cudaMemcpyAsync(x, h->hx, B * P.n * 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_recover(kkt_handle h, const double* r2, const double* r4, const double* dx,
+                                   double* dz, double* ds) {
+  if (!h || !dx) return KKT_ERR_ARG;
+  if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
+  if (h->Dov) { g_err = "kkt_recover needs the Sigma_s form of kkt_condense (no D override)"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  const long long tot = (long long)P.batch * (P.m - P.m_eq);
+  if (tot == 0) return KKT_OK;
+  if (!r2 || !r4 || !dz || !ds) return KKT_ERR_ARG;
+  recover_kernel<<<grid_for(tot, 256, h->sms), 256, 0, h->ls>>>(h->dp, h->Jv, h->Ss, h->dw, h->dc, r2, r4,
+                                                                  dx, dz, ds);
+  LAUNCH_CHECK();
+  h->launches = 1;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_recover_bounds(kkt_handle h, const double* x, const double* u, const double* s,
+                                          const double* v, double mu, const double* dx, const double* ds,
+                                          double* du, double* dv) {
+  if (!h || !x || !u || !dx || !du) return KKT_ERR_ARG;
+  if (!h->bound) { g_err = "kkt_bind first"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  const long long nx = (long long)P.batch * P.n, ns = (long long)P.batch * (P.m - P.m_eq);
+  if (ns > 0 && (!s || !v || !ds || !dv)) return KKT_ERR_ARG;
+  recover_bounds_kernel<<<grid_for(nx + ns, 256, h->sms), 256, 0, h->ls>>>(nx, ns, x, u, s, v, mu, dx, ds,
+                                                                            du, dv);
+  LAUNCH_CHECK();
+  h->launches = 1;
   return KKT_OK;
 }
 

@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve",
-           "kkt_sync_info", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
+           "kkt_sync_info", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
            "kkt_last_error", "kkt_destroy"]
 
 
@@ -77,6 +77,8 @@ def lib(build_if_missing: bool = True):
                               C.POINTER(D)],
             "kkt_step_host": [P, P, P, P, P, P, D, D, D, P, P, I, D],
             "kkt_get_condensed": [P, I, P, P, P],
+            "kkt_recover": [P, P, P, P, P, P],
+            "kkt_recover_bounds": [P, P, P, P, P, D, P, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
             "kkt_get_trace": [P, P],
@@ -171,6 +173,15 @@ def kkt_sync_info(h):
                 fail_col=fc.value, refine_iters=it.value, cg_iters=cg.value, bwd_err=be.value)
 
 
+def kkt_recover(h, r2, r4, dx, dz, ds):
+    _chk(lib().kkt_recover(h, _ptr(r2), _ptr(r4), _ptr(dx), _ptr(dz), _ptr(ds)), "kkt_recover")
+
+
+def kkt_recover_bounds(h, x, u, s, v, mu, dx, ds, du, dv):
+    _chk(lib().kkt_recover_bounds(h, _ptr(x), _ptr(u), _ptr(s), _ptr(v), float(mu), _ptr(dx), _ptr(ds),
+                                  _ptr(du), _ptr(dv)), "kkt_recover_bounds")
+
+
 def kkt_step_host(h, W_vals, J_vals, Sigma_x, Sigma_s, D, delta_w, delta_c, gamma, b, x,
                   max_refine=10, tol_bwd=0.0):
     _chk(lib().kkt_step_host(h, _ptr(W_vals), _ptr(J_vals), _ptr(Sigma_x), _ptr(Sigma_s), _ptr(D),
@@ -257,6 +268,12 @@ class KKTSolver:
 
     def hykkt_solve(self, rbar1, rbar2, dx, dy, cg_rtol=1e-12, cg_maxit=0, max_outer_refine=2):
         hykkt_solve(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine)
+
+    def recover(self, r2, r4, dx, dz, ds):
+        kkt_recover(self.h, r2, r4, dx, dz, ds)
+
+    def recover_bounds(self, x, u, s, v, mu, dx, ds, du, dv):
+        kkt_recover_bounds(self.h, x, u, s, v, mu, dx, ds, du, dv)
 
     def sync_info(self):
         return kkt_sync_info(self.h)

@@ -226,3 +226,52 @@ def test_hykkt_parity_C3():
     assert info["status"] == 0, info
     assert relerr(dx, R["dx"]) <= 1e-8 and relerr(dy, R["dy"]) <= 1e-8, (relerr(dx, R["dx"]), relerr(dy, R["dy"]))
     S.close()
+
+
+@pytest.mark.parametrize("seed,dw,dc", [(3, 0.0, 0.0), (4, 1e-3, 1e-2)])
+def test_recover_matches_augmented_K2(seed, dw, dc):
+    """NEXT-1: condensed solve on the GPU + kkt_recover reproduces the dense K2
+    solution for all of dx, ds, dz; kkt_recover_bounds satisfies the K3 rows
+    U dx + X du = -(X u - mu e) and V ds + S dv = -(S v - mu e)."""
+    import torch
+    from oracle import dense
+    from kkt_gpu import dev
+    import paper_2405_14236_b200 as K
+    rng = np.random.default_rng(seed)
+    n, mi = 24, 14
+    inst = tiny_random(n, mi, 0, seed=seed, Xi=1e-2, delta_w=dw, delta_c=dc)
+    Ds = rng.uniform(0.1, 10.0, mi)
+    inst.Sigma_s = Ds
+    H = dense.dense_J(inst)
+    W = dense.dense_W(inst)
+    K2 = dense.k2_matrix(W, np.zeros((0, n)), H, inst.Sigma_x, Ds, dw, dc)
+    r1, r2, r4 = rng.standard_normal(n), rng.standard_normal(mi), rng.standard_normal(mi)
+    sol = np.linalg.solve(K2, -np.concatenate([r1, r2, r4]))
+    dx2, ds2, dz2 = sol[:n], sol[n:n + mi], sol[n + mi:]
+    Cd = 1.0 / (1.0 + dc * (Ds + dw)); DH = (Ds + dw) * Cd
+    rb1 = -(r1 + H.T @ (DH * r4 - Cd * r2))
+    S = K.KKTSolver.from_instance(inst).bind(0)
+    t = [dev(a, "cuda:0") for a in (inst.W_vals, inst.J_vals, inst.Sigma_x, Ds, rb1, r2, r4)]
+    W_, J_, Sx_, Ss_, b_, r2_, r4_ = t
+    x_ = torch.zeros_like(b_); dz_ = torch.zeros_like(r2_); ds_ = torch.zeros_like(r2_)
+    S.condense(W_, J_, Sx_, Ss_, None, dw, dc, 0.0)
+    S.factor()
+    S.solve(b_, x_, 10, 0.0)
+    S.recover(r2_, r4_, x_, dz_, ds_)
+    info = S.sync_info()
+    assert info["status"] == 0
+    scale = np.abs(sol).max()
+    for a, b in ((x_, dx2), (dz_, dz2), (ds_, ds2)):
+        assert np.abs(a.cpu().numpy() - b).max() <= 1e-9 * scale
+    # bound multipliers
+    xv, uv = rng.uniform(0.5, 2, n), rng.uniform(0.5, 2, n)
+    sv, vv = rng.uniform(0.5, 2, mi), rng.uniform(0.5, 2, mi)
+    mu = 0.1
+    du_ = torch.zeros_like(x_); dv_ = torch.zeros_like(r2_)
+    S.recover_bounds(dev(xv, "cuda:0"), dev(uv, "cuda:0"), dev(sv, "cuda:0"), dev(vv, "cuda:0"), mu,
+                     x_, ds_, du_, dv_)
+    du, dv = du_.cpu().numpy(), dv_.cpu().numpy()
+    dxv, dsv = x_.cpu().numpy(), ds_.cpu().numpy()
+    assert np.abs(uv * dxv + xv * du + (xv * uv - mu)).max() <= 1e-12 * (1 + np.abs(uv * dxv).max())
+    assert np.abs(vv * dsv + sv * dv + (sv * vv - mu)).max() <= 1e-12 * (1 + np.abs(vv * dsv).max())
+    S.close()

@@ -52,7 +52,7 @@ int main() {
   long long* d; double* c; cudaMalloc(&d, 64); cudaMalloc(&c, 64);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
   for (int m : {16, 32, 40, 64}) {
-    bench<<<1, 32, 150 * 1024>>>(m, 20, d, c);
+    bench<<<148, 32, 150 * 1024>>>(m, 400, d, c);
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("m=%d: minimal shuffle version %lld cyc, library trailing_update_rows %lld cyc\n", m, h[0], h[1]);
   }
