@@ -38,7 +38,8 @@ struct CtaGroup {
         __threadfence();
         gen++;
         atomicAdd(ctr, 1);
-        while (ld_acquire(ctr) < gen * size) { }
+        while (ld_volatile(ctr) < gen * size) { }
+        __threadfence();
       }
       __syncthreads();
     }
@@ -109,19 +110,35 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
         const double* Uc = Ub + C.Up;
         const long long tot = (long long)Rc * (Rc + 1) / 2;
         G.sync();
-        for (long long q = gtid; q < tot; q += gnt) {
-          // decode packed (column-major lower) index q -> (ic, jc)
-          const double tR = 2.0 * Rc + 1.0;
-          int jc = (int)((tR - sqrt(tR * tR - 8.0 * (double)q)) * 0.5);
-          if (jc < 0) jc = 0;
-          if (jc > Rc - 1) jc = Rc - 1;
-          while (jc > 0 && upk(jc, jc, Rc) > q) jc--;
-          while (jc + 1 < Rc && upk(jc + 1, jc + 1, Rc) <= q) jc++;
-          const int ic = jc + (int)(q - upk(jc, jc, Rc));
-          const int pj = __ldg(rel + jc), pi = __ldg(rel + ic);
-          const double v = ldcg(Uc + q);
-          double* dst = (pj < w) ? F + (long long)pj * r + pi : U + upk(pi - w, pj - w, R);
-          *dst = ldcg(dst) + v;  // L1 is not coherent across CTAs: read through L2
+        for (long long q0 = gtid; q0 < tot; q0 += gnt * 8) {
+          // 8 entries per thread per round: all loads (child values, relative indices, old
+          // front values) are issued before the stores
+          double* dst[8];
+          double val[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const long long q = q0 + (long long)u * gnt;
+            dst[u] = nullptr;
+            if (q < tot) {
+              // decode packed (column-major lower) index q -> (ic, jc)
+              const double tR = 2.0 * Rc + 1.0;
+              int jc = (int)((tR - sqrt(tR * tR - 8.0 * (double)q)) * 0.5);
+              if (jc < 0) jc = 0;
+              if (jc > Rc - 1) jc = Rc - 1;
+              while (jc > 0 && upk(jc, jc, Rc) > q) jc--;
+              while (jc + 1 < Rc && upk(jc + 1, jc + 1, Rc) <= q) jc++;
+              const int ic = jc + (int)(q - upk(jc, jc, Rc));
+              const int pj = __ldg(rel + jc), pi = __ldg(rel + ic);
+              val[u] = ldcg(Uc + q);
+              dst[u] = (pj < w) ? F + (long long)pj * r + pi : U + upk(pi - w, pj - w, R);
+            }
+          }
+          double old[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) old[u] = dst[u] ? ldcg(dst[u]) : 0.0;  // L1 is not coherent
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (dst[u]) *dst[u] = old[u] + val[u];
         }
       }
       G.sync();
@@ -205,11 +222,22 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
             const int ti = tj + (int)rem;
             const int i0 = j0 + ti * HT, jj0 = j0 + tj * HT;
             __syncthreads();
-            for (int q = tid; q < HB * HT; q += nt) {
-              const int k = q / HT, i = q % HT;
-              const bool kin = k < kb;
-              As[k * HT_LD + i] = (kin && i0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + i0 + i) : 0.0;
-              Bs[k * HT_LD + i] = (kin && jj0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + jj0 + i) : 0.0;
+            {  // stage the two 32 x 64 operand panels: all loads in flight before the stores
+              constexpr int PER = (HB * HT) / 256;  // 8 elements of each panel per thread
+              double va[PER], vb[PER];
+#pragma unroll
+              for (int u = 0; u < PER; u++) {
+                const int q = tid + u * 256, k = q / HT, i = q % HT;
+                const bool kin = k < kb;
+                va[u] = (kin && i0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + i0 + i) : 0.0;
+                vb[u] = (kin && jj0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + jj0 + i) : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < PER; u++) {
+                const int q = tid + u * 256, k = q / HT, i = q % HT;
+                As[k * HT_LD + i] = va[u];
+                Bs[k * HT_LD + i] = vb[u];
+              }
             }
             __syncthreads();
             // 64 x 64 = 8 x 8 DMMA tiles; warp w owns tile row w x all 8 tile columns
@@ -227,13 +255,21 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
               for (int y = 0; y < 8; y++) dmma8x8x4(c0[y], c1[y], a, bb[y]);
             }
             const int i = i0 + warp * 8 + (lane >> 2);
+            // read-modify-write of the 16 outputs: all 16 loads issued before the stores
+            double* pp[16];
+            double old[16];
 #pragma unroll
             for (int y = 0; y < 8; y++) {
               const int jb = jj0 + y * 8 + (lane & 3) * 2;
-              if (i < r) {
-                if (jb <= i) { double* p = front_at(F, U, r, w, i, jb); *p = ldcg(p) - c0[y]; }
-                if (jb + 1 <= i) { double* p = front_at(F, U, r, w, i, jb + 1); *p = ldcg(p) - c1[y]; }
-              }
+              pp[2 * y] = (i < r && jb <= i) ? front_at(F, U, r, w, i, jb) : nullptr;
+              pp[2 * y + 1] = (i < r && jb + 1 <= i) ? front_at(F, U, r, w, i, jb + 1) : nullptr;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; e++) old[e] = pp[e] ? ldcg(pp[e]) : 0.0;
+#pragma unroll
+            for (int y = 0; y < 8; y++) {
+              if (pp[2 * y]) *pp[2 * y] = old[2 * y] - c0[y];
+              if (pp[2 * y + 1]) *pp[2 * y + 1] = old[2 * y + 1] - c1[y];
             }
           }
         }

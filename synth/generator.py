@@ -388,6 +388,7 @@ CONFIGS = {
     "C3": "ACOPF ~10,000 buses, HyKKT (gamma=1e4..1e7)",
     "C4": "ACOPF ~78,484 buses, LiftedKKT",
     "C5": "batch of 512 x ACOPF 500 buses (same pattern)",
+    "C6": "NEXT-3: COPS bearing 800x800 (n=640,000, bound-only)",
 }
 
 
@@ -417,4 +418,6 @@ def make_config(name: str, instance: int = 0, gamma: float = 1e7, batch: int | N
         # a partition reproduces the same instances as the full batch (bitwise)
         return acopf(500, seed, batch=512 if batch is None else batch, name="C5-acopf500-batch",
                      _pattern_rng_seed=5000, **kw)
+    if name == "C6":
+        return bearing(800, 800, seed=seed, **kw)
     raise KeyError(name)

@@ -275,3 +275,15 @@ def test_recover_matches_augmented_K2(seed, dw, dc):
     assert np.abs(uv * dxv + xv * du + (xv * uv - mu)).max() <= 1e-12 * (1 + np.abs(uv * dxv).max())
     assert np.abs(vv * dsv + sv * dv + (sv * vv - mu)).max() <= 1e-12 * (1 + np.abs(vv * dsv).max())
     S.close()
+
+
+def test_bearing_120_parity():
+    """NEXT-3 workload family (COPS bearing) at an oracle-checkable size."""
+    from kkt_gpu import run_lifted, relerr
+    from synth.generator import bearing
+    inst = bearing(120, 120, seed=6000)
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8
+    S.close()
