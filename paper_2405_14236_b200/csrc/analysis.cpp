@@ -565,13 +565,11 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       bool leaf = P.sn_cp[s + 1] == P.sn_cp[s];
       if (!big[s] && leaf) P.up_s.push_back(s);
       if (big[s] && nbigch[s] == 0) P.up_b.push_back(s);
-      if (big[s] && par < 0) P.dn_b.push_back(s);
       if (!big[s] && (par < 0 || big[par])) P.dn_s.push_back(s);
     }
     auto by_height = [&](int a, int b) {
       return P.sn_hsub[a] != P.sn_hsub[b] ? P.sn_hsub[a] > P.sn_hsub[b] : a < b;
     };
-    std::sort(P.dn_b.begin(), P.dn_b.end(), by_height);
     std::sort(P.dn_s.begin(), P.dn_s.end(), by_height);
     std::sort(P.up_s.begin(), P.up_s.end(), [&](int a, int b) {  // deepest chains first
       int ha = 0, hb = 0;
@@ -596,9 +594,12 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       for (int s = 0; s < ns; s++)
         if (big[s] && !huge[s] && P.sn_parent[s] >= 0) nbn[P.sn_parent[s]]++;
       for (int s = 0; s < ns; s++) {
+        const int par = P.sn_parent[s];
         if (big[s] && !huge[s] && nbn[s] == 0) P.up_bf.push_back(s);
+        if (big[s] && !huge[s] && (par < 0 || huge[par])) P.dn_b.push_back(s);
         if (huge[s]) P.order_h.push_back(s);  // postorder = topological
       }
+      std::sort(P.dn_b.begin(), P.dn_b.end(), by_height);
     }
     P.sn.resize(ns);
     for (int s = 0; s < ns; s++) {

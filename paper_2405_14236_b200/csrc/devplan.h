@@ -29,7 +29,7 @@ static_assert(sizeof(SnInfo) == 64, "SnInfo must be 64 bytes");
 struct DevPlan {
   int n, m, m_eq, nnzW, nnzJ, nnzK, ns, batch;
   int max_front;
-  int ns_s, ns_b;              // small / big supernode counts
+  int ns_s, ns_b, ns_bn;       // small / big / big non-huge supernode counts
   int max_r_small;             // largest front among small supernodes
   long long nnzL_stored, update_doubles, uvec_doubles, nprod;
   const int *perm, *iperm;
@@ -42,7 +42,7 @@ struct DevPlan {
   const int *up_s, *up_b, *dn_b, *dn_s;   // see plan.h
   long long* trace;              // optional [3][ns][2] globaltimer stamps (KKT_TRACE=1), else NULL
   int n_up_s, n_up_b, n_dn_b, n_dn_s;
-  const int *up_bf, *order_h;    // factor-only: big non-huge start list; huge supernodes in order
+  const int *up_bf, *order_h;    // big non-huge bottom-up start list; huge supernodes in order
   int n_up_bf, n_h;
   const long long *sn_Lp, *sn_Up, *sn_uvp;
   const int *Wf_p, *Wf_c, *Wf_k, *Jt_p, *Jt_r, *Jt_k, *Gt_end;

@@ -47,7 +47,8 @@ struct CtaGroup {
 };
 
 // Level schedule of the huge fronts (built at kkt_bind for the launch grid G):
-//   hl_ptr[L]..hl_ptr[L+1]: entries of level L; entry e = {front s, first CTA, #CTAs, counter slot}
+//   lvl_ptr[L]..lvl_ptr[L+1]: entries of level L; entry e = {front s, first CTA, #CTAs, offset of
+//   the front's block flags (hsolve.cuh)}; the group barrier counter of entry e is ctr[e]
 // Fronts of one level are independent; a level with more fronts than CTAs is run round-robin by
 // single-CTA groups (ncta = 0 marks that mode: CTA c takes entries c, c+G, ...).
 struct HugeSched {
@@ -55,6 +56,7 @@ struct HugeSched {
   const int4* ent;      // [nent]
   int nlev;
   int* ctr;             // [nent] group barrier counters (zeroed by the kernel)
+  int nflag;            // sum over entries of ceil(w / 32) (solve block flags per direction)
 };
 
 __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const double* __restrict__ Kv_all,

@@ -15,7 +15,7 @@
 #include "cg_kernels.cuh"
 #include "condense.cuh"
 #include "factor.cuh"
-#include "huge.cuh"
+#include "hsolve.cuh"
 #include "resid.cuh"
 #include "trsv.cuh"
 #include "plan.h"
@@ -93,7 +93,10 @@ struct kkt_plan {
   int* pinned_flags = nullptr;
   long long* trace_buf = nullptr;
   void* huge_mem = nullptr;
-  HugeSched hsched{};
+  HugeSched hsched{}, hsched_s{};  // factor / solve grids
+  void* hsolve_mem = nullptr;
+  int g_hsolve = 1;
+  int* hflags = nullptr;  // [2 * hsched.nflag] block flags of the huge-front solves
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -267,6 +270,69 @@ static void rebuild_J_csr(const Plan& P, std::vector<int>& Jrp, std::vector<int>
 template <class T>
 static size_t vbytes(const std::vector<T>& v) { return align_up(v.size() * sizeof(T) + 1); }
 
+// Level schedule of the huge fronts for a cooperative grid of G CTAs (see HugeSched in
+// huge.cuh): one allocation holding the entries, their barrier counters, the level pointers and
+// 2 x nflag block flags of the solves (hsolve.cuh).
+static kkt_status build_huge_sched(kkt_plan* h, int G, HugeSched* out, void** mem) {
+  const Plan& P = h->P;
+  std::vector<int> hl(P.ns, -1);
+  int nlev = 0;
+  for (int s : P.order_h) {  // postorder: children first
+    int l = 0;
+    for (int q = P.sn_cp[s]; q < P.sn_cp[s + 1]; q++) {
+      int c = P.sn_ch[q];
+      if (hl[c] >= 0) l = std::max(l, hl[c] + 1);
+    }
+    hl[s] = l;
+    nlev = std::max(nlev, l + 1);
+  }
+  std::vector<std::vector<int>> lv(nlev);
+  for (int s : P.order_h) lv[hl[s]].push_back(s);
+  std::vector<int> lptr(1, 0);
+  std::vector<int4> ent;
+  int nflag = 0;
+  auto flag_off = [&](int s) {  // block flags of front s
+    const int o = nflag;
+    nflag += (P.sn_first[s + 1] - P.sn_first[s] + 31) / 32;
+    return o;
+  };
+  for (int L = 0; L < nlev; L++) {
+    const auto& F = lv[L];
+    const int k = (int)F.size();
+    if (k > G) {
+      for (int s : F) ent.push_back(make_int4(s, 0, 0, flag_off(s)));
+    } else {
+      std::vector<double> wgt(k);
+      double tot = 0;
+      for (int i = 0; i < k; i++) {
+        double r = P.sn_rp[F[i] + 1] - P.sn_rp[F[i]], w = P.sn_first[F[i] + 1] - P.sn_first[F[i]];
+        wgt[i] = r * r * (w + 2.0);
+        tot += wgt[i];
+      }
+      std::vector<int> g(k);
+      int sum = 0;
+      for (int i = 0; i < k; i++) { g[i] = std::max(1, (int)(G * wgt[i] / tot)); sum += g[i]; }
+      while (sum > G) {  // trim the largest groups
+        int im = (int)(std::max_element(g.begin(), g.end()) - g.begin());
+        g[im]--; sum--;
+      }
+      int c0 = 0;
+      for (int i = 0; i < k; i++) { ent.push_back(make_int4(F[i], c0, g[i], flag_off(F[i]))); c0 += g[i]; }
+    }
+    lptr.push_back((int)ent.size());
+  }
+  const size_t hbytes = ent.size() * sizeof(int4) * 2 + (lptr.size() + 2 * (size_t)nflag) * sizeof(int) + 256;
+  CUDA_TRY(cudaMalloc(mem, hbytes));
+  char* hb = (char*)*mem;
+  int4* d_ent = (int4*)hb;
+  CUDA_TRY(cudaMemcpy(d_ent, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  int* d_ctr = (int*)(hb + ent.size() * sizeof(int4));
+  int* d_lptr = (int*)(hb + ent.size() * sizeof(int4) * 2);
+  CUDA_TRY(cudaMemcpy(d_lptr, lptr.data(), lptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  out->lvl_ptr = d_lptr; out->ent = d_ent; out->nlev = nlev; out->ctr = d_ctr; out->nflag = nflag;
+  return KKT_OK;
+}
+
 extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size_t bytes,
                                kkt_stream_t stream) {
   if (!h) return KKT_ERR_ARG;
@@ -318,7 +384,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   DevPlan& d = h->dp;
   d.n = P.n; d.m = P.m; d.m_eq = P.m_eq; d.nnzW = P.nnzW; d.nnzJ = P.nnzJ; d.nnzK = P.Kp[P.n];
   d.ns = P.ns; d.batch = P.batch; d.max_front = P.max_front;
-  d.ns_s = (int)P.order_s.size(); d.ns_b = (int)P.order_b.size(); d.max_r_small = P.max_r_small;
+  d.ns_s = (int)P.order_s.size(); d.ns_b = (int)P.order_b.size();
+  d.ns_bn = d.ns_b - (int)P.order_h.size(); d.max_r_small = P.max_r_small;
   d.n_up_s = (int)P.up_s.size(); d.n_up_b = (int)P.up_b.size();
   d.n_dn_b = (int)P.dn_b.size(); d.n_dn_s = (int)P.dn_s.size();
   d.n_up_bf = (int)P.up_bf.size(); d.n_h = (int)P.order_h.size();
@@ -396,13 +463,9 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(grid_of(factor_small_kernel, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
   CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
-  CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, ub, 1, &h->g_tbig));
+  CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, (long long)P.up_bf.size() * P.batch, 1, &h->g_tbig));
   CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
-  {  // top-down workers mostly wait on the queue: cap them so idle pollers do not crowd the SMs
-    int cap = h->sms;
-    if (const char* e = getenv("KKT_BWD_CTAS")) cap = std::max(1, atoi(e));
-    h->g_bsmall = std::min(h->g_bsmall, cap);
-  }
+  if (const char* e = getenv("KKT_BWD_CTAS")) h->g_bsmall = std::min(h->g_bsmall, std::max(1, atoi(e)));
   CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
@@ -412,57 +475,13 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_huge_kernel, 256, h->huge_smem));
     h->g_huge = std::max(1, occ) * h->sms;
-    // level schedule of the huge fronts for this grid (see HugeSched in huge.cuh)
+    int occ_s = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, solve_huge_kernel, 256, 0));
+    h->g_hsolve = std::max(1, occ_s) * h->sms;
     if (!P.order_h.empty()) {
-      const int G = h->g_huge;
-      std::vector<int> hl(P.ns, -1);
-      int nlev = 0;
-      for (int s : P.order_h) {  // postorder: children first
-        int l = 0;
-        for (int q = P.sn_cp[s]; q < P.sn_cp[s + 1]; q++) {
-          int c = P.sn_ch[q];
-          if (hl[c] >= 0) l = std::max(l, hl[c] + 1);
-        }
-        hl[s] = l;
-        nlev = std::max(nlev, l + 1);
-      }
-      std::vector<std::vector<int>> lv(nlev);
-      for (int s : P.order_h) lv[hl[s]].push_back(s);
-      std::vector<int> lptr(1, 0);
-      std::vector<int4> ent;
-      for (int L = 0; L < nlev; L++) {
-        const auto& F = lv[L];
-        const int k = (int)F.size();
-        if (k > G) {
-          for (int s : F) ent.push_back(make_int4(s, 0, 0, 0));
-        } else {
-          std::vector<double> wgt(k);
-          double tot = 0;
-          for (int i = 0; i < k; i++) {
-            double r = P.sn_rp[F[i] + 1] - P.sn_rp[F[i]], w = P.sn_first[F[i] + 1] - P.sn_first[F[i]];
-            wgt[i] = r * r * (w + 2.0);
-            tot += wgt[i];
-          }
-          std::vector<int> g(k);
-          int sum = 0;
-          for (int i = 0; i < k; i++) { g[i] = std::max(1, (int)(G * wgt[i] / tot)); sum += g[i]; }
-          while (sum > G) {  // trim the largest groups
-            int im = (int)(std::max_element(g.begin(), g.end()) - g.begin());
-            g[im]--; sum--;
-          }
-          int c0 = 0;
-          for (int i = 0; i < k; i++) { ent.push_back(make_int4(F[i], c0, g[i], 0)); c0 += g[i]; }
-        }
-        lptr.push_back((int)ent.size());
-      }
-      CUDA_TRY(cudaMalloc(&h->huge_mem, lptr.size() * sizeof(int) + ent.size() * sizeof(int4) * 2 + 256));
-      char* hb = (char*)h->huge_mem;
-      int4* d_ent = (int4*)hb;
-      CUDA_TRY(cudaMemcpy(d_ent, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
-      int* d_ctr = (int*)(hb + ent.size() * sizeof(int4));
-      int* d_lptr = (int*)(hb + ent.size() * sizeof(int4) * 2);
-      CUDA_TRY(cudaMemcpy(d_lptr, lptr.data(), lptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-      h->hsched.lvl_ptr = d_lptr; h->hsched.ent = d_ent; h->hsched.nlev = nlev; h->hsched.ctr = d_ctr;
+      TRY(build_huge_sched(h, h->g_huge, &h->hsched, &h->huge_mem));
+      TRY(build_huge_sched(h, h->g_hsolve, &h->hsched_s, &h->hsolve_mem));
+      h->hflags = const_cast<int*>(h->hsched_s.lvl_ptr) + h->hsched_s.nlev + 1;
     }
   }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
@@ -547,13 +566,31 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
     h->launches++;
   }
   if (!P.order_b.empty()) {
-    fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 3 * KKT_CTL, done, h->pcap);
-    LAUNCH_CHECK();
-    bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap);
-    LAUNCH_CHECK();
-    h->launches += 2;
+    if (!P.up_bf.empty()) {
+      fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->ls>>>(
+          h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 3 * KKT_CTL, done, h->pcap);
+      LAUNCH_CHECK();
+      h->launches++;
+    }
+    if (!P.order_h.empty()) {
+      DevPlan dp = h->dp;
+      const double *lx = h->Lx, *dv = h->Dv, *rh = rhs;
+      double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
+      long long rs_ = rs, xs_ = xs;
+      const int* dn = done;
+      HugeSched hs = h->hsched_s;
+      int* fl = h->hflags;
+      void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs, &fl};
+      CUDA_TRY(cudaLaunchCooperativeKernel((const void*)solve_huge_kernel, dim3(h->g_hsolve), dim3(256), args, 0,
+                                           h->ls));
+      h->launches++;
+    }
+    if (P.order_b.size() > P.order_h.size()) {
+      bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
+          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap);
+      LAUNCH_CHECK();
+      h->launches++;
+    }
   }
   if (!P.order_s.empty()) {
     bwd_small_kernel<<<h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
@@ -884,6 +921,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
     if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
     if (h->trace_buf) cudaFree(h->trace_buf);
     if (h->huge_mem) cudaFree(h->huge_mem);
+    if (h->hsolve_mem) cudaFree(h->hsolve_mem);
     if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
     if (h->cap) cudaStreamDestroy(h->cap);
   }

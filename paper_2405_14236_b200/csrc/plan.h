@@ -55,9 +55,10 @@ struct Plan {
   int max_r_small = 0;
   // Ready lists (spin-free scheduling, see factor.cuh):
   //   up_s: small leaves (phase-1 bottom-up start);  up_b: big supernodes with no big child
-  //   dn_b: big roots (phase-1 top-down start);      dn_s: small roots + small children of big
+  //   dn_b: big non-huge roots + big non-huge children of huge (top-down start after the huge
+  //         phase);                                  dn_s: small roots + small children of big
   std::vector<int> up_s, up_b, dn_b, dn_s;
-  std::vector<int> up_bf, order_h;  // factor: big non-huge supernodes with no big non-huge child; huge list
+  std::vector<int> up_bf, order_h;  // big non-huge supernodes with no big non-huge child; huge list
   std::vector<SnInfo> sn;
   std::vector<SnInfo> chinfo;    // parallel to sn_ch: SnInfo of each child (one hop less)
   std::vector<int> sn_hsub;      // subtree height

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
   extern __shared__ double sm[];
   __shared__ int s_task, s_last;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int ninit = P.n_up_b * P.batch;
+  const int ninit = P.n_up_bf * P.batch;
   double* v = sm;                         // [max_front]
   double* L11 = sm + P.max_front;         // [64 * 64] (unstaged path)
   double* Pn = L11 + 64 * 64;             // [pcap] staged panel
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
     if (t >= ninit) break;
     const int b = t % P.batch;
     if (done && done[b]) continue;
-    int s = __ldg(P.up_b + t / P.batch);
+    int s = __ldg(P.up_bf + t / P.batch);
     int* cnt = cnt_all + (long long)b * P.ns;
     const double* Lb = Lx_all + (long long)b * P.nnzL_stored;
     double* uv = uv_all + (long long)b * P.uvec_doubles;
@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       for (int q = tid; q < R; q += nt) us[q] = v[w + q];
       __threadfence();
       __syncthreads();
+      if (P.sn[I.par].huge) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
       if (tid == 0) {
         const SnInfo Ip = P.sn[I.par];
         const int old = atom_add_acq_rel(cnt + I.par, 1);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
   extern __shared__ double sm[];
   __shared__ int s_task;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  const int total = P.ns_b * P.batch;
+  const int total = P.ns_bn * P.batch;
   double* xa = sm;                   // [max_front]  x over R_s (own columns then ancestors)
   double* L11 = sm + P.max_front;    // [64*64] (unstaged path)
   double* Pn = L11 + 64 * 64;        // [pcap] staged panel

@@ -1,0 +1,3 @@
+# perf-only GPU round: bench C2/C4/C6 + C6 trace
+for c in C2 C4 C6; do timeout 300 python bench.py --workload $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; python tools/bench_summary.py gpurun_out/bench_$c.json; tail -1 gpurun_out/bench_$c.err; done
+KKT_TRACE=1 KKT_NO_GRAPH=1 timeout 600 python tools/trace_analyze.py C6 > gpurun_out/trace_c6.txt 2>&1; grep "==" gpurun_out/trace_c6.txt
