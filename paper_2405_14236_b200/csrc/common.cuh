@@ -26,6 +26,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -42,6 +43,12 @@ __device__ __forceinline__ int ld_volatile(const int* p) {
   asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Wait until *f >= target: relaxed polling (no per-poll L1 invalidation, which would stall the
+// SM's other warps), then one acquire fence (relaxed read + fence = acquire pattern).
+__device__ __forceinline__ void spin_acquire(const int* f, int target) {
+  while (ld_volatile(f) < target) { }
+  fence_acq_rel();
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -52,6 +59,12 @@ __device__ __forceinline__ long long gtimer() {
 #define KKT_TRACE_SLOTS 8
 __device__ __forceinline__ void trace_stamp(const DevPlan& P, int kind, int s, int b, int which) {
   if (P.trace && b == 0) P.trace[((long long)kind * P.ns + s) * KKT_TRACE_SLOTS + which] = gtimer();
+}
+// latest-of stamp (several warps finish a phase; the last one counts)
+__device__ __forceinline__ void trace_max(const DevPlan& P, int kind, int s, int b, int which) {
+  if (P.trace && b == 0)
+    atomicMax((unsigned long long*)&P.trace[((long long)kind * P.ns + s) * KKT_TRACE_SLOTS + which],
+              (unsigned long long)gtimer());
 }
 // Coalesced global -> shared copy with KKT_MLP loads in flight per thread (the loads are issued
 // back to back before any store, so a copy of n elements costs ~ceil(n / (nt*KKT_MLP)) memory

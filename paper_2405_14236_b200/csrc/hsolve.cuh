@@ -23,17 +23,14 @@ namespace kkt {
 
 #define SB 32  // row / column block of the huge-front solves (one warp lane per row)
 
-__device__ __forceinline__ void wait_flag(const int* f, int target) {
-  while (ld_acquire(f) < target) { }
-}
+__device__ __forceinline__ void wait_flag(const int* f, int target) { spin_acquire(f, target); }
 
 __global__ void __launch_bounds__(256, 1) solve_huge_kernel(DevPlan P, const double* __restrict__ Lx_all,
                                                             const double* __restrict__ Dv_all,
                                                             const double* __restrict__ rhs, long long rs,
                                                             double* Y_all, double* uv_all, double* Xp_all,
                                                             double* xout, long long xs,
-                                                            const int* __restrict__ done, HugeSched H,
-                                                            int* flags) {
+                                                            const int* __restrict__ done, HugeSched H) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double part[8][SB];
@@ -42,7 +39,7 @@ __global__ void __launch_bounds__(256, 1) solve_huge_kernel(DevPlan P, const dou
   const unsigned full = 0xffffffffu;
   const int nent = H.lvl_ptr[H.nlev];
   for (int q = blockIdx.x * nt + tid; q < nent; q += gridDim.x * nt) H.ctr[q] = 0;
-  for (int q = blockIdx.x * nt + tid; q < 2 * H.nflag; q += gridDim.x * nt) flags[q] = 0;
+  for (int q = blockIdx.x * nt + tid; q < 2 * H.nflag; q += gridDim.x * nt) H.flags[q] = 0;
   grid.sync();
 
   for (int phase = 0; phase < 2; phase++) {
@@ -64,7 +61,7 @@ __global__ void __launch_bounds__(256, 1) solve_huge_kernel(DevPlan P, const dou
         const SnInfo I = P.sn[s];
         const int r = I.r, w = I.w, R = r - w;
         const int nb = (w + SB - 1) / SB, nR = (R + SB - 1) / SB;
-        int* fl = flags + (fwd ? 0 : H.nflag) + E.w;
+        int* fl = H.flags + (fwd ? 0 : H.nflag) + E.w;
         for (int b = 0; b < P.batch; b++) {
           if (done && done[b]) continue;
           const int tgt = b + 1;
@@ -232,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) solve_huge_kernel(DevPlan P, const dou
               __syncthreads();
             }
           }
-          if (G.rank == 0 && tid == 0) trace_stamp(P, fwd ? 1 : 2, s, b, 1);
+          if (lane == 0) trace_max(P, fwd ? 1 : 2, s, b, 1);
         }
       }
       grid.sync();  // level done: the next level reads these u vectors / x values

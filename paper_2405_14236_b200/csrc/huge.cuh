@@ -1,16 +1,24 @@
 // huge.cuh -- whole-GPU factorisation of the top fronts ("huge": front > one CTA's shared
-// memory), one front at a time in topological order, by a cooperative persistent kernel:
+// memory).  Fronts are processed by levels (children before parents, one grid barrier per level);
+// the fronts of one level run side by side on disjoint CTA groups.  Per front:
 //
-//   assemble    grid-stride zero / K scatter / extend-add of every child's update matrix
-//               (children in fixed order, grid barrier between children: deterministic)
-//   for each column block [k0, k0+kb), kb <= 32:
-//     a. every CTA factors the kb x kb diagonal block in one warp's registers (redundantly,
-//        saving a barrier); CTA 0 writes L_kk and the inverse pivots
-//     b. TRSM: rows below the block, one thread per row, column-oriented sweep
-//     -- grid barrier --
-//     c. trailing update of the lower triangle of rows/cols [k0+kb, r) in 64 x 64 tiles over
-//        all CTAs: operands staged in shared memory, 8 warps x 8 DMMA (m8n8k4.f64) tiles
-//     -- grid barrier --
+//   assemble    group-stride zero / K scatter / extend-add of every child's update matrix
+//               (children in fixed order, group barrier between children: deterministic)
+//   factorise   tiled right-looking Cholesky as a dataflow over WARPS: the front's lower
+//               triangle is cut into 32 x 32 tiles (row/column blocks restart at w so a tile is
+//               either panel or update matrix); every tile belongs to one warp of the group for
+//               its whole life, so the read-modify-writes of a tile are ordered by that warp's
+//               program order.  For step k (panel column block k < nb):
+//                 POTRF(k)      L_kk = chol(A_kk)                (warp registers)
+//                 TRSM(i,k)     L_ik = A_ik L_kk^-T              (lane = row, L_kk in smem)
+//                 UPDATE(i,j,k) A_ij -= L_ik L_jk^T, j > k       (DMMA m8n8k4.f64, fragments
+//                                                                  straight from L2)
+//               A finished panel tile publishes a flag (batch index + 1); consumers spin on it.
+//               Each warp runs its tiles in (k, column, row) order and finalises a tile of
+//               column k+1 right after applying step k to it (look-ahead), so the critical path
+//               per 32 columns is TRSM -> UPDATE -> POTRF plus three flag hand-offs.  Every wait
+//               is on a task earlier in that global order: deadlock-free with all CTAs resident
+//               (cooperative launch).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -18,12 +26,10 @@
 
 namespace kkt {
 
-#define HB 32          // column block of the huge path (diagonal block held in registers)
-#define HT 64          // trailing-update tile edge
-#define HT_LD (HT + 1) // padded leading dimension of staged operands (bank spread)
+#define HB 32  // tile edge of the huge path (one warp lane per tile row)
 
-// shared memory layout of factor_huge_kernel (doubles)
-constexpr int HUGE_SMEM_DOUBLES = HB * HB + HB + 2 * HB * HT_LD;
+// shared memory of factor_huge_kernel: one 32 x 32 scratch tile per warp (doubles)
+constexpr int HUGE_SMEM_DOUBLES = 8 * HB * HB;
 
 // Group of CTAs cooperating on one front (contiguous blockIdx range); a group barrier is an
 // arrival counter in its own slot (targets grow with the generation), or __syncthreads for 1 CTA.
@@ -56,23 +62,194 @@ struct HugeSched {
   const int4* ent;      // [nent]
   int nlev;
   int* ctr;             // [nent] group barrier counters (zeroed by the kernel)
-  int nflag;            // sum over entries of ceil(w / 32) (solve block flags per direction)
+  int nflag;            // flags per direction: sum over entries of the front's flag count
+  int* flags;           // [2 * nflag] tile / block flags (zeroed by the kernel)
+  long long* dbg;       // optional [4096][8] per-step stamps of the root front (KKT_TRACE=2)
 };
 
-__global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const double* __restrict__ Kv_all,
-                                                          double* Lx_all, double* U_all, double* Dv_all,
-                                                          int* cnt_all, int* fail_all, HugeSched H) {
+// Tile geometry of one huge front: blocks 0..nb-1 cover the w pivot columns in 32s, blocks
+// nb..nt-1 the R update rows/columns (restarting at w).  Tiles (i, j), i >= j, are numbered
+// column-major over the lower triangle.
+struct HFront {
+  double* F;  // r x w panel, ld r
+  double* U;  // packed lower update matrix, R x R
+  int r, w, nb, nt;
+  __device__ __forceinline__ int bstart(int t) const { return t < nb ? t * HB : w + (t - nb) * HB; }
+  __device__ __forceinline__ int bsize(int t) const {
+    return t < nb ? min(HB, w - t * HB) : min(HB, r - w - (t - nb) * HB);
+  }
+  __device__ __forceinline__ int lin(int i, int j) const { return j * nt - j * (j - 1) / 2 + (i - j); }
+};
+
+__device__ __forceinline__ void tile_wait(const int* f, int target) { spin_acquire(f, target); }
+// The warp barrier orders every lane's tile stores before lane 0's gpu-scope release (release is
+// cumulative over writes ordered before it), so consumers that acquire the flag see the tile.
+__device__ __forceinline__ void tile_publish(int* f, int target, int lane) {
+  __syncwarp();
+  if (lane == 0) st_release(f, target);
+}
+
+// POTRF of diagonal tile k (one warp; lane = row): L_kk and the inverse pivots.  Blocked by 8:
+// inside a panel of 8 columns the pivot column is broadcast by shuffles (short dependent chain);
+// the panel then updates the trailing columns as a rank-8 update with the panel rows staged in
+// the warp's scratch (broadcast LDS.128).  A non-positive pivot lowers *fail_col to its column.
+template <int PNL>
+__device__ __forceinline__ void potrf_panel(double (&a)[HB], double& myinv, int& fail_col, double* pb,
+                                            int lane, int kb, int c0) {
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int c = 8 * PNL; c < 8 * PNL + 8; c++) {
+    if (c < kb) {
+      const double d = __shfl_sync(full, a[c], c);
+      const bool bad = !(d > 0.0) || !isfinite(d);
+      const double inv = bad ? nan_d() : rsqrt(d);
+      double l = a[c] * inv;
+      if (lane == c) {
+        l = d * inv;
+        myinv = inv;
+        if (bad) fail_col = min(fail_col, c0 + c);
+      }
+      a[c] = (lane >= c) ? l : 0.0;
+#pragma unroll
+      for (int cc = c + 1; cc < 8 * PNL + 8; cc++) {
+        const double lcc = __shfl_sync(full, l, cc);  // L[cc][c]
+        if (lane > c) a[cc] = fma(-l, lcc, a[cc]);
+      }
+    }
+  }
+  if (PNL < HB / 8 - 1 && 8 * PNL + 8 < kb) {  // trailing: a[cc] -= sum_q L[lane][8P+q] L[cc][8P+q]
+#pragma unroll
+    for (int q = 0; q < 8; q++) pb[lane * 8 + q] = a[8 * PNL + q];
+    __syncwarp();
+#pragma unroll
+    for (int cc = 8 * PNL + 8; cc < HB; cc++) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) a[cc] = fma(-a[8 * PNL + q], pb[cc * 8 + q], a[cc]);
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void tile_potrf(const HFront& H, int k, double* dinv, double* pb, int lane,
+                                           int* fail_col) {
+  const int c0 = k * HB, kb = H.bsize(k);
+  double a[HB];
+#pragma unroll
+  for (int c = 0; c < HB; c++)
+    a[c] = (lane < kb && c < kb && c <= lane) ? ldcg(H.F + (long long)(c0 + c) * H.r + c0 + lane) : 0.0;
+  double myinv = 0.0;
+  int fc = *fail_col;
+  potrf_panel<0>(a, myinv, fc, pb, lane, kb, c0);
+  if (kb > 8) potrf_panel<1>(a, myinv, fc, pb, lane, kb, c0);
+  if (kb > 16) potrf_panel<2>(a, myinv, fc, pb, lane, kb, c0);
+  if (kb > 24) potrf_panel<3>(a, myinv, fc, pb, lane, kb, c0);
+  *fail_col = fc;
+#pragma unroll
+  for (int c = 0; c < HB; c++)
+    if (lane < kb && c < kb && c <= lane) H.F[(long long)(c0 + c) * H.r + c0 + lane] = a[c];
+  if (lane < kb) dinv[c0 + lane] = myinv;
+}
+
+// TRSM of panel tile (i, k), i > k: L_ik = A_ik L_kk^-T (one warp; lane = row; L_kk staged in
+// the warp's shared scratch for broadcast reads).
+__device__ __forceinline__ void tile_trsm(const HFront& H, int i, int k, const double* dinv, double* Ls,
+                                          int lane) {
+  const int c0 = k * HB, kb = H.bsize(k);
+  const int r0 = H.bstart(i), ib = H.bsize(i);
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int c = 0; c < HB; c++)
+    Ls[c * HB + lane] = (c < kb && lane < kb && lane > c) ? ldcg(H.F + (long long)(c0 + c) * H.r + c0 + lane) : 0.0;
+  const double di = (lane < kb) ? ldcg(dinv + c0 + lane) : 0.0;
+  double x[HB];
+#pragma unroll
+  for (int c = 0; c < HB; c++)
+    x[c] = (lane < ib && c < kb) ? ldcg(H.F + (long long)(c0 + c) * H.r + r0 + lane) : 0.0;
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < HB; c++) {
+    if (c < kb) {
+      x[c] *= __shfl_sync(full, di, c);
+#pragma unroll
+      for (int t = c + 1; t < HB; t++) x[t] = fma(-x[c], Ls[c * HB + t], x[t]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < HB; c++)
+    if (lane < ib && c < kb) H.F[(long long)(c0 + c) * H.r + r0 + lane] = x[c];
+  __syncwarp();  // scratch reuse
+}
+
+// UPDATE of tile (i, j) by panel column block k: A_ij -= L_ik L_jk^T on DMMA (one warp).
+// m8n8k4 fragments come straight from L2: for k-step ks the lane reads
+// L[8m + lane/4][4 ks + lane%4] of row block i (A operand) and of row block j (B operand).
+__device__ __forceinline__ void tile_update(const HFront& H, int i, int j, int k, int lane) {
+  const int c0 = k * HB, kb = H.bsize(k);
+  const int ri = H.bstart(i), ni = H.bsize(i), rj = H.bstart(j), nj = H.bsize(j);
+  const bool dg = (i == j);
+  const int lr = lane >> 2, lc = lane & 3;
+  double c0v[4][4], c1v[4][4];
+#pragma unroll
+  for (int m = 0; m < 4; m++)
+#pragma unroll
+    for (int n = 0; n < 4; n++) { c0v[m][n] = 0.0; c1v[m][n] = 0.0; }
+#pragma unroll
+  for (int ks = 0; ks < HB / 4; ks++) {
+    if (ks * 4 < kb) {
+      const int kk = ks * 4 + lc;
+      const bool kv = kk < kb;
+      const double* col = H.F + (long long)(c0 + kk) * H.r;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int m = 0; m < 4; m++) fa[m] = (kv && 8 * m + lr < ni) ? ldcg(col + ri + 8 * m + lr) : 0.0;
+#pragma unroll
+      for (int n = 0; n < 4; n++)
+        fb[n] = dg ? fa[n] : ((kv && 8 * n + lr < nj) ? ldcg(col + rj + 8 * n + lr) : 0.0);
+#pragma unroll
+      for (int m = 0; m < 4; m++)
+#pragma unroll
+        for (int n = 0; n < 4; n++)
+          if (!dg || n <= m) dmma8x8x4(c0v[m][n], c1v[m][n], fa[m], fb[n]);
+    }
+  }
+  // read-modify-write of the tile, two row halves: all loads of a half before its stores
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    double* pp[16];
+    double old[16];
+#pragma unroll
+    for (int mm = 0; mm < 2; mm++)
+#pragma unroll
+      for (int n = 0; n < 4; n++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int a = 8 * (2 * h + mm) + lr, b = 8 * n + 2 * lc + e;
+          const bool v = (a < ni) && (b < nj) && (!dg || a >= b);
+          pp[(mm * 4 + n) * 2 + e] = v ? front_at(H.F, H.U, H.r, H.w, ri + a, rj + b) : nullptr;
+        }
+#pragma unroll
+    for (int q = 0; q < 16; q++) old[q] = pp[q] ? ldcg(pp[q]) : 0.0;
+#pragma unroll
+    for (int mm = 0; mm < 2; mm++)
+#pragma unroll
+      for (int n = 0; n < 4; n++) {
+        const int q = (mm * 4 + n) * 2;
+        if (pp[q]) *pp[q] = old[q] - c0v[2 * h + mm][n];
+        if (pp[q + 1]) *pp[q + 1] = old[q + 1] - c1v[2 * h + mm][n];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) factor_huge_kernel(DevPlan P, const double* __restrict__ Kv_all,
+                                                             double* Lx_all, double* U_all, double* Dv_all,
+                                                             int* cnt_all, int* fail_all, HugeSched H) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
-  double* Dg = sm;                  // [HB][HB] diagonal block, column-major (ld HB)
-  double* dsh = Dg + HB * HB;       // [HB] inverse pivots
-  double* As = dsh + HB;            // [HB][HT_LD] rows of tile i (k-major)
-  double* Bs = As + HB * HT_LD;     // [HB][HT_LD] rows of tile j
-  __shared__ int s_fail;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-
-  for (int e = blockIdx.x; e < H.lvl_ptr[H.nlev]; e += gridDim.x) H.ctr[e] = 0;
+  double* ws = sm + warp * HB * HB;  // this warp's scratch tile
+  for (int q = blockIdx.x * nt + tid; q < H.lvl_ptr[H.nlev]; q += gridDim.x * nt) H.ctr[q] = 0;
+  for (int q = blockIdx.x * nt + tid; q < H.nflag; q += gridDim.x * nt) H.flags[q] = 0;
   grid.sync();
   for (int L = 0; L < H.nlev; L++) {
    const int e0 = H.lvl_ptr[L], e1 = H.lvl_ptr[L + 1];
@@ -145,142 +322,62 @@ __global__ void __launch_bounds__(256) factor_huge_kernel(DevPlan P, const doubl
       }
       G.sync();
       if (gtid == 0) trace_stamp(P, 0, s, b, 2);
-      // ---------------- blocked factorisation ----------------
-      if (tid == 0) s_fail = -1;
-      for (int k0 = 0; k0 < w; k0 += HB) {
-        const int kb = (w - k0) < HB ? (w - k0) : HB;
-        // a. diagonal block in warp 0's registers (every CTA)
-        if (warp == 0) {
-          double a[HB];
-          const int row = k0 + lane;
-#pragma unroll
-          for (int c = 0; c < HB; c++)
-            a[c] = (lane < kb && c < kb && c <= lane) ? ldcg(F + (long long)(k0 + c) * r + row) : 0.0;
-#pragma unroll
-          for (int c = 0; c < HB; c++) {
-            if (c < kb) {
-              __syncwarp();
-              double lc[HB];
-#pragma unroll
-              for (int cc = 0; cc < HB; cc++) lc[cc] = __shfl_sync(0xffffffffu, a[c], cc);
-              const double d = lc[c];
-              const bool bad = !(d > 0.0) || !isfinite(d);
-              const double inv = bad ? nan_d() : rsqrt(d);
-              if (lane == 0) {
-                dsh[c] = inv;
-                if (bad && s_fail < 0) s_fail = k0 + c;
-              }
-              if (lane > c) {
-                const double l = a[c] * inv;
-                a[c] = l;
-#pragma unroll
-                for (int cc = c + 1; cc < HB; cc++) a[cc] = fma(-l, lc[cc] * inv, a[cc]);
-              } else if (lane == c) {
-                a[c] = d * inv;
-              }
-            }
+      // ---------------- tile dataflow factorisation ----------------
+      {
+        HFront Hf;
+        Hf.F = F; Hf.U = U; Hf.r = r; Hf.w = w;
+        Hf.nb = (w + HB - 1) / HB;
+        Hf.nt = Hf.nb + (R + HB - 1) / HB;
+        int* tf = H.flags + E.w;
+        const int tgt = b + 1;
+        const int me = G.rank * 8 + warp, NW = G.size * 8;
+        int fail_col = INT_MAX;
+        // finalise panel tile (i, kk): POTRF if diagonal, else TRSM once L_kk is published
+        long long* dbg = (H.dbg && s == P.ns - 1 && b == 0) ? H.dbg : nullptr;
+        auto stamp = [&](int kk, int ev) { if (dbg && lane == 0 && kk < 4096) dbg[kk * 8 + ev] = gtimer(); };
+        auto finalise = [&](int i, int kk) {
+          if (i == kk) {
+            stamp(kk, 0);
+            tile_potrf(Hf, kk, dinv, ws, lane, &fail_col);
+            stamp(kk, 1);
+            if (lane == 0 && (kk == 1 || kk == 2 || kk == Hf.nb - 1)) trace_stamp(P, 0, s, b, kk == 1 ? 3 : kk == 2 ? 4 : 5);
+          } else {
+            if (i == kk + 1) stamp(kk, 7);
+            tile_wait(tf + Hf.lin(kk, kk), tgt);
+            if (i == kk + 1) stamp(kk, 2);
+            tile_trsm(Hf, i, kk, dinv, ws, lane);
+            if (i == kk + 1) stamp(kk, 3);
           }
-#pragma unroll
-          for (int c = 0; c < HB; c++) Dg[c * HB + lane] = (c <= lane && lane < kb && c < kb) ? a[c] : 0.0;
-        }
-        __syncthreads();
-        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 3);
-        // b. TRSM: rows i in [k0+kb, r), x = f L_kk^-T, column-oriented sweep per row
-        for (long long i = k0 + kb + gtid; i < r; i += gnt) {
-          double x[HB];
-#pragma unroll
-          for (int c = 0; c < HB; c++) x[c] = (c < kb) ? ldcg(F + (long long)(k0 + c) * r + i) : 0.0;
-#pragma unroll
-          for (int c = 0; c < HB; c++) {
-            if (c < kb) {
-              x[c] *= dsh[c];
-#pragma unroll
-              for (int t = c + 1; t < HB; t++) x[t] = fma(-x[c], Dg[c * HB + t], x[t]);
+          tile_publish(tf + Hf.lin(i, kk), tgt, lane);
+        };
+        for (int k = 0; k < Hf.nb; k++) {
+          // this warp's tiles with column >= k, column-major (tile t is owned by warp t mod NW)
+          const int l0 = Hf.lin(k, k);
+          int q = ((me - l0) % NW + NW) % NW;  // offset of the first owned tile from (k, k)
+          int j = k;
+          while (j < Hf.nt && q >= Hf.nt - j) { q -= Hf.nt - j; j++; }
+          while (j < Hf.nt) {
+            const int i = j + q;
+            if (j == k) {
+              if (k == 0) finalise(i, 0);  // columns k > 0 were finalised one step early
+            } else {
+              const bool crit = (i == k + 1 && j == k + 1);
+              if (crit) stamp(k, 6);
+              tile_wait(tf + Hf.lin(i, k), tgt);
+              tile_wait(tf + Hf.lin(j, k), tgt);
+              if (crit) stamp(k, 4);
+              tile_update(Hf, i, j, k, lane);
+              if (crit) stamp(k, 5);
+              if (j == k + 1 && j < Hf.nb) finalise(i, j);  // look-ahead
             }
-          }
-#pragma unroll
-          for (int c = 0; c < HB; c++)
-            if (c < kb) F[(long long)(k0 + c) * r + i] = x[c];
-        }
-        G.sync();
-        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 4);
-        // every CTA has finished reading the unfactored diagonal block: CTA 0 stores L_kk
-        if (G.rank == 0) {
-          for (int q = tid; q < kb * kb; q += nt) {
-            const int c = q / kb, i = q % kb;
-            if (i >= c) F[(long long)(k0 + c) * r + k0 + i] = Dg[c * HB + i];
-          }
-          for (int q = tid; q < kb; q += nt) dinv[k0 + q] = dsh[q];
-        }
-        // c. trailing update in HT x HT tiles
-        const int j0 = k0 + kb, m = r - j0;
-        if (m > 0) {
-          const int ntl = (m + HT - 1) / HT;
-          const long long ntiles = (long long)ntl * (ntl + 1) / 2;
-          for (long long t = G.rank; t < ntiles; t += G.size) {
-            int tj = 0;
-            long long rem = t;
-            while (rem >= ntl - tj) { rem -= ntl - tj; tj++; }
-            const int ti = tj + (int)rem;
-            const int i0 = j0 + ti * HT, jj0 = j0 + tj * HT;
-            __syncthreads();
-            {  // stage the two 32 x 64 operand panels: all loads in flight before the stores
-              constexpr int PER = (HB * HT) / 256;  // 8 elements of each panel per thread
-              double va[PER], vb[PER];
-#pragma unroll
-              for (int u = 0; u < PER; u++) {
-                const int q = tid + u * 256, k = q / HT, i = q % HT;
-                const bool kin = k < kb;
-                va[u] = (kin && i0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + i0 + i) : 0.0;
-                vb[u] = (kin && jj0 + i < r) ? ldcg(F + (long long)(k0 + k) * r + jj0 + i) : 0.0;
-              }
-#pragma unroll
-              for (int u = 0; u < PER; u++) {
-                const int q = tid + u * 256, k = q / HT, i = q % HT;
-                As[k * HT_LD + i] = va[u];
-                Bs[k * HT_LD + i] = vb[u];
-              }
-            }
-            __syncthreads();
-            // 64 x 64 = 8 x 8 DMMA tiles; warp w owns tile row w x all 8 tile columns
-            double c0[8], c1[8];
-#pragma unroll
-            for (int y = 0; y < 8; y++) { c0[y] = 0.0; c1[y] = 0.0; }
-            __syncwarp();
-            for (int kk = 0; kk < kb; kk += 4) {
-              const int k = kk + (lane & 3);
-              const double a = As[k * HT_LD + warp * 8 + (lane >> 2)];
-              double bb[8];
-#pragma unroll
-              for (int y = 0; y < 8; y++) bb[y] = Bs[k * HT_LD + y * 8 + (lane >> 2)];
-#pragma unroll
-              for (int y = 0; y < 8; y++) dmma8x8x4(c0[y], c1[y], a, bb[y]);
-            }
-            const int i = i0 + warp * 8 + (lane >> 2);
-            // read-modify-write of the 16 outputs: all 16 loads issued before the stores
-            double* pp[16];
-            double old[16];
-#pragma unroll
-            for (int y = 0; y < 8; y++) {
-              const int jb = jj0 + y * 8 + (lane & 3) * 2;
-              pp[2 * y] = (i < r && jb <= i) ? front_at(F, U, r, w, i, jb) : nullptr;
-              pp[2 * y + 1] = (i < r && jb + 1 <= i) ? front_at(F, U, r, w, i, jb + 1) : nullptr;
-            }
-#pragma unroll
-            for (int e = 0; e < 16; e++) old[e] = pp[e] ? ldcg(pp[e]) : 0.0;
-#pragma unroll
-            for (int y = 0; y < 8; y++) {
-              if (pp[2 * y]) *pp[2 * y] = old[2 * y] - c0[y];
-              if (pp[2 * y + 1]) *pp[2 * y + 1] = old[2 * y + 1] - c1[y];
-            }
+            q += NW;
+            while (j < Hf.nt && q >= Hf.nt - j) { q -= Hf.nt - j; j++; }
           }
         }
-        G.sync();
-        if (gtid == 0 && k0 == 0) trace_stamp(P, 0, s, b, 5);
-        if (gtid == 0 && k0 == HB) trace_stamp(P, 0, s, b, 6);
+        fail_col = __reduce_min_sync(0xffffffffu, fail_col);
+        if (lane == 0 && fail_col != INT_MAX) atomicMin(fail_all, I.f0 + fail_col);
       }
-      if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
-      if (gtid == 0) trace_stamp(P, 0, s, b, 1);
+      if (lane == 0) trace_max(P, 0, s, b, 1);
     }
    }
    grid.sync();  // level done: the next level's fronts may read these update matrices

@@ -92,11 +92,11 @@ struct kkt_plan {
          *hb = nullptr, *hx = nullptr;
   int* pinned_flags = nullptr;
   long long* trace_buf = nullptr;
+  long long* dbg_buf = nullptr;  // KKT_TRACE=2: per-step stamps of the root front (huge path)
   void* huge_mem = nullptr;
   HugeSched hsched{}, hsched_s{};  // factor / solve grids
   void* hsolve_mem = nullptr;
-  int g_hsolve = 1;
-  int* hflags = nullptr;  // [2 * hsched.nflag] block flags of the huge-front solves
+  int g_hsolve = 1;  // [2 * hsched.nflag] block flags of the huge-front solves
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -273,7 +273,7 @@ static size_t vbytes(const std::vector<T>& v) { return align_up(v.size() * sizeo
 // Level schedule of the huge fronts for a cooperative grid of G CTAs (see HugeSched in
 // huge.cuh): one allocation holding the entries, their barrier counters, the level pointers and
 // 2 x nflag block flags of the solves (hsolve.cuh).
-static kkt_status build_huge_sched(kkt_plan* h, int G, HugeSched* out, void** mem) {
+static kkt_status build_huge_sched(kkt_plan* h, int G, bool tiles, HugeSched* out, void** mem) {
   const Plan& P = h->P;
   std::vector<int> hl(P.ns, -1);
   int nlev = 0;
@@ -291,9 +291,11 @@ static kkt_status build_huge_sched(kkt_plan* h, int G, HugeSched* out, void** me
   std::vector<int> lptr(1, 0);
   std::vector<int4> ent;
   int nflag = 0;
-  auto flag_off = [&](int s) {  // block flags of front s
+  auto flag_off = [&](int s) {  // flags of front s: one per 32 x 32 tile (factor) or per block (solve)
     const int o = nflag;
-    nflag += (P.sn_first[s + 1] - P.sn_first[s] + 31) / 32;
+    const int w = P.sn_first[s + 1] - P.sn_first[s], R = P.sn_rp[s + 1] - P.sn_rp[s] - w;
+    const int nb = (w + 31) / 32, nt = nb + (R + 31) / 32;
+    nflag += tiles ? nt * (nt + 1) / 2 : nb;
     return o;
   };
   for (int L = 0; L < nlev; L++) {
@@ -330,6 +332,7 @@ static kkt_status build_huge_sched(kkt_plan* h, int G, HugeSched* out, void** me
   int* d_lptr = (int*)(hb + ent.size() * sizeof(int4) * 2);
   CUDA_TRY(cudaMemcpy(d_lptr, lptr.data(), lptr.size() * sizeof(int), cudaMemcpyHostToDevice));
   out->lvl_ptr = d_lptr; out->ent = d_ent; out->nlev = nlev; out->ctr = d_ctr; out->nflag = nflag;
+  out->flags = d_lptr + lptr.size();
   return KKT_OK;
 }
 
@@ -409,6 +412,10 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     CUDA_TRY(cudaMalloc(&h->trace_buf, (size_t)3 * std::max(P.ns, 1) * KKT_TRACE_SLOTS * sizeof(long long)));
     CUDA_TRY(cudaMemset(h->trace_buf, 0, (size_t)3 * std::max(P.ns, 1) * KKT_TRACE_SLOTS * sizeof(long long)));
     d.trace = h->trace_buf;
+    if (atoi(getenv("KKT_TRACE")) > 1) {
+      CUDA_TRY(cudaMalloc(&h->dbg_buf, 4096 * 8 * sizeof(long long)));
+      CUDA_TRY(cudaMemset(h->dbg_buf, 0, 4096 * 8 * sizeof(long long)));
+    }
   }
   // ---- workspace ----
   size_t need;
@@ -444,7 +451,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   for (int s : P.order_b)
     maxpanel = std::max(maxpanel, (long long)(P.sn_rp[s + 1] - P.sn_rp[s]) * (P.sn_first[s + 1] - P.sn_first[s]));
   h->pcap = (int)std::min<long long>(maxpanel, 20000);
-  h->tbig_smem = (int)((P.max_front + 64 * 64 + h->pcap) * 8);
+  h->tbig_smem = (int)((P.max_front + 8 * 32) * 8);
   CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fsmall_smem));
   CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
   CUDA_TRY(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
@@ -479,9 +486,9 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, solve_huge_kernel, 256, 0));
     h->g_hsolve = std::max(1, occ_s) * h->sms;
     if (!P.order_h.empty()) {
-      TRY(build_huge_sched(h, h->g_huge, &h->hsched, &h->huge_mem));
-      TRY(build_huge_sched(h, h->g_hsolve, &h->hsched_s, &h->hsolve_mem));
-      h->hflags = const_cast<int*>(h->hsched_s.lvl_ptr) + h->hsched_s.nlev + 1;
+      TRY(build_huge_sched(h, h->g_huge, true, &h->hsched, &h->huge_mem));
+      h->hsched.dbg = h->dbg_buf;
+      TRY(build_huge_sched(h, h->g_hsolve, false, &h->hsched_s, &h->hsolve_mem));
     }
   }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
@@ -579,8 +586,7 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
       long long rs_ = rs, xs_ = xs;
       const int* dn = done;
       HugeSched hs = h->hsched_s;
-      int* fl = h->hflags;
-      void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs, &fl};
+      void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs};
       CUDA_TRY(cudaLaunchCooperativeKernel((const void*)solve_huge_kernel, dim3(h->g_hsolve), dim3(256), args, 0,
                                            h->ls));
       h->launches++;
@@ -920,6 +926,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
       if (p) cudaFree(p);
     if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
     if (h->trace_buf) cudaFree(h->trace_buf);
+    if (h->dbg_buf) cudaFree(h->dbg_buf);
     if (h->huge_mem) cudaFree(h->huge_mem);
     if (h->hsolve_mem) cudaFree(h->hsolve_mem);
     if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
@@ -927,4 +934,11 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
   }
   delete h;
   return KKT_OK;
+}
+
+// debugging aid (not part of the public header): per-step stamps of the root front, KKT_TRACE=2
+extern "C" int kkt_debug_steps(kkt_handle h, long long* out, int n) {
+  if (!h || !h->dbg_buf) return -1;
+  n = std::min(n, 4096 * 8);
+  return cudaMemcpy(out, h->dbg_buf, (size_t)n * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
 }

@@ -18,6 +18,115 @@ struct TaskQueue {
   int* flag;   // [ns * batch] 1 = slot published
 };
 
+// ---------------------------------------------------------------- CTA-blocked sweeps (big)
+// Forward sweep of one supernode by a CTA, v[0:r) in shared memory, L read from L2/HBM:
+// per 32-column block, warp 0 solves the diagonal block in registers (lane = row; the block's
+// rows are fetched while the previous block's rows are updated), then every thread updates
+// rows below with the block (thread per row, 32 independent loads in flight).
+__device__ __forceinline__ void cta_fwd_blocked(const double* __restrict__ L, int r, int w,
+                                                const double* __restrict__ dv, double* v, int tid, int nt) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const unsigned full = 0xffffffffu;
+  double ld[32];
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < 32; c++) ld[c] = (lane < w && c < lane) ? __ldg(L + (long long)c * r + lane) : 0.0;
+  }
+  for (int c0 = 0; c0 < w; c0 += 32) {
+    const int kb = min(32, w - c0);
+    if (warp == 0) {
+      const int row = c0 + lane;
+      double x = (lane < kb) ? v[row] : 0.0;
+      const double di = (lane < kb) ? __ldg(dv + row) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; k++) {
+        if (k < kb) {
+          const double yk = __shfl_sync(full, x * di, k);
+          if (lane == k) x = yk;
+          else if (lane > k) x = fma(-ld[k], yk, x);
+        }
+      }
+      if (lane < kb) v[row] = x;
+      // next diagonal block (L is read-only here)
+      const int n0 = c0 + 32, nkb = min(32, w - n0);
+#pragma unroll
+      for (int c = 0; c < 32; c++)
+        ld[c] = (lane < nkb && c < lane) ? __ldg(L + (long long)(n0 + c) * r + n0 + lane) : 0.0;
+    }
+    __syncthreads();
+    for (int i = c0 + kb + tid; i < r; i += nt) {
+      double l[32];
+#pragma unroll
+      for (int c = 0; c < 32; c++) l[c] = (c < kb) ? __ldg(L + (long long)(c0 + c) * r + i) : 0.0;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        a0 = fma(l[c], (c < kb) ? v[c0 + c] : 0.0, a0);
+        a1 = fma(l[c + 1], (c + 1 < kb) ? v[c0 + c + 1] : 0.0, a1);
+      }
+      v[i] -= a0 + a1;
+    }
+    __syncthreads();
+  }
+}
+
+// Backward sweep of one supernode by a CTA, xa[0:r) in shared memory (own part = y on entry,
+// ancestor part = x): per 32-column block, last first, every thread accumulates its rows'
+// products L_ic x_i for the block's 32 columns, a 31-shuffle transpose-reduce gives each lane
+// its column's warp sum, and warp 0 adds the warp partials in fixed order and solves the
+// transposed diagonal block in registers.  part: [8][32] shared scratch.
+__device__ __forceinline__ void cta_bwd_blocked(const double* __restrict__ L, int r, int w,
+                                                const double* __restrict__ dv, double* xa, double* part,
+                                                int tid, int nt) {
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const unsigned full = 0xffffffffu;
+  for (int c0 = ((w - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
+    const int kb = min(32, w - c0);
+    double ld[32];
+    double y0 = 0.0, di = 0.0;
+    if (warp == 0) {  // column c0+lane of the diagonal block, rows below the diagonal
+      if (lane < kb) { y0 = xa[c0 + lane]; di = __ldg(dv + c0 + lane); }
+#pragma unroll
+      for (int k = 0; k < 32; k++)
+        ld[k] = (lane < kb && k > lane && k < kb) ? __ldg(L + (long long)(c0 + lane) * r + c0 + k) : 0.0;
+    }
+    double p[32];
+#pragma unroll
+    for (int c = 0; c < 32; c++) p[c] = 0.0;
+    for (int i = c0 + kb + tid; i < r; i += nt) {
+      const double xi = xa[i];
+#pragma unroll
+      for (int c = 0; c < 32; c++) p[c] = fma((c < kb) ? __ldg(L + (long long)(c0 + c) * r + i) : 0.0, xi, p[c]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int c = 0; c < o; c++) {
+        const double send = up ? p[c] : p[c + o];
+        const double keep = up ? p[c + o] : p[c];
+        p[c] = keep + __shfl_xor_sync(full, send, o);
+      }
+    }
+    part[warp * 32 + lane] = p[0];
+    __syncthreads();
+    if (warp == 0) {
+      double a = y0;
+      for (int q = 0; q < nw; q++) a -= part[q * 32 + lane];
+#pragma unroll
+      for (int k = 31; k >= 0; k--) {
+        if (k < kb) {
+          const double xk = __shfl_sync(full, a * di, k);
+          if (lane == k) a = xk;
+          else if (lane < k) a = fma(-ld[k], xk, a);
+        }
+      }
+      if (lane < kb) xa[c0 + lane] = a;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- forward, small (warp)
 __device__ __forceinline__ void fwd_sweep_any(const double* Lp, int r, int w, const double* dv,
                                               double* v, int lane) {
@@ -108,8 +217,6 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int ninit = P.n_up_bf * P.batch;
   double* v = sm;                         // [max_front]
-  double* L11 = sm + P.max_front;         // [64 * 64] (unstaged path)
-  double* Pn = L11 + 64 * 64;             // [pcap] staged panel
   if (P.batch == 1 && done && done[0]) return;
   for (;;) {
     const int t = next_task(ctl, &s_task);
@@ -128,14 +235,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       const SnInfo I = P.sn[s];
       const int r = I.r, w = I.w, R = r - w;
       const double* L = Lb + I.Lp;
-      const bool staged = (r <= 256) && ((long long)r * w <= pcap);
-      if (staged) copy_g2s<false>(Pn, L, r * w, tid, nt);
       for (int q = tid; q < r; q += nt) v[q] = (q < w) ? bb[__ldg(P.perm + I.f0 + q)] : 0.0;
-      const int wb = staged ? 0 : (w < 64 ? w : 64);
-      for (int q = tid; q < wb * wb; q += nt) {
-        const int k = q / wb, i = q % wb;
-        L11[q] = (i >= k) ? __ldg(L + (long long)k * r + i) : 0.0;
-      }
       __syncthreads();
       for (int ci = I.c0; ci < I.c1; ci++) {
         const SnInfo C = P.chinfo[ci];
@@ -145,45 +245,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
         for (int q = tid; q < Rc; q += nt) v[__ldg(rel + q)] += ldcg(u + q);
         __syncthreads();
       }
-      if (staged) {
-        if (warp == 0) fwd_sweep_any(Pn, r, w, Dv_all + (long long)b * P.n + I.f0, v, lane);
-        __syncthreads();
-      } else {
-        for (int k0 = 0; k0 < w; k0 += 64) {
-          const int kb = (w - k0) < 64 ? (w - k0) : 64;
-          if (k0 > 0) {
-            for (int q = tid; q < kb * kb; q += nt) {
-              const int k = q / kb, i = q % kb;
-              L11[q] = (i >= k) ? __ldg(L + (long long)(k0 + k) * r + k0 + i) : 0.0;
-            }
-            __syncthreads();
-          }
-          if (warp == 0) {
-            for (int k = 0; k < kb; k++) {
-              const double yk = v[k0 + k] / L11[k * kb + k];
-              __syncwarp();
-              if (lane == 0) v[k0 + k] = yk;
-              for (int i = k + 1 + lane; i < kb; i += 32) v[k0 + i] = fma(-L11[k * kb + i], yk, v[k0 + i]);
-              __syncwarp();
-            }
-          }
-          __syncthreads();
-          for (int i = k0 + kb + tid; i < r; i += nt) {
-            double acc = v[i];
-            const double* Li = L + i;
-            int k = 0;
-            for (; k + 4 <= kb; k += 4) {
-              const double l0 = __ldg(Li + (long long)(k0 + k) * r), l1 = __ldg(Li + (long long)(k0 + k + 1) * r);
-              const double l2 = __ldg(Li + (long long)(k0 + k + 2) * r), l3 = __ldg(Li + (long long)(k0 + k + 3) * r);
-              acc = fma(-l0, v[k0 + k], acc); acc = fma(-l1, v[k0 + k + 1], acc);
-              acc = fma(-l2, v[k0 + k + 2], acc); acc = fma(-l3, v[k0 + k + 3], acc);
-            }
-            for (; k < kb; k++) acc = fma(-__ldg(Li + (long long)(k0 + k) * r), v[k0 + k], acc);
-            v[i] = acc;
-          }
-          __syncthreads();
-        }
-      }
+      cta_fwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, v, tid, nt);
       for (int q = tid; q < w; q += nt) Y[I.f0 + q] = v[q];
       if (tid == 0) trace_stamp(P, 1, s, b, 1);
       if (I.par < 0) break;
@@ -261,8 +323,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int total = P.ns_bn * P.batch;
   double* xa = sm;                   // [max_front]  x over R_s (own columns then ancestors)
-  double* L11 = sm + P.max_front;    // [64*64] (unstaged path)
-  double* Pn = L11 + 64 * 64;        // [pcap] staged panel
+  double* part = sm + P.max_front;   // [8 * 32] warp partials
   if (P.batch == 1 && done && done[0]) return;
   int task = -1;
   for (;;) {
@@ -287,40 +348,9 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     double* Xp = Xp_all + (long long)b * P.n;
     const double* Y = Y_all + (long long)b * P.n;
-    const bool staged = (w <= 128) && ((long long)r * w <= pcap);
-    if (staged) copy_g2s<false>(Pn, L, r * w, tid, nt);
     for (int q = tid; q < r; q += nt) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
     __syncthreads();
-    if (staged) {
-      if (warp == 0) bwd_sweep_any(Pn, r, w, Dv_all + (long long)b * P.n + I.f0, xa, lane);
-      __syncthreads();
-    }
-    const int nblk = staged ? 0 : (w + 63) / 64;
-    for (int bk = nblk - 1; bk >= 0; bk--) {
-      const int k0 = bk * 64, kb = (w - k0) < 64 ? (w - k0) : 64;
-      for (int k = warp; k < kb; k += nw) {
-        const double* Lk = L + (long long)(k0 + k) * r;
-        double acc = 0.0;
-        for (int i = k0 + kb + lane; i < r; i += 32) acc = fma(__ldg(Lk + i), xa[i], acc);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) xa[k0 + k] -= acc;
-      }
-      for (int q = tid; q < kb * kb; q += nt) {
-        const int k = q / kb, i = q % kb;
-        L11[q] = (i >= k) ? __ldg(L + (long long)(k0 + k) * r + k0 + i) : 0.0;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        for (int k = kb - 1; k >= 0; k--) {
-          const double xk = xa[k0 + k] / L11[k * kb + k];
-          __syncwarp();
-          if (lane == 0) xa[k0 + k] = xk;
-          for (int i = lane; i < k; i += 32) xa[k0 + i] = fma(-L11[i * kb + k], xk, xa[k0 + i]);
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-    }
+    cta_bwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part, tid, nt);
     double* xo = xout + (long long)b * xs;
     for (int q = tid; q < w; q += nt) {
       Xp[I.f0 + q] = xa[q];
