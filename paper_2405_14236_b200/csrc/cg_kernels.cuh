@@ -11,6 +11,7 @@ __device__ __forceinline__ double bits2d(unsigned long long b) { return __longlo
 // ---------------------------------------------------------------- refinement control
 __global__ void refine_init_kernel(int batch, DevCtrl C) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) C.done[batch] = batch;  // done[batch]: instances still refining
   if (b >= batch) return;
   C.done[b] = 0; C.refine_iters[b] = 0; C.grow[b] = 0;
   C.omega[b] = 0ULL; C.omega_prev[b] = INFINITY; C.omega_last[b] = 0.0;
@@ -41,11 +42,16 @@ __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep
     else C.grow[b] = 0;
   }
   C.omega_prev[b] = om;
-  if (stop) C.done[b] = 1;
-  else C.refine_iters[b] += 1;
+  if (stop) {
+    C.done[b] = 1;
+    atomicSub(C.done + batch, 1);
+  } else {
+    C.refine_iters[b] += 1;
+  }
 }
 
 __global__ void refine_update_kernel(int batch, int n, double* x, const double* __restrict__ dx, DevCtrl C) {
+  if (C.done[batch] == 0) return;  // every instance has finished refining
   long long total = (long long)batch * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {

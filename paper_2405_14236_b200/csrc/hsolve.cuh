@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256, 1) solve_huge_kernel(DevPlan P, const dou
   __shared__ double Dg[SB][SB + 1];  // diagonal block of the current task: Dg[k][lane] (warp 0)
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const unsigned full = 0xffffffffu;
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining (grid-uniform)
   const int nent = H.lvl_ptr[H.nlev];
   for (int q = blockIdx.x * nt + tid; q < nent; q += gridDim.x * nt) H.ctr[q] = 0;
   for (int q = blockIdx.x * nt + tid; q < 2 * H.nflag; q += gridDim.x * nt) H.flags[q] = 0;

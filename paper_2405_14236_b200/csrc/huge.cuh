@@ -29,7 +29,10 @@ namespace kkt {
 #define HB 32  // tile edge of the huge path (one warp lane per tile row)
 
 // shared memory of factor_huge_kernel: one 32 x 32 scratch tile per warp (doubles)
-constexpr int HUGE_SMEM_DOUBLES = 8 * HB * HB;
+constexpr int HUGE_SMEM_DOUBLES_PER_WARP = HB * HB;
+// warps per CTA of factor_huge_kernel, one CTA per SM (KKT_HUGE_WARPS overrides; 2 or 4 warps
+// per SM did not shorten the critical path: measured)
+constexpr int HUGE_WARPS = 8;
 
 // Group of CTAs cooperating on one front (contiguous blockIdx range); a group barrier is an
 // arrival counter in its own slot (targets grow with the generation), or __syncthreads for 1 CTA.
@@ -330,7 +333,8 @@ __global__ void __launch_bounds__(256, 1) factor_huge_kernel(DevPlan P, const do
         Hf.nt = Hf.nb + (R + HB - 1) / HB;
         int* tf = H.flags + E.w;
         const int tgt = b + 1;
-        const int me = G.rank * 8 + warp, NW = G.size * 8;
+        const int wpc = nt >> 5;  // warps per CTA
+        const int me = G.rank * wpc + warp, NW = G.size * wpc;
         int fail_col = INT_MAX;
         // finalise panel tile (i, kk): POTRF if diagonal, else TRSM once L_kk is published
         long long* dbg = (H.dbg && s == P.ns - 1 && b == 0) ? H.dbg : nullptr;

@@ -85,7 +85,7 @@ struct kkt_plan {
   long long factor_smem_cap = 0;
   int fsmall_smem = 0, fbig_smem = 0, tsmall_smem = 0, tbig_smem = 0, pcap = 0;
   int g_fsmall = 1, g_fbig = 1, g_tsmall = 1, g_tbig = 1, g_bsmall = 1, g_bbig = 1;
-  int g_huge = 1, huge_smem = 0;
+  int g_huge = 1, huge_smem = 0, huge_warps = 4;
   long long launches = 0;
   // host-buffer path (kkt_step_host)
   double *hW = nullptr, *hJ = nullptr, *hSx = nullptr, *hSs = nullptr, *hD = nullptr,
@@ -149,7 +149,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->ctl = c.take<int>(8 * KKT_CTL);
   h->fail = c.take<int>(1);
   h->status = c.take<int>(1);
-  h->C.done = c.take<int>(B);
+  h->C.done = c.take<int>(B + 1);  // [B] = number of instances still refining
   h->C.refine_iters = c.take<int>(B);
   h->C.grow = c.take<int>(B);
   h->C.omega = c.take<unsigned long long>(B);
@@ -158,7 +158,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.dxprev = c.take<double>(B);
   h->C.dxn = c.take<unsigned long long>(B);
   h->C.xn = c.take<unsigned long long>(B);
-  h->C.cg_done = c.take<int>(B);
+  h->C.cg_done = c.take<int>(B + 1);  // [B] stays 1: the solve kernels' all-done test never fires
   h->C.cg_iters = c.take<int>(B);
   h->C.cg_iters_first = c.take<int>(B);
   h->C.rr = c.take<double>(B);
@@ -434,6 +434,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(cudaMemsetAsync(h->ws, 0, need, h->stream));
   int big = INT_MAX;
   CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  static const int one = 1;
+  CUDA_TRY(cudaMemcpyAsync(h->C.cg_done + P.batch, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   // ---- launch configuration ----
   long long maxneed = 0;
   for (int s : P.order_b) {
@@ -477,11 +479,14 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
     CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
-    h->huge_smem = HUGE_SMEM_DOUBLES * 8;
+    h->huge_warps = HUGE_WARPS;
+    if (const char* e = getenv("KKT_HUGE_WARPS")) h->huge_warps = std::min(8, std::max(1, atoi(e)));
+    h->huge_smem = HUGE_SMEM_DOUBLES_PER_WARP * 8 * h->huge_warps;
     CUDA_TRY(cudaFuncSetAttribute(factor_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->huge_smem));
     int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_huge_kernel, 256, h->huge_smem));
-    h->g_huge = std::max(1, occ) * h->sms;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_huge_kernel, 32 * h->huge_warps, h->huge_smem));
+    h->g_huge = (occ >= 1 ? 1 : 0) * h->sms;  // one CTA per SM (see HUGE_WARPS)
+    if (h->g_huge == 0) { g_err = "factor_huge_kernel does not fit on an SM"; return KKT_ERR_CUDA; }
     int occ_s = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, solve_huge_kernel, 256, 0));
     h->g_hsolve = std::max(1, occ_s) * h->sms;
@@ -554,7 +559,7 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     int *cnt = h->facnt, *fail = h->fail;
     HugeSched hs = h->hsched;
     void* args[] = {&dp, &kv, &lx, &ub, &dv, &cnt, &fail, &hs};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)factor_huge_kernel, dim3(h->g_huge), dim3(256), args,
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)factor_huge_kernel, dim3(h->g_huge), dim3(32 * h->huge_warps), args,
                                          (size_t)h->huge_smem, h->ls));
     h->launches++;
   }

@@ -17,6 +17,7 @@ __global__ void resid_rows_kernel(DevPlan P, const double* __restrict__ Jv, cons
                                   long long xs, int mode, const double* __restrict__ dy,
                                   const double* __restrict__ rb2, double* res2, double2* T,
                                   double* A, const int* __restrict__ done) {
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining
   long long total = (long long)P.batch * P.m;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -52,6 +53,7 @@ __global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, cons
                                   const double2* __restrict__ T, const double* __restrict__ A,
                                   double* res, unsigned long long* omega, const int* __restrict__ done) {
   long long total = (long long)P.batch * P.n;
+  if (done && done[P.batch] == 0) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     int b = (int)(idx / P.n), i = (int)(idx % P.n);

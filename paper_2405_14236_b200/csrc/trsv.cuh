@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, cons
   double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
   double* v = Pn + KKT_SCAP;
   const int ninit = P.n_up_s * P.batch;
-  if (P.batch == 1 && done && done[0]) return;  // refinement finished: nothing to do
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining  // refinement finished: nothing to do
   for (;;) {
     const int t = warp_ticket(ctl);
     if (t >= ninit) break;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int ninit = P.n_up_bf * P.batch;
   double* v = sm;                         // [max_front]
-  if (P.batch == 1 && done && done[0]) return;
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining
   for (;;) {
     const int t = next_task(ctl, &s_task);
     if (t >= ninit) break;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
   const int total = P.ns_bn * P.batch;
   double* xa = sm;                   // [max_front]  x over R_s (own columns then ancestors)
   double* part = sm + P.max_front;   // [8 * 32] warp partials
-  if (P.batch == 1 && done && done[0]) return;
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining
   int task = -1;
   for (;;) {
     if (task < 0) {
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
   double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
   double* xa = Pn + KKT_SCAP;
   const int total = P.ns_s * P.batch;
-  if (P.batch == 1 && done && done[0]) return;
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining
   int task = -1;
   for (;;) {
     if (task < 0) {

@@ -31,6 +31,25 @@ __global__ void bench(double* F, double* dinv, long long* out, int reps, int nwa
   }
 }
 
+// cold single call (fresh launch): POTRF then TRSM then UPDATE, globaltimer ns
+__global__ void cold(double* F, double* dinv, long long* out) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31;
+  HFront H;
+  H.F = F; H.U = nullptr; H.r = 1024; H.w = 1024; H.nb = 32; H.nt = 32;
+  int fail = INT_MAX;
+  long long t0 = gtimer();
+  tile_potrf(H, 0, dinv, sm, lane, &fail);
+  long long t1 = gtimer();
+  tile_trsm(H, 1, 0, dinv, sm, lane);
+  long long t2 = gtimer();
+  tile_update(H, 1, 1, 0, lane);
+  long long t3 = gtimer();
+  tile_potrf(H, 1, dinv, sm, lane, &fail);
+  long long t4 = gtimer();
+  if (lane == 0) { out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = t4 - t3; }
+}
+
 int main() {
   const int n = 1024;
   double* hF = new double[(size_t)n * n];
@@ -55,5 +74,13 @@ int main() {
   long long h[5];
   cudaMemcpy(h, out, 40, cudaMemcpyDeviceToHost);
   printf("148 CTAs x 8 warps: POTRF %lld  TRSM %lld  UPDATE offdiag %lld  UPDATE diag %lld  publish %lld\n", h[0], h[1], h[2], h[3], h[4]);
+  cudaFuncSetAttribute(cold, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 32 * 8);
+  for (int rep = 0; rep < 3; rep++) {
+    cold<<<1, 32, 8 * 32 * 32 * 8>>>(F, dinv, out);
+    cudaDeviceSynchronize();
+    long long hc[4];
+    cudaMemcpy(hc, out, 32, cudaMemcpyDeviceToHost);
+    printf("(%s) cold launch %d: POTRF %lld ns  TRSM %lld ns  UPDATE(diag) %lld ns  POTRF again %lld ns\n", cudaGetErrorString(cudaGetLastError()), rep, hc[0], hc[1], hc[2], hc[3]);
+  }
   return 0;
 }
