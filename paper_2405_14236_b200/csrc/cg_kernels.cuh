@@ -11,7 +11,7 @@ __device__ __forceinline__ double bits2d(unsigned long long b) { return __longlo
 // ---------------------------------------------------------------- refinement control
 __global__ void refine_init_kernel(int batch, DevCtrl C) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b == 0) C.done[batch] = batch;  // done[batch]: instances still refining
+  if (b == 0) { C.done[batch] = batch; *C.sweep = 0; }  // done[batch]: instances still refining
   if (b >= batch) return;
   C.done[b] = 0; C.refine_iters[b] = 0; C.grow[b] = 0;
   C.omega[b] = 0ULL; C.omega_prev[b] = INFINITY; C.omega_last[b] = 0.0;
@@ -21,9 +21,11 @@ __global__ void refine_init_kernel(int batch, DevCtrl C) {
 // Stopping rules (R9): omega <= tol (only if tol > 0); ||dx|| <= 2u ||x|| after the previous
 // correction;
 // omega grew in two consecutive sweeps; last sweep (measurement only).
-__global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep, int last) {
+__global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int max_refine) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
+  const int sweep = *C.sweep;
+  const bool last = sweep >= max_refine;
   if (C.done[b]) return;
   double om = bits2d(C.omega[b]);
   C.omega[b] = 0ULL;
@@ -48,6 +50,13 @@ __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int sweep
   } else {
     C.refine_iters[b] += 1;
   }
+}
+
+// End of a sweep: advance the sweep counter and, inside the solve graph, set the condition of
+// the refinement WHILE node (another sweep iff some instance is still refining).
+__global__ void refine_cond_kernel(int batch, DevCtrl C, cudaGraphConditionalHandle handle, int use_handle) {
+  *C.sweep += 1;
+  if (use_handle) cudaGraphSetConditional(handle, C.done[batch] > 0 ? 1u : 0u);
 }
 
 __global__ void refine_update_kernel(int batch, int n, double* x, const double* __restrict__ dx, DevCtrl C) {

@@ -66,6 +66,7 @@ struct DevCtrl {
   double* dxprev;            // ||dx|| of the previous correction
   unsigned long long* dxn;   // bits of ||dx||_inf
   unsigned long long* xn;    // bits of ||x||_inf
+  int* sweep;                // refinement sweep counter (device-side loop control)
   // CG
   int* cg_done;
   int* cg_iters;

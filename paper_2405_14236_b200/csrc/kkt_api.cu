@@ -96,7 +96,10 @@ struct kkt_plan {
   void* huge_mem = nullptr;
   HugeSched hsched{}, hsched_s{};  // factor / solve grids
   void* hsolve_mem = nullptr;
-  int g_hsolve = 1;  // [2 * hsched.nflag] block flags of the huge-front solves
+  int g_hsolve = 1;
+  long long g_pro = 0, g_body = 0;   // kernels in the solve graph's prologue / per correction sweep
+  bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
+  bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -152,6 +155,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.done = c.take<int>(B + 1);  // [B] = number of instances still refining
   h->C.refine_iters = c.take<int>(B);
   h->C.grow = c.take<int>(B);
+  h->C.sweep = c.take<int>(1);
   h->C.omega = c.take<unsigned long long>(B);
   h->C.omega_prev = c.take<double>(B);
   h->C.omega_last = c.take<double>(B);
@@ -346,6 +350,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->ls = h->stream;
   CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
   h->use_graph = !(getenv("KKT_NO_GRAPH") && atoi(getenv("KKT_NO_GRAPH")) > 0);
+  h->solve_while = getenv("KKT_SOLVE_WHILE") && atoi(getenv("KKT_SOLVE_WHILE")) > 0;
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   h->sms = prop.multiProcessorCount;
@@ -520,6 +525,7 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
   h->Wv = W_vals; h->Jv = J_vals; h->Sx = Sigma_x; h->Ss = Sigma_s; h->Dov = D;
   h->dw = delta_w; h->dc = delta_c; h->gamma = gamma;
   h->launches = 0;
+  h->graph_solve_pending = false;
   if (P.m > 0) {
     dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
@@ -630,25 +636,127 @@ static kkt_status launch_resid(kkt_plan* h, const double* x, const double* rhs, 
 }
 
 
-static kkt_status enqueue_solve(kkt_plan* h, const double* b, double* x, int max_refine, double tol_bwd) {
+// One refinement sweep's tail: residual of x, per-instance stop decision, sweep counter (and
+// the WHILE condition when recorded into the solve graph).
+static kkt_status enqueue_check(kkt_plan* h, const double* b, double* x, int max_refine, double tol_bwd,
+                                cudaGraphConditionalHandle hc, int use_handle) {
   const Plan& P = h->P;
-  int gb = (P.batch + 127) / 128;
-  refine_init_kernel<<<gb, 128, 0, h->ls>>>(P.batch, h->C);
+  const int gb = (P.batch + 127) / 128;
+  TRY(launch_resid(h, x, b, 0, nullptr, nullptr, h->res, h->C.omega, h->C.done));
+  refine_decide_kernel<<<gb, 128, 0, h->ls>>>(P.batch, h->C, tol_bwd, max_refine);
+  LAUNCH_CHECK();
+  refine_cond_kernel<<<1, 1, 0, h->ls>>>(P.batch, h->C, hc, use_handle);
+  LAUNCH_CHECK();
+  h->launches += 2;
+  return KKT_OK;
+}
+
+static kkt_status enqueue_correction(kkt_plan* h, double* x) {
+  const Plan& P = h->P;
+  TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
+  refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
+      P.batch, P.n, x, h->dxv, h->C);
   LAUNCH_CHECK();
   h->launches++;
-  TRY(launch_solve(h, b, P.n, x, P.n, nullptr));
+  return KKT_OK;
+}
+
+static kkt_status enqueue_prologue(kkt_plan* h, const double* b, double* x) {
+  const Plan& P = h->P;
+  refine_init_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C);
+  LAUNCH_CHECK();
+  h->launches++;
+  return launch_solve(h, b, P.n, x, P.n, nullptr);
+}
+
+// stream-ordered refined solve (no graph): host loop over the sweeps, finished instances and
+// finished sweeps early-exit on device
+static kkt_status enqueue_solve(kkt_plan* h, const double* b, double* x, int max_refine, double tol_bwd) {
+  TRY(enqueue_prologue(h, b, x));
   for (int k = 0; k <= max_refine; k++) {
-    TRY(launch_resid(h, x, b, 0, nullptr, nullptr, h->res, h->C.omega, h->C.done));
-    refine_decide_kernel<<<gb, 128, 0, h->ls>>>(P.batch, h->C, tol_bwd, k, k == max_refine);
-    LAUNCH_CHECK();
-    h->launches++;
+    TRY(enqueue_check(h, b, x, max_refine, tol_bwd, 0, 0));
     if (k == max_refine) break;
-    TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
-    refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
-        P.batch, P.n, x, h->dxv, h->C);
-    LAUNCH_CHECK();
-    h->launches++;
+    TRY(enqueue_correction(h, x));
   }
+  return KKT_OK;
+}
+
+// Record the refined solve as one graph: prologue (first solve + residual + decision, first
+// correction sweep), then a WHILE node whose body is one correction sweep; the body runs only
+// while some instance is still refining, so converged solves launch no idle sweeps.
+static kkt_status record_solve_graph(kkt_plan* h, int max_refine, double tol_bwd, cudaGraph_t* out,
+                                     long long* n_pro, long long* n_body) {
+  cudaGraph_t g = nullptr;
+  if (!h->solve_while) {  // all sweeps recorded; idle ones exit at once on the all-done count
+    h->ls = h->cap;
+    CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    h->launches = 0;
+    kkt_status st = enqueue_solve(h, h->gb, h->gx, max_refine, tol_bwd);
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    h->ls = h->stream;
+    if (st != KKT_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) { g_err = std::string("graph capture: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    *n_pro = h->launches;
+    *n_body = 0;
+    *out = g;
+    return KKT_OK;
+  }
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hc;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&hc, g, 0, 0);
+  if (e != cudaSuccess) { cudaGraphDestroy(g); g_err = std::string("conditional handle: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+  auto capture = [&](cudaGraph_t into, auto&& body) -> kkt_status {
+    h->ls = h->cap;
+    cudaError_t ce = cudaStreamBeginCaptureToGraph(h->cap, into, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) { h->ls = h->stream; g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
+    kkt_status st = body();
+    cudaGraph_t got = nullptr;
+    ce = cudaStreamEndCapture(h->cap, &got);
+    h->ls = h->stream;
+    if (st != KKT_OK) return st;
+    if (ce != cudaSuccess) { g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
+    return KKT_OK;
+  };
+  h->launches = 0;
+  // the first correction sweep is recorded unconditionally (its kernels exit at once when every
+  // instance has already converged): the WHILE body -- a device-launched graph, measurably
+  // slower to start -- then only runs for systems that need two or more corrections
+  kkt_status st = capture(g, [&] {
+    TRY(enqueue_prologue(h, h->gb, h->gx));
+    TRY(enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 1));
+    if (max_refine < 1) return KKT_OK;
+    TRY(enqueue_correction(h, h->gx));
+    return enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 1);
+  });
+  if (st != KKT_OK) { cudaGraphDestroy(g); return st; }
+  *n_pro = h->launches;
+  // leaves of the prologue: nodes without outgoing edges
+  size_t nn = 0, ne = 0;
+  CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+  CUDA_TRY(cudaGraphGetEdges(g, nullptr, nullptr, &ne));
+  std::vector<cudaGraphNode_t> nodes(nn), from(ne), to(ne);
+  CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+  if (ne) CUDA_TRY(cudaGraphGetEdges(g, from.data(), to.data(), &ne));
+  std::vector<cudaGraphNode_t> leaves;
+  for (auto nd : nodes)
+    if (std::find(from.begin(), from.end(), nd) == from.end()) leaves.push_back(nd);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  e = cudaGraphAddNode(&wn, g, leaves.data(), leaves.size(), &cp);
+  if (e != cudaSuccess) { cudaGraphDestroy(g); g_err = std::string("while node: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  h->launches = 0;
+  st = capture(body, [&] {
+    TRY(enqueue_correction(h, h->gx));
+    return enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 1);
+  });
+  if (st != KKT_OK) { cudaGraphDestroy(g); return st; }
+  *n_body = h->launches;
+  *out = g;
   return KKT_OK;
 }
 
@@ -659,32 +767,27 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   if (tol_bwd < 0) tol_bwd = 0;  // 0 disables the backward-error stop (R9)
   max_refine = std::max(0, max_refine);
   h->launches = 0;
+  h->graph_solve_pending = false;
   if (!h->use_graph) return enqueue_solve(h, b, x, max_refine, tol_bwd);
-  // The refined solve is one CUDA graph (all sweeps; finished instances early-exit on device),
-  // recorded once per (max_refine, tol, value pointers, delta_w) on a private stream.
+  // one CUDA graph per (max_refine, tol, value pointers, delta_w), recorded on a private stream
   const bool stale = !h->solve_exec || h->g_max_refine != max_refine || h->g_tol != tol_bwd ||
                      h->g_W != h->Wv || h->g_J != h->Jv || h->g_Sx != h->Sx || h->g_dw != h->dw;
   if (stale) {
     if (h->solve_exec) { cudaGraphExecDestroy(h->solve_exec); h->solve_exec = nullptr; }
-    h->ls = h->cap;
-    CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-    kkt_status st = enqueue_solve(h, h->gb, h->gx, max_refine, tol_bwd);
     cudaGraph_t g = nullptr;
-    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
-    h->ls = h->stream;
-    if (st != KKT_OK) { if (g) cudaGraphDestroy(g); return st; }
-    if (e != cudaSuccess) { g_err = std::string("graph capture: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
-    e = cudaGraphInstantiate(&h->solve_exec, g, 0);
+    TRY(record_solve_graph(h, max_refine, tol_bwd, &g, &h->g_pro, &h->g_body));
+    cudaError_t e = cudaGraphInstantiate(&h->solve_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) { g_err = std::string("graph instantiate: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
     h->g_max_refine = max_refine; h->g_tol = tol_bwd; h->g_W = h->Wv; h->g_J = h->Jv;
-    h->g_Sx = h->Sx; h->g_dw = h->dw; h->g_launches = h->launches;
+    h->g_Sx = h->Sx; h->g_dw = h->dw;
   }
   const size_t bytes = (size_t)P.batch * P.n * sizeof(double);
   CUDA_TRY(cudaMemcpyAsync(h->gb, b, bytes, cudaMemcpyDeviceToDevice, h->stream));
   CUDA_TRY(cudaGraphLaunch(h->solve_exec, h->stream));
   CUDA_TRY(cudaMemcpyAsync(x, h->gx, bytes, cudaMemcpyDeviceToDevice, h->stream));
-  h->launches = h->g_launches;
+  h->launches = h->g_pro;
+  h->graph_solve_pending = true;  // body executions known once the stream has drained
   return KKT_OK;
 }
 
@@ -749,6 +852,7 @@ extern "C" kkt_status hykkt_solve(kkt_handle h, const double* rbar1, const doubl
   if (cg_rtol <= 0) cg_rtol = 1e-12;
   if (cg_maxit <= 0) cg_maxit = std::max(1, std::min(P.m_eq, 2000));
   h->launches = 0;
+  h->graph_solve_pending = false;
   if (P.m_eq == 0) return kkt_solve(h, rbar1, dx, max_outer_refine, 0.0);
   TRY(hykkt_pass(h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, true));
   const long long nn = (long long)P.batch * P.n, mm = (long long)P.batch * P.m_eq;
@@ -916,6 +1020,13 @@ extern "C" kkt_status kkt_get_trace(kkt_handle h, long long* stamps) {
 
 extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
   if (!h || !launches) return KKT_ERR_ARG;
+  if (h->graph_solve_pending && h->solve_while) {  // a graph solve: add its executed correction sweeps
+    int sw = 0;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    CUDA_TRY(cudaMemcpy(&sw, h->C.sweep, sizeof(int), cudaMemcpyDeviceToHost));
+    h->launches = h->g_pro + h->g_body * std::max(0, sw - (h->g_max_refine >= 1 ? 2 : 1));
+    h->graph_solve_pending = false;
+  }
   *launches = h->launches;
   return KKT_OK;
 }
