@@ -49,6 +49,31 @@ __device__ __forceinline__ void spin_acquire(const int* f, int target) {
   while (ld_volatile(f) < target) { }
   fence_acq_rel();
 }
+// Programmatic dependent launch: let the next kernel in the stream start now (its CTAs wait
+// on device flags, not on this grid's completion).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Wait until every child of an initial big task has been counted by the small phase (which may
+// still be running when the big kernel is a programmatic dependent), then reset the counter.
+__device__ __forceinline__ void wait_children_reset(int* c, int nch) {
+  while (ld_volatile(c) < nch) { __nanosleep(64); }
+  fence_acq_rel();
+  *c = 0;
+}
+// Bottom-up hand-off into a big (CTA) parent whose small children may still be running in the
+// overlapped small kernel: big children add 1 << 16 and the LAST big child continues with the
+// parent after the small children (each adds 1) have all arrived; it then resets the counter.
+// Returns true if the caller continues with the parent.  Called by one thread.
+__device__ __forceinline__ bool big_child_arrive(const DevPlan& P, int* c, int par_c0, int par_c1) {
+  int nbig = 0;
+  for (int ci = par_c0; ci < par_c1; ci++) nbig += P.chinfo[ci].big ? 1 : 0;
+  const int nsmall = (par_c1 - par_c0) - nbig;
+  const int old = atom_add_acq_rel(c, 1 << 16);
+  if ((old >> 16) != nbig - 1) return false;
+  while ((ld_volatile(c) & 0xffff) < nsmall) { __nanosleep(64); }
+  fence_acq_rel();
+  *c = 0;
+  return true;
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, c
   double* region = sm + (long long)wid * KKT_SCAP;
   const int ninit = P.n_up_s * P.batch;
   auto wsync = [] { __syncwarp(); };
+  pdl_launch_dependents();
   for (;;) {
     const int t = warp_ticket(ctl);
     if (t >= ninit) break;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, c
       assemble_front(P, I, F, U, usz, Kv, Ub, lane, 32, wsync);
       if (lane == 0) trace_stamp(P, 0, s, b, 2);
       int fk = -1;
-      front_factor_warp(F, U, I.r, I.w, lane, Dv_all + (long long)b * P.n + I.f0, &fk);
+      front_factor_warp2(F, U, I.r, I.w, lane, Dv_all + (long long)b * P.n + I.f0, &fk);
       if (lane == 0) trace_stamp(P, 0, s, b, 3);
       double* Lg = Lx + I.Lp;
       for (int q = lane; q < I.r * I.w; q += 32) Lg[q] = F[q];
@@ -190,7 +191,11 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
     double* Lx = Lx_all + (long long)b * P.nnzL_stored;
     double* Ub = U_all + (long long)b * P.update_doubles;
     const double* Kv = Kv_all + (long long)b * P.nnzK;
-    if (tid == 0) cnt[s] = 0;  // completed by phase-1 children
+    if (tid == 0) {  // all children are small: wait for phase 1 to have counted them
+      const SnInfo I0 = P.sn[s];
+      wait_children_reset(cnt + s, I0.c1 - I0.c0);
+    }
+    __syncthreads();
     for (;;) {
       if (tid == 0) trace_stamp(P, 0, s, b, 0);
       const SnInfo I = P.sn[s];
@@ -205,7 +210,9 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
       assemble_front(P, I, F, U, usz, Kv, Ub, tid, blockDim.x, bsync);
       if (tid == 0) trace_stamp(P, 0, s, b, 2);
       double* dv = Dv_all + (long long)b * P.n + I.f0;
-      if (in_smem) front_factor_cta<8>(F, U, r, w, dv, &s_fail);
+      // left-looking 32-column blocks for medium/large fronts in shared memory (one U update,
+      // three barriers per block); narrow short fronts keep the 8-column right-looking kernel
+      if (in_smem && (w >= 20 || r >= 128)) front_factor_cta_ll(F, U, r, w, dv, &s_fail);
       else front_factor_cta<8>(F, U, r, w, dv, &s_fail);
       __syncthreads();
       if (tid == 0) trace_stamp(P, 0, s, b, 3);
@@ -229,9 +236,7 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
           red_release_add(cnt + I.par, 1);
           s_last = 0;
         } else {
-          const int old = atom_add_acq_rel(cnt + I.par, 1);
-          s_last = (old == Ip.c1 - Ip.c0 - 1);
-          if (s_last) cnt[I.par] = 0;
+          s_last = big_child_arrive(P, cnt + I.par, Ip.c0, Ip.c1);
         }
       }
       __syncthreads();

@@ -73,7 +73,8 @@ struct kkt_plan {
   double2* T = nullptr;
   double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
-  TaskQueue TQ{};
+  TaskQueue TQ{}, TQs{};  // work queues of bwd_big / bwd_small (separate: the two may overlap)
+  int *bflag = nullptr;  // [batch][ns] backward hand-off big parent -> small children (PDL overlap)
   int *fcnt = nullptr, *facnt = nullptr, *ctl = nullptr, *fail = nullptr,
       *status = nullptr;
   DevCtrl C{};
@@ -99,6 +100,8 @@ struct kkt_plan {
   int g_hsolve = 1;
   long long g_pro = 0, g_body = 0;   // kernels in the solve graph's prologue / per correction sweep
   bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
+  bool pdl = true;                   // overlap the small/big tree phases (programmatic launch)
+  int pdl_mask = 7;
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
 
@@ -148,7 +151,10 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->fcnt = c.take<int>(B * ns);
   h->TQ.q = c.take<int>(B * ns);
   h->TQ.flag = c.take<int>(B * ns);
+  h->TQs.q = c.take<int>(B * ns);
+  h->TQs.flag = c.take<int>(B * ns);
   h->facnt = c.take<int>(B * ns);
+  h->bflag = c.take<int>(B * ns);
   h->ctl = c.take<int>(8 * KKT_CTL);
   h->fail = c.take<int>(1);
   h->status = c.take<int>(1);
@@ -351,6 +357,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
   h->use_graph = !(getenv("KKT_NO_GRAPH") && atoi(getenv("KKT_NO_GRAPH")) > 0);
   h->solve_while = getenv("KKT_SOLVE_WHILE") && atoi(getenv("KKT_SOLVE_WHILE")) > 0;
+  h->pdl = !(getenv("KKT_NO_PDL") && atoi(getenv("KKT_NO_PDL")) > 0);
+  h->pdl_mask = getenv("KKT_PDL_MASK") ? atoi(getenv("KKT_PDL_MASK")) : 7;  // 1 factor, 2 forward, 4 backward
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   h->sms = prop.multiProcessorCount;
@@ -507,6 +515,26 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   return KKT_OK;
 }
 
+// Launch `kern` as a programmatic dependent of the previous kernel in the stream: it may start
+// as soon as every CTA of that kernel has executed griddepcontrol.launch_dependents, and orders
+// itself against the producer through device flags instead of kernel completion (the small/big
+// phase boundary of the tree kernels).  Set KKT_NO_PDL=1 to serialise instead.
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, int smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int grid_for(long long total, int threads, int sms) {
   long long g = (total + threads - 1) / threads;
   return (int)std::max(1LL, std::min(g, (long long)sms * 16));
@@ -553,9 +581,9 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     h->launches++;
   }
   if (!P.up_bf.empty()) {
-    factor_big_kernel<<<h->g_fbig, KKT_BNT, h->fbig_smem, h->ls>>>(
-        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 1 * KKT_CTL, h->fail, h->factor_smem_cap);
-    LAUNCH_CHECK();
+    CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 1) && !P.order_s.empty(), factor_big_kernel, h->g_fbig, KKT_BNT, h->fbig_smem, h->ls,
+                        h->dp, (const double*)h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 1 * KKT_CTL, h->fail,
+                        (long long)h->factor_smem_cap));
     h->launches++;
   }
   if (!P.order_h.empty()) {
@@ -585,9 +613,9 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
   }
   if (!P.order_b.empty()) {
     if (!P.up_bf.empty()) {
-      fwd_big_kernel<<<h->g_tbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-          h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 3 * KKT_CTL, done, h->pcap);
-      LAUNCH_CHECK();
+      CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 2) && !P.order_s.empty(), fwd_big_kernel, h->g_tbig, KKT_BNT, h->tbig_smem, h->ls,
+                          h->dp, (const double*)h->Lx, (const double*)h->Dv, rhs, rs, h->Y, h->uv, h->fcnt,
+                          h->ctl + 3 * KKT_CTL, done, h->pcap));
       h->launches++;
     }
     if (!P.order_h.empty()) {
@@ -604,15 +632,17 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
     }
     if (P.order_b.size() > P.order_h.size()) {
       bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap);
+          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap, h->bflag);
       LAUNCH_CHECK();
       h->launches++;
     }
   }
   if (!P.order_s.empty()) {
-    bwd_small_kernel<<<h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
-        h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 5 * KKT_CTL, done);
-    LAUNCH_CHECK();
+    // overlapped with bwd_big only when bwd_big is the kernel right before it
+    const bool after_big = P.order_b.size() > P.order_h.size() && (h->pdl_mask & 4);
+    CUDA_TRY(launch_pdl(h->pdl && after_big, bwd_small_kernel, h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls,
+                        h->dp, (const double*)h->Lx, (const double*)h->Dv, (const double*)h->Y, h->Xp, xout, xs,
+                        h->TQs, h->ctl + 5 * KKT_CTL, done, h->bflag, (int)(h->pdl && after_big)));
     h->launches++;
   }
   return KKT_OK;

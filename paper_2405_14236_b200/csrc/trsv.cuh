@@ -142,6 +142,96 @@ __device__ __forceinline__ void bwd_sweep_any(const double* Lp, int r, int w, co
   else bwd_sweep_warp<4>(Lp, r, w, dv, xa, lane);  // callers guarantee w <= 128
 }
 
+// Forward-solve input of a small supernode (one warp, r <= 64): panel -> Pn (shared), and
+// v = [b(perm(cols)); 0] + extend-add of the children's update vectors (in child order).
+// All loads are issued before the first dependent use: child metadata arrives with the panel
+// and permutation, then the right-hand side and up to 8 chunks of 32 update entries per lane
+// are in flight together; only the (rare) remainder falls back to a chunk-by-chunk loop.
+__device__ __forceinline__ void stage_in(const DevPlan& P, const SnInfo& I, const double* __restrict__ L,
+                                         const double* __restrict__ bb, const double* uv, double* Pn,
+                                         double* v, int lane) {
+  const int r = I.r, w = I.w, rw = r * w, nch = I.c1 - I.c0;
+  if (nch > 32) {  // many children: plain chunk-by-chunk path
+    copy_g2s<false>(Pn, L, rw, lane, 32);
+    for (int q = lane; q < r; q += 32) v[q] = (q < w) ? bb[__ldg(P.perm + I.f0 + q)] : 0.0;
+    __syncwarp();
+    for (int c = I.c0; c < I.c1; c++) {
+      const SnInfo C = P.chinfo[c];
+      const int Rq = C.r - C.w;
+      for (int q = lane; q < Rq; q += 32) v[__ldg(P.sn_rel + C.rp0 + C.w + q)] += ldcg(uv + C.uvp + q);
+      __syncwarp();
+    }
+    return;
+  }
+  // metadata
+  const int p0 = (lane < w) ? __ldg(P.perm + I.f0 + lane) : 0;
+  const int p1 = (lane + 32 < w) ? __ldg(P.perm + I.f0 + lane + 32) : 0;
+  int cR = 0, cRel = 0, cU = 0;
+  if (lane < nch) {
+    const int4 h = __ldg(reinterpret_cast<const int4*>(P.chinfo + I.c0 + lane));  // f0, w, r, rp0
+    cR = h.z - h.y;
+    cRel = h.w + h.y;
+    cU = __ldg(reinterpret_cast<const int*>(P.chinfo + I.c0 + lane) + 10);        // uvp
+  }
+  // panel
+  double lv[8];
+#pragma unroll
+  for (int u = 0; u < 8; u++) lv[u] = (lane + 32 * u < rw) ? __ldg(L + lane + 32 * u) : 0.0;
+  // right-hand side (own columns)
+  const double b0 = (lane < w) ? bb[p0] : 0.0;
+  const double b1 = (lane + 32 < w) ? bb[p1] : 0.0;
+  // children's update entries: slot k <-> (child ci, chunk base), uniform across the warp
+  int bpos[8], bch[8];
+  double bval[8];
+  int ci = 0, base = 0;
+  int Rc = nch > 0 ? __shfl_sync(0xffffffffu, cR, 0) : 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    while (ci < nch && base >= Rc) {
+      ci++;
+      base = 0;
+      Rc = (ci < nch) ? __shfl_sync(0xffffffffu, cR, ci) : 0;
+    }
+    bch[k] = ci;
+    bpos[k] = -1;
+    bval[k] = 0.0;
+    if (ci < nch) {
+      const int relp = __shfl_sync(0xffffffffu, cRel, ci), up = __shfl_sync(0xffffffffu, cU, ci);
+      const int q = base + lane;
+      if (q < Rc) { bpos[k] = __ldg(P.sn_rel + relp + q); bval[k] = ldcg(uv + up + q); }
+      base += 32;
+    }
+  }
+  // stores: panel, v init, then the children in order
+#pragma unroll
+  for (int u = 0; u < 8; u++) if (lane + 32 * u < rw) Pn[lane + 32 * u] = lv[u];
+  if (rw > 256) copy_g2s<false>(Pn + 256, L + 256, rw - 256, lane, 32);
+  if (lane < r) v[lane] = (lane < w) ? b0 : 0.0;
+  if (lane + 32 < r) v[lane + 32] = (lane + 32 < w) ? b1 : 0.0;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    if (k > 0 && bch[k] != bch[k - 1]) __syncwarp();
+    if (bpos[k] >= 0) v[bpos[k]] += bval[k];
+  }
+  __syncwarp();
+  // remainder (more than 8 chunks of children entries)
+  while (ci < nch) {
+    while (ci < nch && base >= Rc) {
+      ci++;
+      base = 0;
+      Rc = (ci < nch) ? __shfl_sync(0xffffffffu, cR, ci) : 0;
+      __syncwarp();
+    }
+    if (ci >= nch) break;
+    const int relp = __shfl_sync(0xffffffffu, cRel, ci), up = __shfl_sync(0xffffffffu, cU, ci);
+    const int q = base + lane;
+    if (q < Rc) v[__ldg(P.sn_rel + relp + q)] += ldcg(uv + up + q);
+    base += 32;
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, const double* __restrict__ Lx_all,
                                                                  const double* __restrict__ Dv_all,
                                                                  const double* __restrict__ rhs, long long rs,
@@ -152,7 +242,8 @@ __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, cons
   double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
   double* v = Pn + KKT_SCAP;
   const int ninit = P.n_up_s * P.batch;
-  if (done && done[P.batch] == 0) return;  // every instance has finished refining  // refinement finished: nothing to do
+  pdl_launch_dependents();
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining
   for (;;) {
     const int t = warp_ticket(ctl);
     if (t >= ninit) break;
@@ -165,41 +256,29 @@ __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, cons
     double* uv = uv_all + (long long)b * P.uvec_doubles;
     const double* bb = rhs + (long long)b * rs;
     double* Y = Y_all + (long long)b * P.n;
+    SnInfo I = P.sn[s];
     for (;;) {
       if (lane == 0) trace_stamp(P, 1, s, b, 0);
-      const SnInfo I = P.sn[s];
-      const int r = I.r, w = I.w, R = r - w;
+      const int r = I.r, w = I.w;
       const double* L = Lb + I.Lp;
-      copy_g2s<false>(Pn, L, r * w, lane, 32);
-      for (int q = lane; q < r; q += 32) v[q] = (q < w) ? bb[__ldg(P.perm + I.f0 + q)] : 0.0;
-      __syncwarp();
-      for (int ci = I.c0; ci < I.c1; ci++) {
-        const SnInfo C = P.chinfo[ci];
-        const int Rc = C.r - C.w;
-        const int* rel = P.sn_rel + C.rp0 + C.w;
-        const double* u = uv + C.uvp;
-        for (int base = lane; base < Rc; base += 32 * 4) {
-          int ps[4]; double val[4];
-#pragma unroll
-          for (int k = 0; k < 4; k++)
-            if (base + 32 * k < Rc) { ps[k] = __ldg(rel + base + 32 * k); val[k] = ldcg(u + base + 32 * k); }
-#pragma unroll
-          for (int k = 0; k < 4; k++)
-            if (base + 32 * k < Rc) v[ps[k]] += val[k];
-        }
-        __syncwarp();
-      }
-      // sweep: y_k = v_k / L_kk ; v_i -= L_ik y_k for i > k (covers L11 and L21), registers
+      // every independent load of the supernode is issued before the first use (one memory
+      // round trip for metadata, one for values): parent info, own permutation entries,
+      // children's info (lane c holds child c), the panel (registers), then the right-hand
+      // side and the children's update vectors
+      SnInfo Ip;
+      if (I.par >= 0) Ip = P.sn[I.par];
+      stage_in(P, I, L, bb, uv, Pn, v, lane);
       fwd_sweep_any(Pn, r, w, Dv + I.f0, v, lane);
       __syncwarp();
       for (int q = lane; q < w; q += 32) Y[I.f0 + q] = v[q];
       if (lane == 0) trace_stamp(P, 1, s, b, 1);
       if (I.par < 0) break;
+      const int R = r - w;
       double* us = uv + I.uvp;
       for (int q = lane; q < R; q += 32) us[q] = v[w + q];
-      const SnInfo Ip = P.sn[I.par];
       if (!warp_signal_parent(I, Ip, cnt, lane, true)) break;
       s = I.par;
+      I = Ip;
     }
   }
   warp_exit(ctl, gridDim.x * KKT_WPB);
@@ -229,7 +308,11 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
     double* uv = uv_all + (long long)b * P.uvec_doubles;
     const double* bb = rhs + (long long)b * rs;
     double* Y = Y_all + (long long)b * P.n;
-    if (tid == 0) cnt[s] = 0;
+    if (tid == 0) {  // all children are small: wait for the small phase to have counted them
+      const SnInfo I0 = P.sn[s];
+      wait_children_reset(cnt + s, I0.c1 - I0.c0);
+    }
+    __syncthreads();
     for (;;) {
       if (tid == 0) trace_stamp(P, 1, s, b, 0);
       const SnInfo I = P.sn[s];
@@ -256,9 +339,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       if (P.sn[I.par].huge) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
       if (tid == 0) {
         const SnInfo Ip = P.sn[I.par];
-        const int old = atom_add_acq_rel(cnt + I.par, 1);
-        s_last = (old == Ip.c1 - Ip.c0 - 1);
-        if (s_last) cnt[I.par] = 0;
+        s_last = big_child_arrive(P, cnt + I.par, Ip.c0, Ip.c1);
       }
       __syncthreads();
       if (!s_last) break;
@@ -291,25 +372,45 @@ __device__ __forceinline__ int pop_task(int* ctl, const int* init, int ninit_nod
 }
 
 // Continue with the first eligible child, push the others.  Called by one lane / thread after
-// the supernode's results are globally visible.
+// the supernode's results are globally visible.  One slot reservation for all pushed children;
+// a supernode with an eligible child cannot be the phase's last completion (the child completes
+// after it), so it counts itself with a fire-and-forget reduction and only childless supernodes
+// wait for the counter (all-done detection) -- the continuation pays at most one round trip.
 __device__ __forceinline__ int spawn_children(const DevPlan& P, const SnInfo& I, int b, int* ctl,
                                               TaskQueue Q, bool big_phase, int total) {
-  int next = -1;
+  int next = -1, nextra = 0;
   for (int ci = I.c0; ci < I.c1; ci++) {
-    const int c = __ldg(P.sn_ch + ci);
-    if (big_phase && !P.sn[c].big) continue;  // small children start phase 2 from dn_s
-    const int task = c * P.batch + b;
-    if (next < 0) {
-      next = task;
-    } else {
-      const int slot = atomicAdd(ctl + 2, 1);
-      Q.q[slot] = task;
+    if (big_phase && !P.chinfo[ci].big) continue;  // small children start phase 2 from dn_s
+    if (next < 0) next = __ldg(P.sn_ch + ci) * P.batch + b;
+    else nextra++;
+  }
+  if (nextra > 0) {
+    int slot = atomicAdd(ctl + 2, nextra);
+    bool first = true;
+    for (int ci = I.c0; ci < I.c1; ci++) {
+      if (big_phase && !P.chinfo[ci].big) continue;
+      if (first) { first = false; continue; }
+      Q.q[slot] = __ldg(P.sn_ch + ci) * P.batch + b;
       st_release(Q.flag + slot, 1);
+      slot++;
     }
   }
-  __threadfence();
-  if (atomicAdd(ctl + 3, 1) == total - 1) st_release(ctl + 8, 1);  // completed -> all done
+  if (next >= 0) {
+    atomicAdd(ctl + 3, 1);  // result unused -> RED
+  } else {
+    __threadfence();
+    if (atomicAdd(ctl + 3, 1) == total - 1) st_release(ctl + 8, 1);  // completed -> all done
+  }
   return next;
+}
+
+// Backward hand-off from a big (CTA) supernode to its small children, which the small kernel
+// may already be polling (programmatic launch): the flag holds the number of small children
+// still to consume it; each consumer decrements it, so every flag is back to 0 after a solve.
+__device__ __forceinline__ void release_small_children(const DevPlan& P, const SnInfo& I, int s, int b, int* bflag) {
+  int nsm = 0;
+  for (int ci = I.c0; ci < I.c1; ci++) nsm += P.chinfo[ci].big ? 0 : 1;
+  if (nsm) st_release(bflag + (long long)b * P.ns + s, nsm);
 }
 
 // ---------------------------------------------------------------- backward, big (CTA)
@@ -317,9 +418,11 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
                                                           const double* __restrict__ Dv_all,
                                                           const double* __restrict__ Y_all, double* Xp_all,
                                                           double* xout, long long xs, TaskQueue Q,
-                                                          int* ctl, const int* __restrict__ done, int pcap) {
+                                                          int* ctl, const int* __restrict__ done, int pcap,
+                                                          int* bflag) {
   extern __shared__ double sm[];
   __shared__ int s_task;
+  pdl_launch_dependents();
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int total = P.ns_bn * P.batch;
   double* xa = sm;                   // [max_front]  x over R_s (own columns then ancestors)
@@ -336,7 +439,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     }
     const int s = task / P.batch, b = task % P.batch;
     if (done && done[b]) {  // finished instance: account for its whole subtree without work
-      if (tid == 0) s_task = spawn_children(P, P.sn[s], b, ctl, Q, true, total);
+      if (tid == 0) { release_small_children(P, P.sn[s], s, b, bflag); s_task = spawn_children(P, P.sn[s], b, ctl, Q, true, total); }
       __syncthreads();
       task = s_task;
       __syncthreads();
@@ -359,7 +462,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     if (tid == 0) trace_stamp(P, 2, s, b, 1);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_task = spawn_children(P, I, b, ctl, Q, true, total);
+    if (tid == 0) { release_small_children(P, I, s, b, bflag); s_task = spawn_children(P, I, b, ctl, Q, true, total); }
     __syncthreads();
     task = s_task;
     __syncthreads();
@@ -372,14 +475,18 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
                                                                  const double* __restrict__ Dv_all,
                                                                  const double* __restrict__ Y_all, double* Xp_all,
                                                                  double* xout, long long xs, TaskQueue Q,
-                                                                 int* ctl, const int* __restrict__ done) {
+                                                                 int* ctl, const int* __restrict__ done,
+                                                                 int* bflag, int pdl) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
   double* xa = Pn + KKT_SCAP;
   const int total = P.ns_s * P.batch;
+  (void)pdl;
   if (done && done[P.batch] == 0) return;  // every instance has finished refining
   int task = -1;
+  SnInfo Cn;           // first child's metadata, prefetched (the continuation's next supernode)
+  int cn_task = -1;
   for (;;) {
     if (task < 0) {
       int t = 0;
@@ -388,20 +495,53 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
       if (task < 0) break;
     }
     const int s = task / P.batch, b = task % P.batch;
-    const SnInfo I = P.sn[s];
+    const SnInfo I = (task == cn_task) ? Cn : P.sn[s];
+    if (I.par >= 0 && task != cn_task) {  // a small root under a big (CTA) parent: take its hand-off
+      int t = 0;
+      if (lane == 0) {
+        const SnInfo Ipar = P.sn[I.par];
+        if (Ipar.big && !Ipar.huge) {
+          int* f = bflag + (long long)b * P.ns + I.par;
+          while (ld_volatile(f) <= 0) { __nanosleep(64); }
+          fence_acq_rel();
+          atomicSub(f, 1);
+        }
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+    }
     if (done && done[b]) {
       int t = 0;
       if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false, total);
       task = __shfl_sync(0xffffffffu, t, 0);
+      cn_task = -1;
       continue;
     }
     if (lane == 0) trace_stamp(P, 2, s, b, 0);
-    const int r = I.r, w = I.w;
+    const int r = I.r, w = I.w, rw = r * w;
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     double* Xp = Xp_all + (long long)b * P.n;
     const double* Y = Y_all + (long long)b * P.n;
-    copy_g2s<false>(Pn, L, r * w, lane, 32);
-    for (int q = lane; q < r; q += 32) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
+    // every independent load first: child metadata, row indices / permutation, panel, y;
+    // then the ancestors' x (dependent on the row indices)
+    cn_task = -1;
+    if (I.c0 < I.c1) { Cn = P.chinfo[I.c0]; cn_task = __ldg(P.sn_ch + I.c0) * P.batch + b; }
+    const int q0 = lane, q1 = lane + 32;
+    const int i0 = (q0 >= w && q0 < r) ? __ldg(P.sn_rows + I.rp0 + q0) : 0;
+    const int i1 = (q1 >= w && q1 < r) ? __ldg(P.sn_rows + I.rp0 + q1) : 0;
+    const int p0 = (q0 < w) ? __ldg(P.perm + I.f0 + q0) : 0;
+    const int p1 = (q1 < w) ? __ldg(P.perm + I.f0 + q1) : 0;
+    double lv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) lv[u] = (lane + 32 * u < rw) ? __ldg(L + lane + 32 * u) : 0.0;
+    double x0 = (q0 < w) ? ldcg(Y + I.f0 + q0) : 0.0, x1 = (q1 < w) ? ldcg(Y + I.f0 + q1) : 0.0;
+    if (q0 >= w && q0 < r) x0 = ldcg(Xp + i0);
+    if (q1 >= w && q1 < r) x1 = ldcg(Xp + i1);
+#pragma unroll
+    for (int u = 0; u < 8; u++) if (lane + 32 * u < rw) Pn[lane + 32 * u] = lv[u];
+    if (rw > 256) copy_g2s<false>(Pn + 256, L + 256, rw - 256, lane, 32);
+    if (q0 < r) xa[q0] = x0;
+    if (q1 < r) xa[q1] = x1;
+    for (int q = lane + 64; q < r; q += 32) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
     __syncwarp();
     if (w <= 128) {
       bwd_sweep_any(Pn, r, w, Dv_all + (long long)b * P.n + I.f0, xa, lane);
@@ -418,13 +558,14 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
       }
     }
     double* xo = xout + (long long)b * xs;
-    for (int q = lane; q < w; q += 32) {
+    if (q0 < w) { Xp[I.f0 + q0] = xa[q0]; xo[p0] = xa[q0]; }
+    if (q1 < w) { Xp[I.f0 + q1] = xa[q1]; xo[p1] = xa[q1]; }
+    for (int q = lane + 64; q < w; q += 32) {
       Xp[I.f0 + q] = xa[q];
       xo[__ldg(P.perm + I.f0 + q)] = xa[q];
     }
     if (lane == 0) trace_stamp(P, 2, s, b, 1);
-    __threadfence();
-    __syncwarp();
+    __syncwarp();  // lanes' x writes are ordered before lane 0's release (spawn_children)
     int t = 0;
     if (lane == 0) t = spawn_children(P, I, b, ctl, Q, false, total);
     task = __shfl_sync(0xffffffffu, t, 0);
