@@ -611,6 +611,14 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
       I.k0 = P.Kp[snf[s]]; I.k1 = P.Kp[snf[s + 1]];
       I.Lp = P.sn_Lp[s]; I.Up = P.sn_Up[s]; I.uvp = (int)P.sn_uvp[s]; I.huge = huge[s];
     }
+    P.sn_Lip.assign(ns, -1);
+    P.linv_doubles = 0;
+    for (int s = 0; s < ns; s++)
+      if (big[s] && !huge[s]) {
+        const long long w = snf[s + 1] - snf[s];
+        P.sn_Lip[s] = P.linv_doubles;
+        P.linv_doubles += w * w;
+      }
     P.chinfo.resize(P.sn_ch.size());
     for (size_t t = 0; t < P.sn_ch.size(); t++) P.chinfo[t] = P.sn[P.sn_ch[t]];
     for (int s : P.order) {

@@ -44,7 +44,8 @@ struct DevPlan {
   int n_up_s, n_up_b, n_dn_b, n_dn_s;
   const int *up_bf, *order_h;    // big non-huge bottom-up start list; huge supernodes in order
   int n_up_bf, n_h;
-  const long long *sn_Lp, *sn_Up, *sn_uvp;
+  const long long *sn_Lp, *sn_Up, *sn_uvp, *sn_Lip;
+  long long linv_doubles;
   const int *Wf_p, *Wf_c, *Wf_k, *Jt_p, *Jt_r, *Jt_k, *Gt_end;
   const int *Jrp, *Jci;       // J CSR pattern (caller's, copied at analysis)
 };

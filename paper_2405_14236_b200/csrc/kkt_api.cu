@@ -74,6 +74,7 @@ struct kkt_plan {
   double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
   TaskQueue TQ{}, TQs{};  // work queues of bwd_big / bwd_small (separate: the two may overlap)
+  double* Li = nullptr;   // [batch][linv_doubles] L11^-1 of the big (CTA) supernodes (solve operator)
   int *bflag = nullptr;  // [batch][ns] backward hand-off big parent -> small children (PDL overlap)
   int *fcnt = nullptr, *facnt = nullptr, *ctl = nullptr, *fail = nullptr,
       *status = nullptr;
@@ -102,6 +103,8 @@ struct kkt_plan {
   bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
   bool pdl = true;                   // overlap the small/big tree phases (programmatic launch)
   int pdl_mask = 7;
+  bool use_linv = true;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
+  int linv_smem = 0, g_linv = 1;
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
 
@@ -124,6 +127,7 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   size_t B = P.batch, n = P.n, m = P.m, me = P.m_eq, ns = P.ns;
   h->Kv = c.take<double>(B * P.Kp[n]);
   h->Lx = c.take<double>(B * P.nnzL_stored);
+  h->Li = c.take<double>(B * std::max(P.linv_doubles, 1LL));
   h->Ub = c.take<double>(B * P.update_doubles);
   h->uv = c.take<double>(B * P.uvec_doubles);
   h->Y = c.take<double>(B * n);
@@ -359,6 +363,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->solve_while = getenv("KKT_SOLVE_WHILE") && atoi(getenv("KKT_SOLVE_WHILE")) > 0;
   h->pdl = !(getenv("KKT_NO_PDL") && atoi(getenv("KKT_NO_PDL")) > 0);
   h->pdl_mask = getenv("KKT_PDL_MASK") ? atoi(getenv("KKT_PDL_MASK")) : 7;  // 1 factor, 2 forward, 4 backward
+  h->use_linv = !(getenv("KKT_NO_LINV") && atoi(getenv("KKT_NO_LINV")) > 0);
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   h->sms = prop.multiProcessorCount;
@@ -372,7 +377,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
                                   &P.order, &P.order_s, &P.order_b, &P.up_s, &P.up_b,
                                   &P.dn_b, &P.dn_s, &P.up_bf, &P.order_h, &P.Wf_p, &P.Wf_c, &P.Wf_k, &P.Jt_p, &P.Jt_r,
                                   &P.Jt_k, &P.Gt_end, &Jrp, &Jci};
-  const std::vector<long long>* lv[] = {&P.sn_Lp, &P.sn_Up, &P.sn_uvp};
+  const std::vector<long long>* lv[] = {&P.sn_Lp, &P.sn_Up, &P.sn_uvp, &P.sn_Lip};
   size_t tot = 0;
   for (auto* v : iv) tot += vbytes(*v);
   for (auto* v : lv) tot += vbytes(*v);
@@ -416,8 +421,10 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   d.dn_s = I(); d.up_bf = I(); d.order_h = I(); d.Wf_p = I(); d.Wf_c = I(); d.Wf_k = I(); d.Jt_p = I(); d.Jt_r = I();
   d.Jt_k = I(); d.Gt_end = I(); d.Jrp = I(); d.Jci = I();
   d.sn_Lp = (const long long*)dptr[k++];
+  d.linv_doubles = P.linv_doubles;
   d.sn_Up = (const long long*)dptr[k++];
   d.sn_uvp = (const long long*)dptr[k++];
+  d.sn_Lip = (const long long*)dptr[k++];
   d.sn = d_sn;
   d.chinfo = d_ch;
   d.trace = nullptr;
@@ -489,6 +496,20 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
   if (const char* e = getenv("KKT_BWD_CTAS")) h->g_bsmall = std::min(h->g_bsmall, std::max(1, atoi(e)));
   CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
+  {
+    long long maxw2 = 0;
+    for (int s_ : P.order_b)
+      if (P.sn_Lip[s_] >= 0) {
+        const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_], ld_ = (w_ + 31) / 32 * 32;
+        maxw2 = std::max(maxw2, ld_ * ld_);
+      }
+    if (maxw2 == 0 || maxw2 * 8 > 220 * 1024) h->use_linv = false;
+    if (h->use_linv) {
+      h->linv_smem = (int)(maxw2 * 8);
+      CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->linv_smem));
+      CUDA_TRY(grid_of(linv_kernel, KKT_BNT, h->linv_smem, (long long)P.order_b.size() * P.batch, 1, &h->g_linv));
+    }
+  }
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
     CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
@@ -586,6 +607,11 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
                         (long long)h->factor_smem_cap));
     h->launches++;
   }
+  if (h->use_linv) {  // L11^-1 of the big supernodes for the solve sweeps (parallel, off the tree path)
+    linv_kernel<<<h->g_linv, KKT_BNT, h->linv_smem, h->ls>>>(h->dp, h->Lx, h->Dv, h->Li);
+    LAUNCH_CHECK();
+    h->launches++;
+  }
   if (!P.order_h.empty()) {
     DevPlan dp = h->dp;
     const double* kv = h->Kv;
@@ -615,7 +641,7 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
     if (!P.up_bf.empty()) {
       CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 2) && !P.order_s.empty(), fwd_big_kernel, h->g_tbig, KKT_BNT, h->tbig_smem, h->ls,
                           h->dp, (const double*)h->Lx, (const double*)h->Dv, rhs, rs, h->Y, h->uv, h->fcnt,
-                          h->ctl + 3 * KKT_CTL, done, h->pcap));
+                          h->ctl + 3 * KKT_CTL, done, h->pcap, (const double*)(h->use_linv ? h->Li : nullptr)));
       h->launches++;
     }
     if (!P.order_h.empty()) {
@@ -632,7 +658,8 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
     }
     if (P.order_b.size() > P.order_h.size()) {
       bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap, h->bflag);
+          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap, h->bflag,
+          h->use_linv ? h->Li : nullptr);
       LAUNCH_CHECK();
       h->launches++;
     }

@@ -47,6 +47,7 @@ struct Plan {
   std::vector<long long> sn_Lp;  // [ns+1] panel offsets (r_s x w_s column-major, ld = r_s)
   std::vector<long long> sn_Up;  // [ns+1] packed lower update-matrix offsets, (R)(R+1)/2, R = r-w
   std::vector<long long> sn_uvp; // [ns+1] forward-solve update-vector offsets (length R)
+  std::vector<long long> sn_Lip; // [ns] offset of L11^-1 (w x w, col-major) of big non-huge supernodes, -1 otherwise
   std::vector<int> sn_parent;    // -1 root
   std::vector<int> sn_cp, sn_ch; // children lists (CSR)
   std::vector<int> sn_level;     // 0 = leaf
@@ -72,7 +73,7 @@ struct Plan {
   std::vector<int> Gt_end;             // per column: end of the rows < m_eq inside Jt (G^T prefix)
 
   // ---- stats ----
-  long long nnzL = 0, nnzL_stored = 0, nprod = 0, update_doubles = 0, uvec_doubles = 0;
+  long long nnzL = 0, nnzL_stored = 0, nprod = 0, update_doubles = 0, uvec_doubles = 0, linv_doubles = 0;
   double flops = 0.0, analyze_ms = 0.0, order_ms = 0.0;
 };
 

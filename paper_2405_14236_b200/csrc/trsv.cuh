@@ -127,6 +127,163 @@ __device__ __forceinline__ void cta_bwd_blocked(const double* __restrict__ L, in
   }
 }
 
+// =====================================================================================
+// Inverse-diagonal-block supernodal sweeps for the big (CTA) supernodes.  After the numeric
+// factorization, linv_kernel forms Li = L11^-1 of every big non-huge supernode (all in
+// parallel, off the tree's critical path); the solves then replace the w-step dependent
+// substitution on L11 by two data-parallel products per supernode:
+//   forward:   y1 = Li v[0:w),            u = v[w:r) - L21 y1
+//   backward:  z = y1 - L21^T x(anc),     x1 = Li^T z
+// (the same operator L11^-1 applied as a matrix; the refinement loop measures and corrects
+// the result against the unassembled operator exactly as before).
+// =====================================================================================
+__global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* __restrict__ Lx_all,
+                                                       const double* __restrict__ Dv_all, double* Li_all) {
+  // L11 staged row-major in shared memory, padded to nb*32 with the identity:
+  //   Ls[i * LD + k] = L11(i, k), LD = nb * 32.
+  // Phase 1: warp I inverts diagonal block I (lane j: column j in registers, substitution with
+  //          broadcast rows of L11).
+  // Phase 2: warp J forms the blocks below it in block column J, top to bottom:
+  //          X_IJ = -X_II * sum_{K=J}^{I-1} L_IK X_KJ   (X_KJ and X_II read back from Li).
+  extern __shared__ double Ls[];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const long long tasks = (long long)P.ns_b * P.batch;
+  for (long long t = blockIdx.x; t < tasks; t += gridDim.x) {
+    const int b = (int)(t % P.batch);
+    const int s = __ldg(P.order_b + t / P.batch);
+    const long long lip = __ldg(P.sn_Lip + s);
+    if (lip < 0) continue;  // huge: solved by the whole-GPU path
+    const SnInfo I = P.sn[s];
+    const int w = I.w, r = I.r, nb = (w + 31) >> 5, LD = nb * 32;
+    const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
+    const double* dv = Dv_all + (long long)b * P.n + I.f0;
+    double* Li = Li_all + (long long)b * P.linv_doubles + lip;  // column-major w x w
+    __syncthreads();
+    for (int q = tid; q < LD * LD; q += nt) {
+      const int i = q / LD, k = q % LD;
+      Ls[q] = (i < w && k < w) ? (k <= i ? __ldg(L + (long long)k * r + i) : 0.0) : (i == k ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    // phase 1: diagonal blocks
+    for (int Ib = warp; Ib < nb; Ib += nw) {
+      const int o = Ib * 32;
+      const int j = lane;
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        const double di = (o + i < w) ? __ldg(dv + o + i) : 1.0;
+        const double* Lrow = Ls + (o + i) * LD + o;
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < i; k++) a = fma(Lrow[k], x[k], a);
+        x[i] = (i < j) ? 0.0 : (i == j ? di : -di * a);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; i++)
+        if (o + i < w && o + j < w) Li[(long long)(o + j) * w + o + i] = x[i];
+    }
+    __syncthreads();
+    // phase 2: below-diagonal blocks, block column J per warp
+    for (int Jb = warp; Jb < nb - 1; Jb += nw) {
+      const int oj = Jb * 32, j = lane;
+      const bool jin = oj + j < w;
+      for (int Ib = Jb + 1; Ib < nb; Ib++) {
+        const int oi = Ib * 32;
+        double tacc[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) tacc[i] = 0.0;
+        for (int Kb = Jb; Kb < Ib; Kb++) {
+          const int ok = Kb * 32;
+          double xk[32];
+#pragma unroll
+          for (int k = 0; k < 32; k++) xk[k] = (jin && ok + k < w) ? Li[(long long)(oj + j) * w + ok + k] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            const double* Lrow = Ls + (oi + i) * LD + ok;
+            double a = tacc[i];
+#pragma unroll
+            for (int k = 0; k < 32; k++) a = fma(Lrow[k], xk[k], a);
+            tacc[i] = a;
+          }
+        }
+        // X_IJ = -X_II * T  (X_II lower triangular, read from Li: broadcast across lanes)
+        double xo[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+          double a = 0.0;
+#pragma unroll
+          for (int k = 0; k <= i; k++)
+            a = fma((oi + i < w && oi + k < w) ? Li[(long long)(oi + k) * w + oi + i] : (i == k ? 1.0 : 0.0),
+                    tacc[k], a);
+          xo[i] = -a;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+          if (jin && oi + i < w) Li[(long long)(oj + j) * w + oi + i] = xo[i];
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// forward sweep of a big supernode with Li: v[0:r) in shared memory; tmp: >= w doubles
+__device__ __forceinline__ void cta_fwd_inv(const double* __restrict__ L, const double* __restrict__ Li, int r,
+                                            int w, double* v, double* tmp, int tid, int nt) {
+  for (int i = tid; i < w; i += nt) {  // y1 = Li v[0:w) (lower triangular)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = 0;
+    for (; k + 3 <= i; k += 4) {
+      a0 = fma(__ldg(Li + (long long)k * w + i), v[k], a0);
+      a1 = fma(__ldg(Li + (long long)(k + 1) * w + i), v[k + 1], a1);
+      a2 = fma(__ldg(Li + (long long)(k + 2) * w + i), v[k + 2], a2);
+      a3 = fma(__ldg(Li + (long long)(k + 3) * w + i), v[k + 3], a3);
+    }
+    for (; k <= i; k++) a0 = fma(__ldg(Li + (long long)k * w + i), v[k], a0);
+    tmp[i] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+  for (int i = tid; i < w; i += nt) v[i] = tmp[i];
+  for (int i = w + tid; i < r; i += nt) {  // u = v[w:r) - L21 y1
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = 0;
+    for (; k + 3 < w; k += 4) {
+      a0 = fma(__ldg(L + (long long)k * r + i), tmp[k], a0);
+      a1 = fma(__ldg(L + (long long)(k + 1) * r + i), tmp[k + 1], a1);
+      a2 = fma(__ldg(L + (long long)(k + 2) * r + i), tmp[k + 2], a2);
+      a3 = fma(__ldg(L + (long long)(k + 3) * r + i), tmp[k + 3], a3);
+    }
+    for (; k < w; k++) a0 = fma(__ldg(L + (long long)k * r + i), tmp[k], a0);
+    v[i] -= (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+}
+
+// backward sweep of a big supernode with Li: xa[0:w) = y1 on entry, xa[w:r) = ancestors' x;
+// on return xa[0:w) = x1.  Warp per column (lanes along the contiguous column), fixed-order
+// shuffle reductions.  tmp: >= w doubles.
+__device__ __forceinline__ void cta_bwd_inv(const double* __restrict__ L, const double* __restrict__ Li, int r,
+                                            int w, double* xa, double* tmp, int tid, int nt) {
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int k = warp; k < w; k += nw) {  // z_k = y_k - L21(:,k)^T x(anc)
+    const double* Lk = L + (long long)k * r;
+    double a = 0.0;
+    for (int i = w + lane; i < r; i += 32) a = fma(__ldg(Lk + i), xa[i], a);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) tmp[k] = xa[k] - a;
+  }
+  __syncthreads();
+  for (int k = warp; k < w; k += nw) {  // x_k = sum_{i>=k} Li(i,k) z_i
+    const double* Lik = Li + (long long)k * w;
+    double a = 0.0;
+    for (int i = k + lane; i < w; i += 32) a = fma(__ldg(Lik + i), tmp[i], a);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) xa[k] = a;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- forward, small (warp)
 __device__ __forceinline__ void fwd_sweep_any(const double* Lp, int r, int w, const double* dv,
                                               double* v, int lane) {
@@ -290,7 +447,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
                                                           const double* __restrict__ rhs, long long rs,
                                                           double* Y_all, double* uv_all, int* cnt_all,
                                                           int* ctl, const int* __restrict__ done,
-                                                          int pcap) {
+                                                          int pcap, const double* __restrict__ Li_all) {
   extern __shared__ double sm[];
   __shared__ int s_task, s_last;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -328,7 +485,9 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
         for (int q = tid; q < Rc; q += nt) v[__ldg(rel + q)] += ldcg(u + q);
         __syncthreads();
       }
-      cta_fwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, v, tid, nt);
+      const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
+      if (lip >= 0) cta_fwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, v, sm + P.max_front, tid, nt);
+      else cta_fwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, v, tid, nt);
       for (int q = tid; q < w; q += nt) Y[I.f0 + q] = v[q];
       if (tid == 0) trace_stamp(P, 1, s, b, 1);
       if (I.par < 0) break;
@@ -419,7 +578,7 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
                                                           const double* __restrict__ Y_all, double* Xp_all,
                                                           double* xout, long long xs, TaskQueue Q,
                                                           int* ctl, const int* __restrict__ done, int pcap,
-                                                          int* bflag) {
+                                                          int* bflag, const double* __restrict__ Li_all) {
   extern __shared__ double sm[];
   __shared__ int s_task;
   pdl_launch_dependents();
@@ -453,7 +612,9 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     const double* Y = Y_all + (long long)b * P.n;
     for (int q = tid; q < r; q += nt) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
     __syncthreads();
-    cta_bwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part, tid, nt);
+    const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
+    if (lip >= 0) cta_bwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, xa, part, tid, nt);
+    else cta_bwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part, tid, nt);
     double* xo = xout + (long long)b * xs;
     for (int q = tid; q < w; q += nt) {
       Xp[I.f0 + q] = xa[q];
