@@ -35,7 +35,7 @@ __device__ __forceinline__ void warp_exit(int* ctl, int nwarps_total) {
 // F, U may live in shared or global memory; `nt`/`tid` describe the cooperating group
 // (a warp: nt = 32, tid = lane; a CTA: nt = blockDim, tid = threadIdx).  The caller
 // synchronises the group between the zero/scatter/extend-add stages via `sync`.
-template <class Sync>
+template <int MLP = KKT_MLP, class Sync>
 __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I, double* F,
                                                double* U, long long usz,
                                                const double* __restrict__ Kv, const double* Ub,
@@ -46,16 +46,16 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I
   for (long long q = tid; q < usz; q += nt) U[q] = 0.0;
   sync();
   // K entries of the supernode's columns: batched loads, then scatter
-  for (int base = I.k0 + tid; base < I.k1; base += nt * KKT_MLP) {
-    int pos[KKT_MLP];
-    double val[KKT_MLP];
+  for (int base = I.k0 + tid; base < I.k1; base += nt * MLP) {
+    int pos[MLP];
+    double val[MLP];
 #pragma unroll
-    for (int u = 0; u < KKT_MLP; u++) {
+    for (int u = 0; u < MLP; u++) {
       const int k = base + u * nt;
       if (k < I.k1) { pos[u] = __ldg(P.kpos + k); val[u] = __ldg(Kv + k); }
     }
 #pragma unroll
-    for (int u = 0; u < KKT_MLP; u++)
+    for (int u = 0; u < MLP; u++)
       if (base + u * nt < I.k1) F[pos[u]] = val[u];
   }
   sync();
@@ -69,15 +69,15 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I
     const double* Uc = Ub + C.Up;
     const long long tot = (long long)Rc * (Rc + 1) / 2;
     // each member walks the packed child matrix with stride nt (monotone q -> incremental
-    // column decode); KKT_MLP entries are loaded before any is accumulated.  Positions within
+    // column decode); MLP entries are loaded before any is accumulated.  Positions within
     // one child are distinct, so there are no conflicts; children are applied in order.
     int jc = 0;
     long long cs = 0;  // start of column jc
-    for (long long base = tid; base < tot; base += (long long)nt * KKT_MLP) {
-      int pi[KKT_MLP], pj[KKT_MLP];
-      double v[KKT_MLP];
+    for (long long base = tid; base < tot; base += (long long)nt * MLP) {
+      int pi[MLP], pj[MLP];
+      double v[MLP];
 #pragma unroll
-      for (int u = 0; u < KKT_MLP; u++) {
+      for (int u = 0; u < MLP; u++) {
         const long long q = base + (long long)u * nt;
         if (q < tot) {
           while (q >= cs + (Rc - jc)) { cs += Rc - jc; jc++; }
@@ -88,7 +88,7 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const SnInfo& I
         }
       }
 #pragma unroll
-      for (int u = 0; u < KKT_MLP; u++) {
+      for (int u = 0; u < MLP; u++) {
         if (base + (long long)u * nt < tot) {
           if (pj[u] < w) F[(long long)pj[u] * r + pi[u]] += v[u];
           else U[upk(pi[u] - w, pj[u] - w, R)] += v[u];

@@ -135,22 +135,13 @@ __device__ __forceinline__ void potrf_panel(double (&a)[HB], double& myinv, int&
 
 __device__ __forceinline__ void tile_potrf(const HFront& H, int k, double* dinv, double* pb, int lane,
                                            int* fail_col) {
-  const int c0 = k * HB, kb = H.bsize(k);
-  double a[HB];
-#pragma unroll
-  for (int c = 0; c < HB; c++)
-    a[c] = (lane < kb && c < kb && c <= lane) ? ldcg(H.F + (long long)(c0 + c) * H.r + c0 + lane) : 0.0;
-  double myinv = 0.0;
-  int fc = *fail_col;
-  potrf_panel<0>(a, myinv, fc, pb, lane, kb, c0);
-  if (kb > 8) potrf_panel<1>(a, myinv, fc, pb, lane, kb, c0);
-  if (kb > 16) potrf_panel<2>(a, myinv, fc, pb, lane, kb, c0);
-  if (kb > 24) potrf_panel<3>(a, myinv, fc, pb, lane, kb, c0);
-  *fail_col = fc;
-#pragma unroll
-  for (int c = 0; c < HB; c++)
-    if (lane < kb && c < kb && c <= lane) H.F[(long long)(c0 + c) * H.r + c0 + lane] = a[c];
-  if (lane < kb) dinv[c0 + lane] = myinv;
+  // software-pipelined warp Cholesky of the diagonal tile (dense.cuh ll_diag_warp: raw shuffle +
+  // branch-free rsqrt on the pivot chain, shared-memory column broadcasts); loads bypass L1
+  // (the tile was produced by other SMs in this launch).  pb: the warp's 32 x 32 scratch.
+  int fk = -1;
+  ll_diag_warp<true>(H.F, H.r, k * HB, H.bsize(k), lane, dinv, pb, pb, &fk);
+  if (lane == 0 && fk >= 0) *fail_col = min(*fail_col, fk);
+  __syncwarp();  // scratch reuse
 }
 
 // TRSM of panel tile (i, k), i > k: L_ik = A_ik L_kk^-T (one warp; lane = row; L_kk staged in
