@@ -501,11 +501,11 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     for (int s_ : P.order_b)
       if (P.sn_Lip[s_] >= 0) {
         const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_], ld_ = (w_ + 31) / 32 * 32;
-        maxw2 = std::max(maxw2, ld_ * ld_);
+        maxw2 = std::max(maxw2, ld_ * (ld_ + 1));
       }
-    if (maxw2 == 0 || maxw2 * 8 > 220 * 1024) h->use_linv = false;
+    if (maxw2 == 0 || (maxw2 + 1024) * 8 > 220 * 1024) h->use_linv = false;
     if (h->use_linv) {
-      h->linv_smem = (int)(maxw2 * 8);
+      h->linv_smem = (int)((maxw2 + 32 * 32) * 8);  // L11 (padded) + one 32 x 32 staging block
       CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->linv_smem));
       CUDA_TRY(grid_of(linv_kernel, KKT_BNT, h->linv_smem, (long long)P.order_b.size() * P.batch, 1, &h->g_linv));
     }

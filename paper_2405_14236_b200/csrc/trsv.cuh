@@ -140,7 +140,7 @@ __device__ __forceinline__ void cta_bwd_blocked(const double* __restrict__ L, in
 __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* __restrict__ Lx_all,
                                                        const double* __restrict__ Dv_all, double* Li_all) {
   // L11 staged row-major in shared memory, padded to nb*32 with the identity:
-  //   Ls[i * LD + k] = L11(i, k), LD = nb * 32.
+  //   Ls[i * (LD + 1) + k] = L11(i, k), LD = nb * 32.
   // Phase 1: warp I inverts diagonal block I (lane j: column j in registers, substitution with
   //          broadcast rows of L11).
   // Phase 2: warp J forms the blocks below it in block column J, top to bottom:
@@ -154,14 +154,23 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     const long long lip = __ldg(P.sn_Lip + s);
     if (lip < 0) continue;  // huge: solved by the whole-GPU path
     const SnInfo I = P.sn[s];
-    const int w = I.w, r = I.r, nb = (w + 31) >> 5, LD = nb * 32;
+    const int w = I.w, r = I.r, nb = (w + 31) >> 5, LD = nb * 32, LDP = LD + 1;  // odd row pitch: conflict-free column stores
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     const double* dv = Dv_all + (long long)b * P.n + I.f0;
     double* Li = Li_all + (long long)b * P.linv_doubles + lip;  // column-major w x w
     __syncthreads();
-    for (int q = tid; q < LD * LD; q += nt) {
-      const int i = q / LD, k = q % LD;
-      Ls[q] = (i < w && k < w) ? (k <= i ? __ldg(L + (long long)k * r + i) : 0.0) : (i == k ? 1.0 : 0.0);
+    for (int q0 = tid; q0 < LD * LD; q0 += nt * 8) {  // coalesced along the columns of L11, 8 loads in flight
+      double v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int q = q0 + u * nt, k = q / LD, i = q % LD;
+        v8[u] = (q < LD * LD && i < w && k < w && k <= i) ? __ldg(L + (long long)k * r + i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int q = q0 + u * nt, k = q / LD, i = q % LD;
+        if (q < LD * LD) Ls[i * LDP + k] = (i < w && k < w) ? v8[u] : (i == k ? 1.0 : 0.0);
+      }
     }
     __syncthreads();
     // phase 1: diagonal blocks
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
 #pragma unroll
       for (int i = 0; i < 32; i++) {
         const double di = (o + i < w) ? __ldg(dv + o + i) : 1.0;
-        const double* Lrow = Ls + (o + i) * LD + o;
+        const double* Lrow = Ls + (o + i) * LDP + o;
         double a = 0.0;
 #pragma unroll
         for (int k = 0; k < i; k++) a = fma(Lrow[k], x[k], a);
@@ -183,44 +192,45 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
         if (o + i < w && o + j < w) Li[(long long)(o + j) * w + o + i] = x[i];
     }
     __syncthreads();
-    // phase 2: below-diagonal blocks, block column J per warp
-    for (int Jb = warp; Jb < nb - 1; Jb += nw) {
-      const int oj = Jb * 32, j = lane;
-      const bool jin = oj + j < w;
-      for (int Ib = Jb + 1; Ib < nb; Ib++) {
-        const int oi = Ib * 32;
-        double tacc[32];
-#pragma unroll
-        for (int i = 0; i < 32; i++) tacc[i] = 0.0;
+    // phase 2: below-diagonal blocks in dependency order (block distance d = I - J), one block
+    // at a time by the whole CTA: warp q forms rows q, q+8, q+16, q+24 of T = sum_K L_IK X_KJ
+    // (lane = column), then of X_IJ = -X_II T (T staged in shared memory).
+    double* Ts = Ls + LD * LDP;  // [32][32]
+    for (int d = 1; d < nb; d++) {
+      for (int Jb = 0; Jb + d < nb; Jb++) {
+        const int Ib = Jb + d, oi = Ib * 32, oj = Jb * 32, j = lane;
+        const bool jin = oj + j < w;
+        double tq[4] = {0.0, 0.0, 0.0, 0.0};
         for (int Kb = Jb; Kb < Ib; Kb++) {
           const int ok = Kb * 32;
           double xk[32];
 #pragma unroll
           for (int k = 0; k < 32; k++) xk[k] = (jin && ok + k < w) ? Li[(long long)(oj + j) * w + ok + k] : 0.0;
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            const double* Lrow = Ls + (oi + i) * LD + ok;
-            double a = tacc[i];
+          for (int u = 0; u < 4; u++) {
+            const double* Lrow = Ls + (oi + warp + 8 * u) * LDP + ok;
+            double a = tq[u];
 #pragma unroll
             for (int k = 0; k < 32; k++) a = fma(Lrow[k], xk[k], a);
-            tacc[i] = a;
+            tq[u] = a;
           }
         }
-        // X_IJ = -X_II * T  (X_II lower triangular, read from Li: broadcast across lanes)
-        double xo[32];
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
+        for (int u = 0; u < 4; u++) Ts[(warp + 8 * u) * 32 + j] = tq[u];
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = warp + 8 * u;
+          double xii[32];  // row i of X_II: independent loads, all in flight together
+#pragma unroll
+          for (int k = 0; k < 32; k++)
+            xii[k] = (k <= i && oi + i < w && oi + k < w) ? Li[(long long)(oi + k) * w + oi + i] : 0.0;
           double a = 0.0;
 #pragma unroll
-          for (int k = 0; k <= i; k++)
-            a = fma((oi + i < w && oi + k < w) ? Li[(long long)(oi + k) * w + oi + i] : (i == k ? 1.0 : 0.0),
-                    tacc[k], a);
-          xo[i] = -a;
+          for (int k = 0; k < 32; k++) a = fma(xii[k], Ts[k * 32 + j], a);
+          if (jin && oi + i < w) Li[(long long)(oj + j) * w + oi + i] = -a;
         }
-#pragma unroll
-        for (int i = 0; i < 32; i++)
-          if (jin && oi + i < w) Li[(long long)(oj + j) * w + oi + i] = xo[i];
-        __syncwarp();
+        __syncthreads();
       }
     }
   }
