@@ -103,7 +103,10 @@ struct kkt_plan {
   bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
   bool pdl = true;                   // overlap the small/big tree phases (programmatic launch)
   int pdl_mask = 7;
-  bool use_linv = true;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
+  bool use_linv = true;
+  bool huge_solve_cta = true;        // solve the huge fronts with the CTA kernels (KKT_HUGE_SOLVE=1: whole-GPU kernel)
+  DevPlan dps{};                     // solve-side view of the plan (huge fronts as CTA supernodes)
+  void* dps_mem = nullptr;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
   int linv_smem = 0, g_linv = 1;
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
@@ -364,6 +367,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->pdl = !(getenv("KKT_NO_PDL") && atoi(getenv("KKT_NO_PDL")) > 0);
   h->pdl_mask = getenv("KKT_PDL_MASK") ? atoi(getenv("KKT_PDL_MASK")) : 7;  // 1 factor, 2 forward, 4 backward
   h->use_linv = !(getenv("KKT_NO_LINV") && atoi(getenv("KKT_NO_LINV")) > 0);
+
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   h->sms = prop.multiProcessorCount;
@@ -437,6 +441,34 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
       CUDA_TRY(cudaMemset(h->dbg_buf, 0, 4096 * 8 * sizeof(long long)));
     }
   }
+  // solve-side plan view: huge fronts are solved by the CTA kernels (their fronts are only needed
+  // in shared memory for the factorization); the big phase then starts from the big leaves
+  // (up_b) and, top-down, from the big roots
+  {
+    // huge fronts up to 512 rows are solved faster by the CTA kernels (one CTA per front, no grid
+    // barriers); beyond that the whole-GPU wavefront wins (measured: C3 max front 322 -> CTA,
+    // C4/C6 831/1239 -> whole GPU).  KKT_HUGE_SOLVE=1 forces the whole-GPU kernel, =0 the CTA one.
+    int maxr_h = 0;
+    for (int s_ : P.order_h) maxr_h = std::max(maxr_h, P.sn_rp[s_ + 1] - P.sn_rp[s_]);
+    h->huge_solve_cta = maxr_h <= 512;
+    if (const char* e = getenv("KKT_HUGE_SOLVE")) h->huge_solve_cta = atoi(e) == 0;
+  }
+  h->dps = d;
+  h->dps.solve_huge_cta = 0;
+  if (h->huge_solve_cta && !P.order_h.empty()) {
+    std::vector<int> roots;
+    for (int s_ : P.order_b) if (P.sn_parent[s_] < 0) roots.push_back(s_);
+    CUDA_TRY(cudaMalloc(&h->dps_mem, std::max<size_t>(roots.size(), 1) * sizeof(int)));
+    if (!roots.empty()) CUDA_TRY(cudaMemcpy(h->dps_mem, roots.data(), roots.size() * sizeof(int), cudaMemcpyHostToDevice));
+    h->dps.solve_huge_cta = 1;
+    h->dps.up_bf = d.up_b;
+    h->dps.n_up_bf = d.n_up_b;
+    h->dps.dn_b = (const int*)h->dps_mem;
+    h->dps.n_dn_b = (int)roots.size();
+    h->dps.ns_bn = d.ns_b;
+  } else {
+    h->huge_solve_cta = false;
+  }
   // ---- workspace ----
   size_t need;
   kkt_workspace_size(h, &need);
@@ -492,7 +524,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   CUDA_TRY(grid_of(factor_small_kernel, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
   CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
-  CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem, (long long)P.up_bf.size() * P.batch, 1, &h->g_tbig));
+  CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem,
+                   (long long)(h->huge_solve_cta ? P.up_b.size() : P.up_bf.size()) * P.batch, 1, &h->g_tbig));
   CUDA_TRY(grid_of(bwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, ts, KKT_WPB, &h->g_bsmall));
   if (const char* e = getenv("KKT_BWD_CTAS")) h->g_bsmall = std::min(h->g_bsmall, std::max(1, atoi(e)));
   CUDA_TRY(grid_of(bwd_big_kernel, KKT_BNT, h->tbig_smem, tb, 1, &h->g_bbig));
@@ -631,20 +664,22 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
 static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, double* xout,
                                long long xs, const int* done) {
   const Plan& P = h->P;
+  const DevPlan& dq = h->huge_solve_cta ? h->dps : h->dp;  // solve-side plan view
+  const bool cta_huge = h->huge_solve_cta;
   if (!P.order_s.empty()) {
     fwd_small_kernel<<<h->g_tsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
-        h->dp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done);
+        dq, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done);
     LAUNCH_CHECK();
     h->launches++;
   }
   if (!P.order_b.empty()) {
-    if (!P.up_bf.empty()) {
+    if (cta_huge ? !P.up_b.empty() : !P.up_bf.empty()) {
       CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 2) && !P.order_s.empty(), fwd_big_kernel, h->g_tbig, KKT_BNT, h->tbig_smem, h->ls,
-                          h->dp, (const double*)h->Lx, (const double*)h->Dv, rhs, rs, h->Y, h->uv, h->fcnt,
+                          dq, (const double*)h->Lx, (const double*)h->Dv, rhs, rs, h->Y, h->uv, h->fcnt,
                           h->ctl + 3 * KKT_CTL, done, h->pcap, (const double*)(h->use_linv ? h->Li : nullptr)));
       h->launches++;
     }
-    if (!P.order_h.empty()) {
+    if (!P.order_h.empty() && !cta_huge) {
       DevPlan dp = h->dp;
       const double *lx = h->Lx, *dv = h->Dv, *rh = rhs;
       double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
@@ -656,9 +691,9 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
                                            h->ls));
       h->launches++;
     }
-    if (P.order_b.size() > P.order_h.size()) {
+    if (cta_huge || P.order_b.size() > P.order_h.size()) {
       bwd_big_kernel<<<h->g_bbig, KKT_BNT, h->tbig_smem, h->ls>>>(
-          h->dp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap, h->bflag,
+          dq, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->TQ, h->ctl + 4 * KKT_CTL, done, h->pcap, h->bflag,
           h->use_linv ? h->Li : nullptr);
       LAUNCH_CHECK();
       h->launches++;
@@ -666,9 +701,9 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
   }
   if (!P.order_s.empty()) {
     // overlapped with bwd_big only when bwd_big is the kernel right before it
-    const bool after_big = P.order_b.size() > P.order_h.size() && (h->pdl_mask & 4);
+    const bool after_big = (cta_huge ? !P.order_b.empty() : P.order_b.size() > P.order_h.size()) && (h->pdl_mask & 4);
     CUDA_TRY(launch_pdl(h->pdl && after_big, bwd_small_kernel, h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls,
-                        h->dp, (const double*)h->Lx, (const double*)h->Dv, (const double*)h->Y, h->Xp, xout, xs,
+                        dq, (const double*)h->Lx, (const double*)h->Dv, (const double*)h->Y, h->Xp, xout, xs,
                         h->TQs, h->ctl + 5 * KKT_CTL, done, h->bflag, (int)(h->pdl && after_big)));
     h->launches++;
   }
@@ -1094,6 +1129,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
     if (h->plan_mem) cudaFree(h->plan_mem);
+    if (h->dps_mem) cudaFree(h->dps_mem);
     if (h->ws_owned && h->ws) cudaFree(h->ws);
     for (double* p : {h->hW, h->hJ, h->hSx, h->hSs, h->hD, h->hb, h->hx})
       if (p) cudaFree(p);

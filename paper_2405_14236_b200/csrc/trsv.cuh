@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       for (int q = tid; q < R; q += nt) us[q] = v[w + q];
       __threadfence();
       __syncthreads();
-      if (P.sn[I.par].huge) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
+      if (P.sn[I.par].huge && !P.solve_huge_cta) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
       if (tid == 0) {
         const SnInfo Ip = P.sn[I.par];
         s_last = big_child_arrive(P, cnt + I.par, Ip.c0, Ip.c1);
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
       int t = 0;
       if (lane == 0) {
         const SnInfo Ipar = P.sn[I.par];
-        if (Ipar.big && !Ipar.huge) {
+        if (Ipar.big && (!Ipar.huge || P.solve_huge_cta)) {
           int* f = bflag + (long long)b * P.ns + I.par;
           while (ld_volatile(f) <= 0) { __nanosleep(64); }
           fence_acq_rel();
