@@ -63,9 +63,17 @@ __device__ __forceinline__ void wait_children_reset(int* c, int nch) {
 // overlapped small kernel: big children add 1 << 16 and the LAST big child continues with the
 // parent after the small children (each adds 1) have all arrived; it then resets the counter.
 // Returns true if the caller continues with the parent.  Called by one thread.
-__device__ __forceinline__ bool big_child_arrive(const DevPlan& P, int* c, int par_c0, int par_c1) {
-  int nbig = 0;
-  for (int ci = par_c0; ci < par_c1; ci++) nbig += P.chinfo[ci].big ? 1 : 0;
+__device__ __forceinline__ bool big_child_arrive_n(int* c, int nbig, int nch) {
+  const int nsmall = nch - nbig;
+  const int old = atom_add_acq_rel(c, 1 << 16);
+  if ((old >> 16) != nbig - 1) return false;
+  while ((ld_volatile(c) & 0xffff) < nsmall) { __nanosleep(64); }
+  fence_acq_rel();
+  *c = 0;
+  return true;
+}
+__device__ __forceinline__ bool big_child_arrive(const DevPlan& P, int* c, int par, int par_c0, int par_c1) {
+  const int nbig = __ldg(P.sn_nbig + par);
   const int nsmall = (par_c1 - par_c0) - nbig;
   const int old = atom_add_acq_rel(c, 1 << 16);
   if ((old >> 16) != nbig - 1) return false;

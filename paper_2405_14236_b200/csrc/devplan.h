@@ -44,6 +44,7 @@ struct DevPlan {
   int n_up_s, n_up_b, n_dn_b, n_dn_s;
   const int *up_bf, *order_h;    // big non-huge bottom-up start list; huge supernodes in order
   int solve_huge_cta;            // 1: the solve kernels treat huge supernodes as CTA (big) supernodes
+  const int* sn_nbig;            // [ns] number of big (CTA-path) children
   int n_up_bf, n_h;
   const long long *sn_Lp, *sn_Up, *sn_uvp, *sn_Lip;
   long long linv_doubles;

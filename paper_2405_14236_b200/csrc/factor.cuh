@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
           red_release_add(cnt + I.par, 1);
           s_last = 0;
         } else {
-          s_last = big_child_arrive(P, cnt + I.par, Ip.c0, Ip.c1);
+          s_last = big_child_arrive(P, cnt + I.par, I.par, Ip.c0, Ip.c1);
         }
       }
       __syncthreads();

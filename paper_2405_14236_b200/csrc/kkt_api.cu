@@ -103,10 +103,11 @@ struct kkt_plan {
   bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
   bool pdl = true;                   // overlap the small/big tree phases (programmatic launch)
   int pdl_mask = 7;
-  bool use_linv = true;
+  bool use_linv = true;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
   bool huge_solve_cta = true;        // solve the huge fronts with the CTA kernels (KKT_HUGE_SOLVE=1: whole-GPU kernel)
   DevPlan dps{};                     // solve-side view of the plan (huge fronts as CTA supernodes)
-  void* dps_mem = nullptr;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
+  void* dps_mem = nullptr;
+  void* nbig_mem = nullptr;          // [ns] big-children counts
   int linv_smem = 0, g_linv = 1;
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
@@ -452,6 +453,14 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     for (int s_ : P.order_h) maxr_h = std::max(maxr_h, P.sn_rp[s_ + 1] - P.sn_rp[s_]);
     h->huge_solve_cta = maxr_h <= 512;
     if (const char* e = getenv("KKT_HUGE_SOLVE")) h->huge_solve_cta = atoi(e) == 0;
+  }
+  {  // big-children counts (bottom-up hand-off into CTA parents)
+    std::vector<int> nbig(std::max(P.ns, 1), 0);
+    for (int s_ = 0; s_ < P.ns; s_++)
+      if (P.sn_parent[s_] >= 0 && P.sn[s_].big) nbig[P.sn_parent[s_]]++;
+    CUDA_TRY(cudaMalloc(&h->nbig_mem, nbig.size() * sizeof(int)));
+    CUDA_TRY(cudaMemcpy(h->nbig_mem, nbig.data(), nbig.size() * sizeof(int), cudaMemcpyHostToDevice));
+    d.sn_nbig = (const int*)h->nbig_mem;
   }
   h->dps = d;
   h->dps.solve_huge_cta = 0;
@@ -1130,6 +1139,7 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
     cudaStreamSynchronize(h->stream);
     if (h->plan_mem) cudaFree(h->plan_mem);
     if (h->dps_mem) cudaFree(h->dps_mem);
+    if (h->nbig_mem) cudaFree(h->nbig_mem);
     if (h->ws_owned && h->ws) cudaFree(h->ws);
     for (double* p : {h->hW, h->hJ, h->hSx, h->hSs, h->hD, h->hb, h->hx})
       if (p) cudaFree(p);

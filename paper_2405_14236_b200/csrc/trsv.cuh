@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
                                                           int pcap, const double* __restrict__ Li_all) {
   extern __shared__ double sm[];
   __shared__ int s_task, s_last;
+  __shared__ int s_cR[32], s_cRel[32], s_cU[32];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int ninit = P.n_up_bf * P.batch;
   double* v = sm;                         // [max_front]
@@ -480,20 +481,61 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       wait_children_reset(cnt + s, I0.c1 - I0.c0);
     }
     __syncthreads();
+    SnInfo I = P.sn[s];
     for (;;) {
       if (tid == 0) trace_stamp(P, 1, s, b, 0);
-      const SnInfo I = P.sn[s];
-      const int r = I.r, w = I.w, R = r - w;
+      const int r = I.r, w = I.w, R = r - w, nch = I.c1 - I.c0;
       const double* L = Lb + I.Lp;
+      // all independent loads first: parent info and big-children count (for the hand-off),
+      // permutation, children's metadata (thread c: child c), then rhs and children's entries
+      SnInfo Ip;
+      int pnbig = 0;
+      if (I.par >= 0) { Ip = P.sn[I.par]; pnbig = __ldg(P.sn_nbig + I.par); }
+      const bool fast = nch <= 32;
+      if (fast && tid < nch) {
+        const int4 h4 = __ldg(reinterpret_cast<const int4*>(P.chinfo + I.c0 + tid));  // f0, w, r, rp0
+        s_cR[tid] = h4.z - h4.y;
+        s_cRel[tid] = h4.w + h4.y;
+        s_cU[tid] = __ldg(reinterpret_cast<const int*>(P.chinfo + I.c0 + tid) + 10);  // uvp
+      }
       for (int q = tid; q < r; q += nt) v[q] = (q < w) ? bb[__ldg(P.perm + I.f0 + q)] : 0.0;
       __syncthreads();
-      for (int ci = I.c0; ci < I.c1; ci++) {
-        const SnInfo C = P.chinfo[ci];
-        const int Rc = C.r - C.w;
-        const int* rel = P.sn_rel + C.rp0 + C.w;
-        const double* u = uv + C.uvp;
-        for (int q = tid; q < Rc; q += nt) v[__ldg(rel + q)] += ldcg(u + q);
+      if (fast) {
+        // children's update entries: slot k <-> (child ci, chunk base), uniform across the CTA
+        int bpos[6], bch[6];
+        double bval[6];
+        int ci = 0, base = 0, Rc = nch > 0 ? s_cR[0] : 0;
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          while (ci < nch && base >= Rc) { ci++; base = 0; Rc = (ci < nch) ? s_cR[ci] : 0; }
+          bch[k] = ci; bpos[k] = -1; bval[k] = 0.0;
+          if (ci < nch) {
+            const int q = base + tid;
+            if (q < Rc) { bpos[k] = __ldg(P.sn_rel + s_cRel[ci] + q); bval[k] = ldcg(uv + s_cU[ci] + q); }
+            base += nt;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          if (k > 0 && bch[k] != bch[k - 1]) __syncthreads();
+          if (bpos[k] >= 0) v[bpos[k]] += bval[k];
+        }
         __syncthreads();
+        while (ci < nch) {  // remainder beyond 6 chunks
+          while (ci < nch && base >= Rc) { ci++; base = 0; Rc = (ci < nch) ? s_cR[ci] : 0; __syncthreads(); }
+          if (ci >= nch) break;
+          const int q = base + tid;
+          if (q < Rc) v[__ldg(P.sn_rel + s_cRel[ci] + q)] += ldcg(uv + s_cU[ci] + q);
+          base += nt;
+        }
+        __syncthreads();
+      } else {
+        for (int c = I.c0; c < I.c1; c++) {
+          const SnInfo C = P.chinfo[c];
+          const int Rq = C.r - C.w;
+          for (int q = tid; q < Rq; q += nt) v[__ldg(P.sn_rel + C.rp0 + C.w + q)] += ldcg(uv + C.uvp + q);
+          __syncthreads();
+        }
       }
       const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
       if (lip >= 0) cta_fwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, v, sm + P.max_front, tid, nt);
@@ -505,14 +547,12 @@ __global__ void __launch_bounds__(KKT_BNT) fwd_big_kernel(DevPlan P, const doubl
       for (int q = tid; q < R; q += nt) us[q] = v[w + q];
       __threadfence();
       __syncthreads();
-      if (P.sn[I.par].huge && !P.solve_huge_cta) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
-      if (tid == 0) {
-        const SnInfo Ip = P.sn[I.par];
-        s_last = big_child_arrive(P, cnt + I.par, Ip.c0, Ip.c1);
-      }
+      if (Ip.huge && !P.solve_huge_cta) break;  // the whole-GPU phase (hsolve.cuh) takes it from here
+      if (tid == 0) s_last = big_child_arrive_n(cnt + I.par, pnbig, Ip.c1 - Ip.c0);
       __syncthreads();
       if (!s_last) break;
       s = I.par;
+      I = Ip;
     }
   }
   persistent_exit(ctl);
@@ -591,13 +631,15 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
                                                           int* bflag, const double* __restrict__ Li_all) {
   extern __shared__ double sm[];
   __shared__ int s_task;
+  __shared__ int s_cid[32], s_cbig[32];
   pdl_launch_dependents();
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int total = P.ns_bn * P.batch;
   double* xa = sm;                   // [max_front]  x over R_s (own columns then ancestors)
   double* part = sm + P.max_front;   // [8 * 32] warp partials
   if (done && done[P.batch] == 0) return;  // every instance has finished refining
-  int task = -1;
+  int task = -1, cn_task = -1;
+  SnInfo Cn;  // first child's metadata, prefetched (usually the continuation)
   for (;;) {
     if (task < 0) {
       if (tid == 0) s_task = pop_task(ctl, P.dn_b, P.n_dn_b, P.batch, Q, total);
@@ -611,15 +653,22 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
       if (tid == 0) { release_small_children(P, P.sn[s], s, b, bflag); s_task = spawn_children(P, P.sn[s], b, ctl, Q, true, total); }
       __syncthreads();
       task = s_task;
+      cn_task = -1;
       __syncthreads();
       continue;
     }
     if (tid == 0) trace_stamp(P, 2, s, b, 0);
-    const SnInfo I = P.sn[s];
-    const int r = I.r, w = I.w;
+    const SnInfo I = (task == cn_task) ? Cn : P.sn[s];
+    const int r = I.r, w = I.w, nch = I.c1 - I.c0;
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     double* Xp = Xp_all + (long long)b * P.n;
     const double* Y = Y_all + (long long)b * P.n;
+    // independent loads first: children ids / classes, big-children count, first child's info
+    const bool fast = nch <= 32;
+    if (fast && tid < nch) { s_cid[tid] = __ldg(P.sn_ch + I.c0 + tid); s_cbig[tid] = P.chinfo[I.c0 + tid].big; }
+    const int nbig = __ldg(P.sn_nbig + s);
+    cn_task = -1;
+    if (nch > 0) { Cn = P.chinfo[I.c0]; cn_task = __ldg(P.sn_ch + I.c0) * P.batch + b; }
     for (int q = tid; q < r; q += nt) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
     __syncthreads();
     const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
@@ -633,7 +682,34 @@ __global__ void __launch_bounds__(KKT_BNT) bwd_big_kernel(DevPlan P, const doubl
     if (tid == 0) trace_stamp(P, 2, s, b, 1);
     __threadfence();
     __syncthreads();
-    if (tid == 0) { release_small_children(P, I, s, b, bflag); s_task = spawn_children(P, I, b, ctl, Q, true, total); }
+    if (tid == 0) {
+      if (nch - nbig > 0) st_release(bflag + (long long)b * P.ns + s, nch - nbig);  // small children's hand-off
+      if (fast) {  // continue with the first big child, publish the others (one slot reservation)
+        int next = -1;
+        if (nbig > 1) {
+          int slot = atomicAdd(ctl + 2, nbig - 1);
+          for (int c = 0; c < nch; c++) {
+            if (!s_cbig[c]) continue;
+            const int tk = s_cid[c] * P.batch + b;
+            if (next < 0) { next = tk; continue; }
+            Q.q[slot] = tk;
+            st_release(Q.flag + slot, 1);
+            slot++;
+          }
+        } else if (nbig == 1) {
+          for (int c = 0; c < nch; c++) if (s_cbig[c]) { next = s_cid[c] * P.batch + b; break; }
+        }
+        if (next >= 0) {
+          atomicAdd(ctl + 3, 1);
+        } else {
+          __threadfence();
+          if (atomicAdd(ctl + 3, 1) == total - 1) st_release(ctl + 8, 1);
+        }
+        s_task = next;
+      } else {
+        s_task = spawn_children(P, I, b, ctl, Q, true, total);
+      }
+    }
     __syncthreads();
     task = s_task;
     __syncthreads();
