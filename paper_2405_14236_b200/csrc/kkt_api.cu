@@ -543,7 +543,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     for (int s_ : P.order_b)
       if (P.sn_Lip[s_] >= 0) {
         const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_], ld_ = (w_ + 31) / 32 * 32;
-        maxw2 = std::max(maxw2, ld_ * (ld_ + 1));
+        const long long need_ = ld_ * (ld_ + 1) + (ld_ <= 128 ? (ld_ / 32) * 1024 + ld_ * 32 : 0);
+        maxw2 = std::max(maxw2, need_);
       }
     if (maxw2 == 0 || (maxw2 + 1024) * 8 > 220 * 1024) h->use_linv = false;
     if (h->use_linv) {

@@ -158,16 +158,20 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     const double* dv = Dv_all + (long long)b * P.n + I.f0;
     double* Li = Li_all + (long long)b * P.linv_doubles + lip;  // column-major w x w
+    double* Ts = Ls + LD * LDP;                // [32][32]
+    const bool resident = LD <= 128;           // X's diagonal blocks + current block column in smem
+    double* Xd = Ts + 1024;                    // [nb][32][32] diagonal inverses (row-major blocks)
+    double* Xc = Xd + nb * 1024;               // [LD][32] current block column
     __syncthreads();
-    for (int q0 = tid; q0 < LD * LD; q0 += nt * 8) {  // coalesced along the columns of L11, 8 loads in flight
-      double v8[8];
+    for (int q0 = tid; q0 < LD * LD; q0 += nt * 16) {  // coalesced along the columns of L11, 16 loads in flight
+      double v8[16];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < 16; u++) {
         const int q = q0 + u * nt, k = q / LD, i = q % LD;
         v8[u] = (q < LD * LD && i < w && k < w && k <= i) ? __ldg(L + (long long)k * r + i) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < 16; u++) {
         const int q = q0 + u * nt, k = q / LD, i = q % LD;
         if (q < LD * LD) Ls[i * LDP + k] = (i < w && k < w) ? v8[u] : (i == k ? 1.0 : 0.0);
       }
@@ -190,12 +194,57 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
 #pragma unroll
       for (int i = 0; i < 32; i++)
         if (o + i < w && o + j < w) Li[(long long)(o + j) * w + o + i] = x[i];
+      if (resident) {
+#pragma unroll
+        for (int i = 0; i < 32; i++) Xd[Ib * 1024 + i * 32 + j] = x[i];
+      }
     }
     __syncthreads();
+    if (resident) {
+      // phase 2, shared-memory resident (LD <= 128): block column J at a time (X_IJ needs only
+      // X_KJ, J <= K < I, and X_II), the current block column kept in Xc [LD][32]
+      for (int Jb = 0; Jb + 1 < nb; Jb++) {
+        const int oj = Jb * 32, j = lane;
+        const bool jin = oj + j < w;
+        for (int q = tid; q < 1024; q += nt) Xc[(oj + (q >> 5)) * 32 + (q & 31)] = Xd[Jb * 1024 + q];
+        __syncthreads();
+        for (int Ib = Jb + 1; Ib < nb; Ib++) {
+          const int oi = Ib * 32;
+          double tq[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int Kb = Jb; Kb < Ib; Kb++) {
+            const int ok = Kb * 32;
+#pragma unroll 8
+            for (int k = 0; k < 32; k++) {
+              const double xk = Xc[(ok + k) * 32 + j];
+#pragma unroll
+              for (int u = 0; u < 4; u++) tq[u] = fma(Ls[(oi + warp + 8 * u) * LDP + ok + k], xk, tq[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) Ts[(warp + 8 * u) * 32 + j] = tq[u];
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int i = warp + 8 * u;
+            const double* xr = Xd + Ib * 1024 + i * 32;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              a0 = fma(xr[k], Ts[k * 32 + j], a0);
+              a1 = fma(xr[k + 1], Ts[(k + 1) * 32 + j], a1);
+            }
+            const double xo = -(a0 + a1);  // X_II is zero above its diagonal
+            Xc[(oi + i) * 32 + j] = xo;
+            if (jin && oi + i < w) Li[(long long)(oj + j) * w + oi + i] = xo;
+          }
+          __syncthreads();
+        }
+      }
+      continue;
+    }
     // phase 2: below-diagonal blocks in dependency order (block distance d = I - J), one block
     // at a time by the whole CTA: warp q forms rows q, q+8, q+16, q+24 of T = sum_K L_IK X_KJ
     // (lane = column), then of X_IJ = -X_II T (T staged in shared memory).
-    double* Ts = Ls + LD * LDP;  // [32][32]
     for (int d = 1; d < nb; d++) {
       for (int Jb = 0; Jb + d < nb; Jb++) {
         const int Ib = Jb + d, oi = Ib * 32, oj = Jb * 32, j = lane;
