@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
                                                              int* cnt_all, int* ctl, int* fail_all,
                                                              long long smem_cap) {
   extern __shared__ double sm[];
-  __shared__ int s_task, s_fail, s_last;
+  __shared__ int s_task, s_fail, s_last, s_pnbig;
+  __shared__ SnInfo s_I, s_Ip;  // current supernode, and its parent (prefetched at node start)
   const int tid = threadIdx.x;
   const int ninit = P.n_up_bf * P.batch;
   auto bsync = [] { __syncthreads(); };
@@ -193,14 +194,16 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
     const double* Kv = Kv_all + (long long)b * P.nnzK;
     if (tid == 0) {  // all children are small: wait for phase 1 to have counted them
       const SnInfo I0 = P.sn[s];
+      s_I = I0;
       wait_children_reset(cnt + s, I0.c1 - I0.c0);
     }
     __syncthreads();
     for (;;) {
       if (tid == 0) trace_stamp(P, 0, s, b, 0);
-      const SnInfo I = P.sn[s];
+      const SnInfo I = s_I;
       const int r = I.r, w = I.w, R = r - w;
       if (tid == 0) s_fail = -1;
+      if (tid == 32 && I.par >= 0) { s_Ip = P.sn[I.par]; s_pnbig = __ldg(P.sn_nbig + I.par); }  // off the critical warp
       __syncthreads();
       const long long pw = (long long)r * w;
       const long long usz = (I.par >= 0) ? (long long)R * (R + 1) / 2 : 0;
@@ -231,12 +234,13 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
       __threadfence();
       __syncthreads();
       if (tid == 0) {
-        const SnInfo Ip = P.sn[I.par];
+        const SnInfo Ip = s_Ip;
         if (Ip.huge) {            // the whole-GPU phase takes it from here
           red_release_add(cnt + I.par, 1);
           s_last = 0;
         } else {
-          s_last = big_child_arrive(P, cnt + I.par, I.par, Ip.c0, Ip.c1);
+          s_last = big_child_arrive_n(cnt + I.par, s_pnbig, Ip.c1 - Ip.c0);
+          if (s_last) s_I = Ip;
         }
       }
       __syncthreads();
