@@ -205,6 +205,43 @@ def test_gpu_wide_front_path_parity(hcap, monkeypatch):
         S.close()
 
 
+@pytest.mark.parametrize("hcap,solve_mode", [("1500", "1"), ("4000", "1"), ("1500", "0")])
+def test_gpu_huge_solve_modes_parity(hcap, solve_mode, monkeypatch):
+    """Huge fronts solved by the whole-GPU wavefront kernel (KKT_HUGE_SOLVE=1, the C4/C6 path) and
+    by the CTA kernels (=0, the C3 path) both match the oracle, and agree with each other to the
+    refinement's accuracy."""
+    from kkt_gpu import run_lifted, relerr
+    monkeypatch.setenv("KKT_HCAP", hcap)
+    monkeypatch.setenv("KKT_HUGE_SOLVE", solve_mode)
+    inst = make_config("C2s")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, relerr(x, R["x"])
+    S.close()
+
+
+@pytest.mark.parametrize("env", [{"KKT_NO_PDL": "1"}, {"KKT_NO_LINV": "1"}, {"KKT_PDL_MASK": "4"},
+                                 {"KKT_NO_GRAPH": "1"}])
+def test_schedule_variants_parity_and_bitwise(env, monkeypatch):
+    """Serialised phases (no programmatic launch), substitution instead of L11^-1 sweeps, partial
+    overlap and the graph-free solve all reproduce the oracle; the phase overlap alone never
+    changes a bit (fixed summation orders, no floating-point atomics)."""
+    from kkt_gpu import run_lifted, relerr
+    inst = make_config("C2")
+    R = oracle.reference_solve(inst)
+    x0, info0, S0 = run_lifted(inst, max_refine=10)
+    S0.close()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, relerr(x, R["x"])
+    if "KKT_NO_LINV" not in env:  # same operator -> same bits
+        assert np.array_equal(x, x0)
+    S.close()
+
+
 def test_lifted_acopf10000_parity():
     """C3 pattern solved as LiftedKKT: exercises big fronts beyond one CTA's shared memory."""
     from kkt_gpu import run_lifted, relerr
