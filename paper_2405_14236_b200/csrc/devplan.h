@@ -31,6 +31,7 @@ struct DevPlan {
   int max_front;
   int ns_s, ns_b, ns_bn;       // small / big / big non-huge supernode counts
   int max_r_small;             // largest front among small supernodes
+  int max_rw_small;            // largest panel (r*w) among small supernodes (solve staging)
   long long nnzL_stored, update_doubles, uvec_doubles, nprod;
   const int *perm, *iperm;
   const int *Kp, *Ki, *kw, *kdiag, *pptr, *pa, *pb, *jrow, *kpos;

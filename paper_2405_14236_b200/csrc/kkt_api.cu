@@ -509,7 +509,14 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->factor_smem_cap = std::min(maxneed, cap_bytes / 8);
   h->fbig_smem = (int)(std::max<long long>(h->factor_smem_cap, 1) * 8);
   h->fsmall_smem = KKT_WPB * KKT_SCAP * 8;
-  h->tsmall_smem = KKT_WPB * (KKT_SCAP + P.max_r_small) * 8;
+  {
+    int mrw = 1;
+    for (int s_ : P.order_s) mrw = std::max(mrw, (P.sn_rp[s_ + 1] - P.sn_rp[s_]) * (P.sn_first[s_ + 1] - P.sn_first[s_]));
+    mrw = (mrw + 1) & ~1;  // keep the per-warp slices 16-byte aligned
+    h->dp.max_rw_small = mrw;
+    h->dps.max_rw_small = mrw;
+  }
+  h->tsmall_smem = KKT_WPB * (h->dp.max_rw_small + P.max_r_small + 1) * 8;
   long long maxpanel = 0;
   for (int s : P.order_b)
     maxpanel = std::max(maxpanel, (long long)(P.sn_rp[s + 1] - P.sn_rp[s]) * (P.sn_first[s + 1] - P.sn_first[s]));

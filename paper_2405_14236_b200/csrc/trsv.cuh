@@ -455,8 +455,8 @@ __global__ void __launch_bounds__(KKT_WPB * 32) fwd_small_kernel(DevPlan P, cons
                                                                  int* ctl, const int* __restrict__ done) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
-  double* v = Pn + KKT_SCAP;
+  double* Pn = sm + (long long)wid * (P.max_rw_small + P.max_r_small);
+  double* v = Pn + P.max_rw_small;
   const int ninit = P.n_up_s * P.batch;
   pdl_launch_dependents();
   if (done && done[P.batch] == 0) return;  // every instance has finished refining
@@ -775,8 +775,8 @@ __global__ void __launch_bounds__(KKT_WPB * 32) bwd_small_kernel(DevPlan P, cons
                                                                  int* bflag, int pdl) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* Pn = sm + (long long)wid * (KKT_SCAP + P.max_r_small);
-  double* xa = Pn + KKT_SCAP;
+  double* Pn = sm + (long long)wid * (P.max_rw_small + P.max_r_small);
+  double* xa = Pn + P.max_rw_small;
   const int total = P.ns_s * P.batch;
   (void)pdl;
   if (done && done[P.batch] == 0) return;  // every instance has finished refining
