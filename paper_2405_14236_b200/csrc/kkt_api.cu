@@ -366,6 +366,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->use_graph = !(getenv("KKT_NO_GRAPH") && atoi(getenv("KKT_NO_GRAPH")) > 0);
   h->solve_while = getenv("KKT_SOLVE_WHILE") && atoi(getenv("KKT_SOLVE_WHILE")) > 0;
   h->pdl = !(getenv("KKT_NO_PDL") && atoi(getenv("KKT_NO_PDL")) > 0);
+  if (h->solve_while) h->pdl = false;  // programmatic launches are not captured into conditional bodies
   h->pdl_mask = getenv("KKT_PDL_MASK") ? atoi(getenv("KKT_PDL_MASK")) : 7;  // 1 factor, 2 forward, 4 backward
   h->use_linv = !(getenv("KKT_NO_LINV") && atoi(getenv("KKT_NO_LINV")) > 0);
 
