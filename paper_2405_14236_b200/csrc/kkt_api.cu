@@ -101,6 +101,8 @@ struct kkt_plan {
   int g_hsolve = 1;
   long long g_pro = 0, g_body = 0;   // kernels in the solve graph's prologue / per correction sweep
   bool solve_while = false;          // refinement loop as a graph WHILE node (KKT_SOLVE_WHILE=1)
+  bool solve_if = false;             // sweeps 2.. behind one graph IF node (KKT_SOLVE_IF=1; measured slower:
+                                     // a graph with a conditional node launches ~0.2 ms slower on C1/C2)
   bool pdl = true;                   // overlap the small/big tree phases (programmatic launch)
   int pdl_mask = 7;
   bool use_linv = true;              // inverse-diagonal-block sweeps for big supernodes (KKT_NO_LINV=1: off)
@@ -367,6 +369,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   h->solve_while = getenv("KKT_SOLVE_WHILE") && atoi(getenv("KKT_SOLVE_WHILE")) > 0;
   h->pdl = !(getenv("KKT_NO_PDL") && atoi(getenv("KKT_NO_PDL")) > 0);
   if (h->solve_while) h->pdl = false;  // programmatic launches are not captured into conditional bodies
+  h->solve_if = getenv("KKT_SOLVE_IF") && atoi(getenv("KKT_SOLVE_IF")) > 0;
   h->pdl_mask = getenv("KKT_PDL_MASK") ? atoi(getenv("KKT_PDL_MASK")) : 7;  // 1 factor, 2 forward, 4 backward
   h->use_linv = !(getenv("KKT_NO_LINV") && atoi(getenv("KKT_NO_LINV")) > 0);
 
@@ -797,6 +800,70 @@ static kkt_status enqueue_solve(kkt_plan* h, const double* b, double* x, int max
 static kkt_status record_solve_graph(kkt_plan* h, int max_refine, double tol_bwd, cudaGraph_t* out,
                                      long long* n_pro, long long* n_body) {
   cudaGraph_t g = nullptr;
+  if (h->solve_if && !h->solve_while && max_refine >= 2) {
+    // prologue + first correction sweep recorded directly (with programmatic overlap); the
+    // remaining sweeps 2..max_refine sit in the body of one IF node taken only when some instance
+    // is still refining after the first correction -- converged solves skip them entirely
+    CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hc;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hc, g, 0, 0);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); g_err = std::string("conditional handle: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    auto capture_into = [&](cudaGraph_t into, auto&& body) -> kkt_status {
+      h->ls = h->cap;
+      cudaError_t ce = cudaStreamBeginCaptureToGraph(h->cap, into, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (ce != cudaSuccess) { h->ls = h->stream; g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
+      kkt_status st = body();
+      cudaGraph_t got = nullptr;
+      ce = cudaStreamEndCapture(h->cap, &got);
+      h->ls = h->stream;
+      if (st != KKT_OK) return st;
+      if (ce != cudaSuccess) { g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
+      return KKT_OK;
+    };
+    h->launches = 0;
+    kkt_status st = capture_into(g, [&] {
+      TRY(enqueue_prologue(h, h->gb, h->gx));
+      TRY(enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 1));
+      TRY(enqueue_correction(h, h->gx));
+      return enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 1);
+    });
+    if (st != KKT_OK) { cudaGraphDestroy(g); return st; }
+    *n_pro = h->launches;
+    size_t nn = 0, ne = 0;
+    CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+    CUDA_TRY(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));  // v2: programmatic edges
+    std::vector<cudaGraphNode_t> nodes(nn), from(ne), to(ne);
+    std::vector<cudaGraphEdgeData> edata(ne);
+    CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+    if (ne) CUDA_TRY(cudaGraphGetEdges_v2(g, from.data(), to.data(), edata.data(), &ne));
+    std::vector<cudaGraphNode_t> leaves;
+    for (auto nd : nodes)
+      if (std::find(from.begin(), from.end(), nd) == from.end()) leaves.push_back(nd);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hc;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t ifn;
+    e = cudaGraphAddNode(&ifn, g, leaves.data(), leaves.size(), &cp);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); g_err = std::string("if node: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const bool pdl_saved = h->pdl;
+    h->pdl = false;  // programmatic launches are not captured into conditional bodies
+    h->launches = 0;
+    st = capture_into(body, [&] {
+      for (int k = 2; k <= max_refine; k++) {
+        TRY(enqueue_correction(h, h->gx));
+        TRY(enqueue_check(h, h->gb, h->gx, max_refine, tol_bwd, hc, 0));
+      }
+      return KKT_OK;
+    });
+    h->pdl = pdl_saved;
+    if (st != KKT_OK) { cudaGraphDestroy(g); return st; }
+    *n_body = h->launches;
+    *out = g;
+    return KKT_OK;
+  }
   if (!h->solve_while) {  // all sweeps recorded; idle ones exit at once on the all-done count
     h->ls = h->cap;
     CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
@@ -1130,11 +1197,12 @@ extern "C" kkt_status kkt_get_trace(kkt_handle h, long long* stamps) {
 
 extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
   if (!h || !launches) return KKT_ERR_ARG;
-  if (h->graph_solve_pending && h->solve_while) {  // a graph solve: add its executed correction sweeps
+  if (h->graph_solve_pending && h->g_body > 0) {  // a graph solve: add its executed conditional body
     int sw = 0;
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     CUDA_TRY(cudaMemcpy(&sw, h->C.sweep, sizeof(int), cudaMemcpyDeviceToHost));
-    h->launches = h->g_pro + h->g_body * std::max(0, sw - (h->g_max_refine >= 1 ? 2 : 1));
+    if (h->solve_while) h->launches = h->g_pro + h->g_body * std::max(0, sw - (h->g_max_refine >= 1 ? 2 : 1));
+    else h->launches = h->g_pro + (sw > 2 ? h->g_body : 0);  // IF body: all of sweeps 2.. or none
     h->graph_solve_pending = false;
   }
   *launches = h->launches;
