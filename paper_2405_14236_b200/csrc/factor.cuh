@@ -123,10 +123,11 @@ __device__ __forceinline__ bool warp_signal_parent(const SnInfo& I, const SnInfo
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
-__global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, const double* __restrict__ Kv_all,
+__global__ void __launch_bounds__(KKT_WPB * 32, 3) factor_small_kernel(DevPlan P, const double* __restrict__ Kv_all,
                                                                     double* Lx_all, double* U_all, double* Dv_all,
                                                                     int* cnt_all, int* ctl, int* fail_all) {
   extern __shared__ double sm[];
+  __shared__ SnInfo s_ip[KKT_WPB];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* region = sm + (long long)wid * KKT_SCAP;
   const int ninit = P.n_up_s * P.batch;
@@ -141,9 +142,12 @@ __global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, c
     double* Lx = Lx_all + (long long)b * P.nnzL_stored;
     double* Ub = U_all + (long long)b * P.update_doubles;
     const double* Kv = Kv_all + (long long)b * P.nnzK;
+    SnInfo I = P.sn[s];
     for (;;) {
       if (lane == 0) trace_stamp(P, 0, s, b, 0);
-      const SnInfo I = P.sn[s];
+      // parent metadata in flight while the front is assembled and factorised: lane k < 16 holds
+      // int k of the parent's 64-byte SnInfo (one register per lane)
+      const int ipw = (I.par >= 0 && lane < 16) ? __ldg(reinterpret_cast<const int*>(P.sn + I.par) + lane) : 0;
       const int R = I.r - I.w;
       const long long usz = I.par >= 0 ? (long long)R * (R + 1) / 2 : 0;
       double* F = region;
@@ -162,9 +166,12 @@ __global__ void __launch_bounds__(KKT_WPB * 32) factor_small_kernel(DevPlan P, c
       if (lane == 0 && fk >= 0) atomicMin(fail_all, I.f0 + fk);
       if (lane == 0) trace_stamp(P, 0, s, b, 1);
       if (I.par < 0) break;
-      const SnInfo Ip = P.sn[I.par];
+      if (lane < 16) reinterpret_cast<int*>(s_ip + wid)[lane] = ipw;
+      __syncwarp();
+      const SnInfo Ip = s_ip[wid];
       if (!warp_signal_parent(I, Ip, cnt, lane, true)) break;
       s = I.par;
+      I = Ip;
     }
   }
   warp_exit(ctl, gridDim.x * KKT_WPB);
