@@ -123,7 +123,10 @@ __device__ __forceinline__ bool warp_signal_parent(const SnInfo& I, const SnInfo
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
-__global__ void __launch_bounds__(KKT_WPB * 32, 3) factor_small_kernel(DevPlan P, const double* __restrict__ Kv_all,
+// MINB = resident CTAs per SM the register allocation must allow: 1 for latency-bound trees
+// (no spills on the critical path), 3 for throughput-bound ones (many small supernodes / batches)
+template <int MINB>
+__global__ void __launch_bounds__(KKT_WPB * 32, MINB) factor_small_kernel(DevPlan P, const double* __restrict__ Kv_all,
                                                                     double* Lx_all, double* U_all, double* Dv_all,
                                                                     int* cnt_all, int* ctl, int* fail_all) {
   extern __shared__ double sm[];
@@ -142,12 +145,10 @@ __global__ void __launch_bounds__(KKT_WPB * 32, 3) factor_small_kernel(DevPlan P
     double* Lx = Lx_all + (long long)b * P.nnzL_stored;
     double* Ub = U_all + (long long)b * P.update_doubles;
     const double* Kv = Kv_all + (long long)b * P.nnzK;
-    SnInfo I = P.sn[s];
+    bool from_smem = false;  // continuing with the parent: its metadata is already in s_ip
     for (;;) {
       if (lane == 0) trace_stamp(P, 0, s, b, 0);
-      // parent metadata in flight while the front is assembled and factorised: lane k < 16 holds
-      // int k of the parent's 64-byte SnInfo (one register per lane)
-      const int ipw = (I.par >= 0 && lane < 16) ? __ldg(reinterpret_cast<const int*>(P.sn + I.par) + lane) : 0;
+      const SnInfo I = from_smem ? s_ip[wid] : P.sn[s];
       const int R = I.r - I.w;
       const long long usz = I.par >= 0 ? (long long)R * (R + 1) / 2 : 0;
       double* F = region;
@@ -157,6 +158,9 @@ __global__ void __launch_bounds__(KKT_WPB * 32, 3) factor_small_kernel(DevPlan P
       int fk = -1;
       front_factor_warp2(F, U, I.r, I.w, lane, Dv_all + (long long)b * P.n + I.f0, &fk);
       if (lane == 0) trace_stamp(P, 0, s, b, 3);
+      // parent metadata in flight while the panel and update matrix are written out: lane k < 16
+      // holds int k of the parent's 64-byte SnInfo
+      const int ipw = (I.par >= 0 && lane < 16) ? __ldg(reinterpret_cast<const int*>(P.sn + I.par) + lane) : 0;
       double* Lg = Lx + I.Lp;
       for (int q = lane; q < I.r * I.w; q += 32) Lg[q] = F[q];
       if (usz) {
@@ -168,10 +172,9 @@ __global__ void __launch_bounds__(KKT_WPB * 32, 3) factor_small_kernel(DevPlan P
       if (I.par < 0) break;
       if (lane < 16) reinterpret_cast<int*>(s_ip + wid)[lane] = ipw;
       __syncwarp();
-      const SnInfo Ip = s_ip[wid];
-      if (!warp_signal_parent(I, Ip, cnt, lane, true)) break;
+      if (!warp_signal_parent(I, s_ip[wid], cnt, lane, true)) break;
       s = I.par;
-      I = Ip;
+      from_smem = true;
     }
   }
   warp_exit(ctl, gridDim.x * KKT_WPB);

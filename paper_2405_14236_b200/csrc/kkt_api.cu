@@ -111,6 +111,7 @@ struct kkt_plan {
   void* dps_mem = nullptr;
   void* nbig_mem = nullptr;          // [ns] big-children counts
   int linv_smem = 0, g_linv = 1;
+  int fsmall_occ = 1;                // factor_small variant (resident CTAs/SM the registers allow)
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
 };
 
@@ -526,7 +527,12 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     maxpanel = std::max(maxpanel, (long long)(P.sn_rp[s + 1] - P.sn_rp[s]) * (P.sn_first[s + 1] - P.sn_first[s]));
   h->pcap = (int)std::min<long long>(maxpanel, 20000);
   h->tbig_smem = (int)((P.max_front + 8 * 32) * 8);
-  CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fsmall_smem));
+  CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fsmall_smem));
+  CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fsmall_smem));
+  // throughput-bound small phases (>= 50k small supernode tasks: C4, C5, C6) take the
+  // occupancy-capped variant, latency-bound ones (C1, C2, C3) the spill-free one (measured)
+  h->fsmall_occ = ((long long)P.order_s.size() * P.batch >= 50000) ? 3 : 1;
+  if (const char* e = getenv("KKT_FSMALL_OCC")) h->fsmall_occ = atoi(e) == 3 ? 3 : 1;
   CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
   CUDA_TRY(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
   CUDA_TRY(cudaFuncSetAttribute(bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
@@ -541,7 +547,8 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   };
   const long long us = (long long)P.up_s.size() * P.batch, ub = (long long)P.up_b.size() * P.batch;
   const long long ts = (long long)P.order_s.size() * P.batch, tb = (long long)P.order_b.size() * P.batch;
-  CUDA_TRY(grid_of(factor_small_kernel, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
+  if (h->fsmall_occ == 3) CUDA_TRY(grid_of(factor_small_kernel<3>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
+  else CUDA_TRY(grid_of(factor_small_kernel<1>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
   CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
   CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem,
@@ -650,7 +657,11 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
   if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
   const Plan& P = h->P;
   if (!P.order_s.empty()) {
-    factor_small_kernel<<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
+    if (h->fsmall_occ == 3)
+      factor_small_kernel<3><<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
+        h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0 * KKT_CTL, h->fail);
+    else
+      factor_small_kernel<1><<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
         h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0 * KKT_CTL, h->fail);
     LAUNCH_CHECK();
     h->launches++;
