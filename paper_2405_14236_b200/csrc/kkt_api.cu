@@ -560,13 +560,14 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     long long maxw2 = 0;
     for (int s_ : P.order_b)
       if (P.sn_Lip[s_] >= 0) {
-        const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_], ld_ = (w_ + 31) / 32 * 32;
-        const long long need_ = ld_ * (ld_ + 1) + (ld_ <= 128 ? (ld_ / 32) * 1024 + ld_ * 32 : 0);
+        const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_];
+        const int nb_ = (int)std::min<long long>((w_ + 31) / 32, 64);
+        const long long need_ = linv_packed(nb_) + (linv_resident(nb_) ? nb_ * 1024 + nb_ * 32 * 32 : 0);
         maxw2 = std::max(maxw2, need_);
       }
-    if (maxw2 == 0 || (maxw2 + 1024) * 8 > 220 * 1024) h->use_linv = false;
+    if (maxw2 == 0 || maxw2 + 1024 > KKT_LINV_CAP) h->use_linv = false;
     if (h->use_linv) {
-      h->linv_smem = (int)((maxw2 + 32 * 32) * 8);  // L11 (padded) + one 32 x 32 staging block
+      h->linv_smem = (int)((maxw2 + 32 * 32) * 8);  // packed L11 (+ X blocks) + one 32 x 32 staging block
       CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->linv_smem));
       CUDA_TRY(grid_of(linv_kernel, KKT_BNT, h->linv_smem, (long long)P.order_b.size() * P.batch, 1, &h->g_linv));
     }

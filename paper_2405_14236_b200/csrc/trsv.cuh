@@ -137,10 +137,18 @@ __device__ __forceinline__ void cta_bwd_blocked(const double* __restrict__ L, in
 // (the same operator L11^-1 applied as a matrix; the refinement loop measures and corrects
 // the result against the unassembled operator exactly as before).
 // =====================================================================================
+// Shared-memory budget of linv_kernel in doubles (host and device decide residency with it).
+#define KKT_LINV_CAP 28160
+// packed block-lower-triangular staging of L11: block (I, K), K <= I, of 32 x 33 doubles
+__host__ __device__ __forceinline__ int linv_packed(int nb) { return nb * (nb + 1) / 2 * 1056; }
+__host__ __device__ __forceinline__ bool linv_resident(int nb) {
+  return linv_packed(nb) + 1024 + nb * 1024 + nb * 32 * 32 <= KKT_LINV_CAP;
+}
+
 __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* __restrict__ Lx_all,
                                                        const double* __restrict__ Dv_all, double* Li_all) {
-  // L11 staged row-major in shared memory, padded to nb*32 with the identity:
-  //   Ls[i * (LD + 1) + k] = L11(i, k), LD = nb * 32.
+  // L11 staged in shared memory as its lower 32 x 32 blocks (packed, row pitch 33), padded to
+  // nb*32 with the identity: L11(i, k) = Ls[(I(I+1)/2 + K) * 1056 + (i%32) * 33 + k%32].
   // Phase 1: warp I inverts diagonal block I (lane j: column j in registers, substitution with
   //          broadcast rows of L11).
   // Phase 2: warp J forms the blocks below it in block column J, top to bottom:
@@ -148,18 +156,21 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
   extern __shared__ double Ls[];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const long long tasks = (long long)P.ns_b * P.batch;
-  for (long long t = blockIdx.x; t < tasks; t += gridDim.x) {
+  // Tasks in reverse topological order: the roots -- the widest blocks, the longest tasks --
+  // start in the first wave instead of queueing behind the leaves (longest-first scheduling).
+  for (long long t0 = blockIdx.x; t0 < tasks; t0 += gridDim.x) {
+    const long long t = tasks - 1 - t0;
     const int b = (int)(t % P.batch);
     const int s = __ldg(P.order_b + t / P.batch);
     const long long lip = __ldg(P.sn_Lip + s);
     if (lip < 0) continue;  // huge: solved by the whole-GPU path
     const SnInfo I = P.sn[s];
-    const int w = I.w, r = I.r, nb = (w + 31) >> 5, LD = nb * 32, LDP = LD + 1;  // odd row pitch: conflict-free column stores
+    const int w = I.w, r = I.r, nb = (w + 31) >> 5, LD = nb * 32;
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     const double* dv = Dv_all + (long long)b * P.n + I.f0;
     double* Li = Li_all + (long long)b * P.linv_doubles + lip;  // column-major w x w
-    double* Ts = Ls + LD * LDP;                // [32][32]
-    const bool resident = LD <= 128;           // X's diagonal blocks + current block column in smem
+    double* Ts = Ls + linv_packed(nb);         // [32][32]
+    const bool resident = linv_resident(nb);   // X's diagonal blocks + current block column in smem
     double* Xd = Ts + 1024;                    // [nb][32][32] diagonal inverses (row-major blocks)
     double* Xc = Xd + nb * 1024;               // [LD][32] current block column
     __syncthreads();
@@ -168,12 +179,14 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
 #pragma unroll
       for (int u = 0; u < 16; u++) {
         const int q = q0 + u * nt, k = q / LD, i = q % LD;
-        v8[u] = (q < LD * LD && i < w && k < w && k <= i) ? __ldg(L + (long long)k * r + i) : 0.0;
+        v8[u] = (q < LD * LD && i < w && k < w && k <= i) ? __ldg(L + (long long)k * r + i) : 0.0;  // k <= i: lower blocks only
       }
 #pragma unroll
       for (int u = 0; u < 16; u++) {
         const int q = q0 + u * nt, k = q / LD, i = q % LD;
-        if (q < LD * LD) Ls[i * LDP + k] = (i < w && k < w) ? v8[u] : (i == k ? 1.0 : 0.0);
+        if (q < LD * LD && (k >> 5) <= (i >> 5))
+          Ls[((i >> 5) * ((i >> 5) + 1) / 2 + (k >> 5)) * 1056 + (i & 31) * 33 + (k & 31)] =
+              (i < w && k < w) ? v8[u] : (i == k ? 1.0 : 0.0);
       }
     }
     __syncthreads();
@@ -181,15 +194,19 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     for (int Ib = warp; Ib < nb; Ib += nw) {
       const int o = Ib * 32;
       const int j = lane;
+      // Right-looking (column) substitution: x[i] accumulates sum_{k<i} L(i,k) x[k] in ascending
+      // k -- the same fma sequence as the row-oriented dot product, hence bitwise the same
+      // result -- but the dependent chain is 32 finalizations, not the 496 fmas of the dots.
       double x[32];
 #pragma unroll
-      for (int i = 0; i < 32; i++) {
-        const double di = (o + i < w) ? __ldg(dv + o + i) : 1.0;
-        const double* Lrow = Ls + (o + i) * LDP + o;
-        double a = 0.0;
+      for (int i = 0; i < 32; i++) x[i] = 0.0;
 #pragma unroll
-        for (int k = 0; k < i; k++) a = fma(Lrow[k], x[k], a);
-        x[i] = (i < j) ? 0.0 : (i == j ? di : -di * a);
+      for (int k = 0; k < 32; k++) {
+        const double dk = (o + k < w) ? __ldg(dv + o + k) : 1.0;
+        x[k] = (k < j) ? 0.0 : (k == j ? dk : -dk * x[k]);
+        const double* Lcol = Ls + (Ib * (Ib + 1) / 2 + Ib) * 1056 + (k + 1) * 33 + k;
+#pragma unroll
+        for (int i = k + 1; i < 32; i++) x[i] = fma(Lcol[(i - k - 1) * 33], x[k], x[i]);
       }
 #pragma unroll
       for (int i = 0; i < 32; i++)
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     }
     __syncthreads();
     if (resident) {
-      // phase 2, shared-memory resident (LD <= 128): block column J at a time (X_IJ needs only
+      // phase 2, shared-memory resident (nb <= 5): block column J at a time (X_IJ needs only
       // X_KJ, J <= K < I, and X_II), the current block column kept in Xc [LD][32]
       for (int Jb = 0; Jb + 1 < nb; Jb++) {
         const int oj = Jb * 32, j = lane;
@@ -213,11 +230,12 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
           double tq[4] = {0.0, 0.0, 0.0, 0.0};
           for (int Kb = Jb; Kb < Ib; Kb++) {
             const int ok = Kb * 32;
+            const double* Lb = Ls + (Ib * (Ib + 1) / 2 + Kb) * 1056 + warp * 33;
 #pragma unroll 8
             for (int k = 0; k < 32; k++) {
               const double xk = Xc[(ok + k) * 32 + j];
 #pragma unroll
-              for (int u = 0; u < 4; u++) tq[u] = fma(Ls[(oi + warp + 8 * u) * LDP + ok + k], xk, tq[u]);
+              for (int u = 0; u < 4; u++) tq[u] = fma(Lb[u * 8 * 33 + k], xk, tq[u]);
             }
           }
 #pragma unroll
@@ -257,7 +275,7 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
           for (int k = 0; k < 32; k++) xk[k] = (jin && ok + k < w) ? Li[(long long)(oj + j) * w + ok + k] : 0.0;
 #pragma unroll
           for (int u = 0; u < 4; u++) {
-            const double* Lrow = Ls + (oi + warp + 8 * u) * LDP + ok;
+            const double* Lrow = Ls + (Ib * (Ib + 1) / 2 + Kb) * 1056 + (warp + 8 * u) * 33;
             double a = tq[u];
 #pragma unroll
             for (int k = 0; k < 32; k++) a = fma(Lrow[k], xk[k], a);
