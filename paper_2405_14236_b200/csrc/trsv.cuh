@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
     const double* dv = Dv_all + (long long)b * P.n + I.f0;
     double* Li = Li_all + (long long)b * P.linv_doubles + lip;  // column-major w x w
+#ifdef KKT_LINV_PROF  // tuning build (-DKKT_LINV_PROF): per-task cycles of staging / phase 1 / phase 2
+    const long long pc0 = clock64();
+#endif
     double* Ts = Ls + linv_packed(nb);         // [32][32]
     const bool resident = linv_resident(nb);   // X's diagonal blocks + current block column in smem
     double* Xd = Ts + 1024;                    // [nb][32][32] diagonal inverses (row-major blocks)
@@ -190,6 +193,9 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
       }
     }
     __syncthreads();
+#ifdef KKT_LINV_PROF
+    const long long pc1 = clock64();
+#endif
     // phase 1: diagonal blocks
     for (int Ib = warp; Ib < nb; Ib += nw) {
       const int o = Ib * 32;
@@ -217,6 +223,9 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
       }
     }
     __syncthreads();
+#ifdef KKT_LINV_PROF
+    const long long pc2 = clock64();
+#endif
     if (resident) {
       // phase 2, shared-memory resident (nb <= 5): block column J at a time (X_IJ needs only
       // X_KJ, J <= K < I, and X_II), the current block column kept in Xc [LD][32]
@@ -258,6 +267,9 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
           __syncthreads();
         }
       }
+#ifdef KKT_LINV_PROF
+      if (tid == 0) printf("linv s=%d w=%d nb=%d stage=%lld p1=%lld p2=%lld\n", s, w, nb, pc1 - pc0, pc2 - pc1, clock64() - pc2);
+#endif
       continue;
     }
     // phase 2: below-diagonal blocks in dependency order (block distance d = I - J), one block
