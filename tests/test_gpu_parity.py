@@ -324,3 +324,21 @@ def test_bearing_120_parity():
     assert info["status"] == 0, info
     assert relerr(x, R["x"]) <= 1e-8
     S.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("relax_big,zero_frac", [(160, 0.3), (192, 0.5), (256, 0.8)])
+def test_wide_supernodes_linv_parity(relax_big, zero_frac):
+    """Coarser amalgamation (perf-only options) widens C2's CTA-path supernodes: (160, 0.3) keeps
+    every L11^-1 block resident in shared memory (w <= 128), (192, 0.5) adds w = 129..181 (packed
+    resident nb = 5 and non-resident nb = 6 linv paths), (256, 0.8) has w = 256 (no linv: the
+    substitution sweeps).  Every setting must match the oracle's exact-input solution."""
+    from kkt_gpu import run_lifted, relerr
+    import paper_2405_14236_b200 as K
+    inst = make_config("C2s")
+    R = oracle.reference_solve(inst)
+    S = K.KKTSolver.from_instance(inst, relax_big=relax_big, relax_zero_frac=zero_frac).bind(0)
+    x, info, S = run_lifted(inst, max_refine=10, solver=S)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, relerr(x, R["x"])
+    S.close()
