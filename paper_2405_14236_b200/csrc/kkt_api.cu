@@ -562,7 +562,9 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
       if (P.sn_Lip[s_] >= 0) {
         const long long w_ = P.sn_first[s_ + 1] - P.sn_first[s_];
         const int nb_ = (int)std::min<long long>((w_ + 31) / 32, 64);
-        const long long need_ = linv_packed(nb_) + (linv_resident(nb_) ? nb_ * 1024 + nb_ * 32 * 32 : 0);
+        const long long need_ = std::max<long long>(
+            linv_packed(nb_) + (linv_resident(nb_) ? nb_ * 1024 + nb_ * 32 * 32 : 0),
+            linv_wave(nb_) ? linv_wave_need(nb_) - 1024 : 0);
         maxw2 = std::max(maxw2, need_);
       }
     if (maxw2 == 0 || maxw2 + 1024 > KKT_LINV_CAP) h->use_linv = false;

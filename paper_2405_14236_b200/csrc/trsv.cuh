@@ -144,6 +144,11 @@ __host__ __device__ __forceinline__ int linv_packed(int nb) { return nb * (nb + 
 __host__ __device__ __forceinline__ bool linv_resident(int nb) {
   return linv_packed(nb) + 1024 + nb * 1024 + nb * 32 * 32 <= KKT_LINV_CAP;
 }
+// wavefront variant: every X block (I, J <= I) and every partial sum T_IJ (J < I) in shared memory
+__host__ __device__ __forceinline__ int linv_wave_need(int nb) {
+  return linv_packed(nb) + 1024 + nb * (nb + 1) / 2 * 1024 + nb * (nb - 1) / 2 * 1024;
+}
+__host__ __device__ __forceinline__ bool linv_wave(int nb) { return nb >= 2 && linv_wave_need(nb) <= KKT_LINV_CAP; }
 
 __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* __restrict__ Lx_all,
                                                        const double* __restrict__ Dv_all, double* Li_all) {
@@ -176,6 +181,9 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
     const bool resident = linv_resident(nb);   // X's diagonal blocks + current block column in smem
     double* Xd = Ts + 1024;                    // [nb][32][32] diagonal inverses (row-major blocks)
     double* Xc = Xd + nb * 1024;               // [LD][32] current block column
+    const bool wave = linv_wave(nb);
+    double* Xw = Ts + 1024;                    // wave: packed X blocks (I, J <= I), row-major 32 x 32
+    double* Tw = Xw + nb * (nb + 1) / 2 * 1024;  // wave: T blocks (I, J < I) at (I(I-1)/2 + J)
     __syncthreads();
     for (int q0 = tid; q0 < LD * LD; q0 += nt * 16) {  // coalesced along the columns of L11, 16 loads in flight
       double v8[16];
@@ -217,15 +225,67 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
 #pragma unroll
       for (int i = 0; i < 32; i++)
         if (o + i < w && o + j < w) Li[(long long)(o + j) * w + o + i] = x[i];
-      if (resident) {
+      if (resident || wave) {
+        double* xd = wave ? Xw + (Ib * (Ib + 1) / 2 + Ib) * 1024 : Xd + Ib * 1024;
 #pragma unroll
-        for (int i = 0; i < 32; i++) Xd[Ib * 1024 + i * 32 + j] = x[i];
+        for (int i = 0; i < 32; i++) xd[i * 32 + j] = x[i];
       }
     }
     __syncthreads();
 #ifdef KKT_LINV_PROF
     const long long pc2 = clock64();
 #endif
+    if (wave) {
+      // phase 2, wavefront form (right-looking over block rows K): step K adds L_IK X_KJ to every
+      // T_IJ (I > K, J <= K) at once, then finalizes block row K+1: X_{K+1,J} = -X_{K+1,K+1} T.
+      // Each T_IJ accumulates the same fma sequence (K, k ascending, from 0) as the column form.
+      for (int Kb = 0; Kb + 1 < nb; Kb++) {
+        const int nJ = Kb + 1, items = (nb - 1 - Kb) * nJ * 32;
+        for (int it = warp * 4; it < items; it += nw * 4) {
+          const int blk = it >> 5, i0 = it & 31, Ib = Kb + 1 + blk / nJ, Jb = blk % nJ;
+          double* T = Tw + (Ib * (Ib - 1) / 2 + Jb) * 1024 + i0 * 32 + lane;
+          const double* Lb = Ls + (Ib * (Ib + 1) / 2 + Kb) * 1056 + i0 * 33;
+          const double* X = Xw + (Kb * (Kb + 1) / 2 + Jb) * 1024 + lane;
+          double tq[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) tq[u] = (Jb == Kb) ? 0.0 : T[u * 32];
+#pragma unroll 8
+          for (int k = 0; k < 32; k++) {
+            const double xk = X[k * 32];
+#pragma unroll
+            for (int u = 0; u < 4; u++) tq[u] = fma(Lb[u * 33 + k], xk, tq[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) T[u * 32] = tq[u];
+        }
+        __syncthreads();
+        const int Ib = Kb + 1, oi = Ib * 32;
+        for (int it = warp * 4; it < nJ * 32; it += nw * 4) {
+          const int Jb = it >> 5, i0 = it & 31, oj = Jb * 32;
+          const double* T = Tw + (Ib * (Ib - 1) / 2 + Jb) * 1024;
+          const double* Xii = Xw + (Ib * (Ib + 1) / 2 + Ib) * 1024;
+          double* Xo = Xw + (Ib * (Ib + 1) / 2 + Jb) * 1024;
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int i = i0 + u;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              a0 = fma(Xii[i * 32 + k], T[k * 32 + lane], a0);
+              a1 = fma(Xii[i * 32 + k + 1], T[(k + 1) * 32 + lane], a1);
+            }
+            const double xo = -(a0 + a1);  // X_II is zero above its diagonal
+            Xo[i * 32 + lane] = xo;
+            if (oj + lane < w && oi + i < w) Li[(long long)(oj + lane) * w + oi + i] = xo;
+          }
+        }
+        __syncthreads();
+      }
+#ifdef KKT_LINV_PROF
+      if (tid == 0) printf("linv wave s=%d w=%d nb=%d stage=%lld p1=%lld p2=%lld\n", s, w, nb, pc1 - pc0, pc2 - pc1, clock64() - pc2);
+#endif
+      continue;
+    }
     if (resident) {
       // phase 2, shared-memory resident (nb <= 5): block column J at a time (X_IJ needs only
       // X_KJ, J <= K < I, and X_II), the current block column kept in Xc [LD][32]
