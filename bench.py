@@ -1,25 +1,33 @@
 #!/usr/bin/env python
 """bench.py -- condensed-KKT condense + factor + solve, ms per IPM iteration (BASELINE.json).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
 
 One step = kkt_condense + kkt_factor + kkt_solve (LiftedKKT; refinement included) or
-kkt_condense + kkt_factor + hykkt_solve (C3) on one synthetic instance per rank whose values
-are re-drawn every step (successive IPM iterations on a fixed pattern).
-Inputs are resident in HBM; L2 is flushed (256 MiB write) before every timed step and the
-flush is outside the per-step CUDA-event window.  N > 1 (torchrun): every rank solves its own
-instance (weak scaling, no data-path collective); value = max-over-ranks time / (N * K).
---workload C5: the 512-instance batch is partitioned over the ranks (strong scaling) and x is
-gathered with NCCL at the end of every step; value = max-over-ranks time per batch iteration.
+kkt_condense + kkt_factor + hykkt_solve (C3) on synthetic values re-drawn every step
+(successive IPM iterations on a fixed pattern).  Inputs are resident in HBM; L2 is
+flushed (256 MiB write) before every timed step, outside the per-step CUDA-event window.
 
---impl reference times the CPU oracle (oracle/, plain C, __float128) on the same workload --
-there is no installable reference implementation for this paper.
+Default workload: C4 (78,484-bus ACOPF, LiftedKKT), the largest single-GPU configuration of
+BASELINE.json (configs[3]).  Multi-GPU (one process per GPU; `--gpus N` without torchrun
+re-launches itself under torch.distributed.run):
+  * C1..C4, C6: replicas only (one KKT system stays on one GPU) -- every rank
+    solves its own instance; value = per-iteration time, max over ranks ("scaling": "weak");
+  * C5: the 512-instance batch is partitioned contiguously over the ranks and x is gathered to
+    rank 0 (NCCL gather) at the end of every step; value = time per batch iteration, max over
+    ranks ("scaling": "strong").
+
+--impl reference times the CPU oracle (oracle/, plain C, __float128 accumulation) on the same
+workload, config dict, metric and unit -- there is no installable reference implementation for
+this paper.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -32,30 +40,32 @@ import numpy as np
 
 METRIC = "condensed KKT condense+factor+solve ms/IPM-iter"
 UNIT = "ms"
+C5_TOTAL = 512
+L2_NOTE = "flushed (256 MiB write) before every step, outside the event window"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-refine", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0,
+                    help="budget of timed oracle iterations for cpu_baseline (after its analysis)")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: wall budget of the timed oracle steps")
     ap.add_argument("--nvalues", type=int, default=4, help="distinct value sets cycled over steps")
     ap.add_argument("--relax", default=None, help="amalgamation 'small,big,zero_frac' (perf tuning)")
     return ap.parse_args()
 
 
-C5_TOTAL = 512
-
-
 def workload(name, rank=0, redraw=0, world=1):
     """Instance(s) of rank `rank`.  C5: the rank's contiguous block of the 512-instance batch
     (instance k draws its values from seed 5000 + k (+1000 per redraw), so every partition
-    reproduces the same instances).  Others: one instance per rank (weak scaling)."""
+    reproduces the same instances).  Others: one instance per rank (replicas)."""
     from synth.generator import make_config, redraw_values, partition
     if name == "C5":
         a, b = partition(C5_TOTAL, world, rank)
@@ -69,6 +79,28 @@ def workload(name, rank=0, redraw=0, world=1):
 def describe(name):
     from synth.generator import CONFIGS
     return CONFIGS.get(name, name)
+
+
+def config_of(args, inst, world):
+    """The config dict both arms print (identical keys and values for the same command)."""
+    batched = args.workload == "C5"
+    return {"workload": f"{args.workload}: {describe(args.workload)}", "n": int(inst.n),
+            "m": int(inst.m), "m_eq": int(inst.m_eq),
+            "batch_total": C5_TOTAL if batched else world,
+            "l2": L2_NOTE, "max_refine": args.max_refine,
+            "parallelism": (f"batch partition x{world}" if batched else f"replicas x{world}")}
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "host": socket.gethostname()}
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -92,7 +124,7 @@ class ClockSampler:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -117,84 +149,113 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle
-def oracle_step(inst):
-    """One IPM iteration of the CPU oracle: condense -> Cholesky -> refined solve (ordering and
-    symbolic analysis are once-per-pattern and excluded, as for the GPU path)."""
-    import oracle
-    K = oracle.condense(inst)
-    return K
-
-
-def oracle_time(inst, budget_s, symbolic=None):
+def oracle_analysis(inst):
+    """Once-per-pattern oracle analysis: ordering + symbolic (timed separately, not per iteration)."""
     import oracle
     t0 = time.perf_counter()
-    if symbolic is None:
-        K = oracle.condense(inst)
-        perm = oracle.md_order(inst.n, K[0], K[1])
-        _, _, Lp, Li = oracle.symbolic(inst.n, K[0], K[1], perm, want_pattern=True)
-        symbolic = (perm, Lp, Li)
-    perm, Lp, Li = symbolic
-    times = []
+    K = oracle.condense(inst)                      # pattern of K (values unused here)
+    t1 = time.perf_counter()
+    perm = oracle.md_order(inst.n, K[0], K[1])
+    t2 = time.perf_counter()
+    _, _, Lp, Li = oracle.symbolic(inst.n, K[0], K[1], perm, want_pattern=True)
+    t3 = time.perf_counter()
+    return (perm, Lp, Li), {"pattern_ms": (t1 - t0) * 1e3, "ordering_ms": (t2 - t1) * 1e3,
+                            "symbolic_ms": (t3 - t2) * 1e3}
+
+
+def oracle_iteration(inst, sym):
+    """One oracle IPM iteration: condense -> Cholesky -> refined solve (or HyKKT), per phase (ms)."""
+    import oracle
+    perm, Lp, Li = sym
+    t0 = time.perf_counter()
+    K = oracle.condense(inst)
+    t1 = time.perf_counter()
+    Lx, fail = oracle.cholesky(inst.n, K[0], K[1], K[2], perm, Lp, Li)
+    t2 = time.perf_counter()
+    if inst.m_eq:
+        oracle.hykkt(inst, Lp, Li, Lx, perm, inst.rbar1, inst.rbar2, 1e-12, 2000, 2)
+    else:
+        oracle.solve_refined(inst, Lp, Li, Lx, perm, inst.b, max_sweeps=10, stop_rel=2.2e-16)
+    t3 = time.perf_counter()
+    return {"condense": (t1 - t0) * 1e3, "factor": (t2 - t1) * 1e3, "solve": (t3 - t2) * 1e3,
+            "total": (t3 - t0) * 1e3}
+
+
+def oracle_baseline(args, inst, budget_s, threads=1):
+    """cpu_baseline: the oracle as it stands on the host cores, bounded sample.  One instance per
+    thread when threads > 1 (C5: embarrassingly parallel batch)."""
+    one = inst.instance(0) if inst.batch > 1 else inst
+    sym, ana = oracle_analysis(one)
+    per = []
     t_start = time.perf_counter()
     while True:
-        t = time.perf_counter()
-        K = oracle.condense(inst)
-        Lx, fail = oracle.cholesky(inst.n, K[0], K[1], K[2], perm, Lp, Li)
-        if inst.m_eq:
-            oracle.hykkt(inst, Lp, Li, Lx, perm, inst.rbar1, inst.rbar2, 1e-12, 2000, 2)
-        else:
-            oracle.solve_refined(inst, Lp, Li, Lx, perm, inst.b, max_sweeps=10, stop_rel=2.2e-16)
-        times.append(time.perf_counter() - t)
-        if time.perf_counter() - t_start >= budget_s or len(times) >= 1000:
+        per.append(oracle_iteration(one, sym))
+        if time.perf_counter() - t_start >= budget_s or len(per) >= 200:
             break
-    return float(np.mean(times)) * 1e3, len(times), symbolic
+    ph = {k: float(np.mean([p[k] for p in per])) for k in per[0]}
+    out = {"iters": len(per), "phases_ms": ph, "analysis_ms": ana, "iter_ms": ph["total"]}
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        insts = [inst.instance(k % inst.batch) for k in range(2 * threads)]
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:   # ctypes releases the GIL inside the C oracle
+            list(ex.map(lambda it: oracle_iteration(it, sym), insts))
+        dt = time.perf_counter() - t0
+        out["parallel"] = {"threads": threads, "instances": len(insts), "wall_s": dt,
+                           "ms_per_instance": dt * 1e3 / len(insts)}
+    return out
 
 
 def run_reference(args, rank, world):
     if rank != 0:
-        return
-    inst = workload(args.workload)
-    if inst.batch > 1:
-        inst = inst.instance(0)
-    import oracle  # noqa: F401
-    _, _, sym = oracle_time(inst, 0.0)         # analysis once (untimed)
-    for _ in range(args.warmup):
-        pass
-    t0 = time.perf_counter()
-    ms_each = []
+        return   # rank 0 alone runs the (CPU) reference arm; other ranks exit 0
+    inst0 = workload(args.workload, 0, 0, 1)
+    one = inst0.instance(0) if inst0.batch > 1 else inst0
     nb = C5_TOTAL if args.workload == "C5" else 1
+    sym, ana = oracle_analysis(one)                   # once per pattern, untimed
+    warm = min(args.warmup, 1)                        # the oracle has no caches to warm
+    for k in range(warm):
+        oracle_iteration(one, sym)
+    sets = []
+    for k in range(min(args.nvalues, args.steps)):   # same re-drawn value sets as our arm
+        it = workload(args.workload, 0, 1 + k, 1)
+        sets.append(it.instance(k % it.batch) if it.batch > 1 else it)
+    per = []
+    t0 = time.perf_counter()
     for k in range(args.steps):
-        it = workload(args.workload, 0, 1 + k % args.nvalues)
-        if it.batch > 1:
-            it = it.instance(k % it.batch)
-        ms, cnt, _ = oracle_time(it, 0.0, sym)
-        ms_each.append(ms * nb)        # C5: one batch iteration = 512 instance solves
+        per.append(oracle_iteration(sets[k % len(sets)], sym))
+        if time.perf_counter() - t0 >= args.ref_budget_s:
+            break
     total = time.perf_counter() - t0
-    v = float(np.mean(ms_each))
-    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{args.workload}: {describe(args.workload)}", "n": inst.n,
-                      "m": inst.m, "m_eq": inst.m_eq},
-           "impl": "reference",
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"{args.steps} full oracle IPM iterations (condense + "
-                                      f"Cholesky + __float128-refined solve){' x 512 (one instance timed per step, scaled)' if nb > 1 else ''}, {total:.1f} s"},
+    v = float(np.mean([p["total"] for p in per])) * nb   # C5: one batch iteration = 512 solves
+    phases = {k: float(np.mean([p[k] for p in per])) * nb for k in ("condense", "factor", "solve")}
+    sample = (f"{len(per)} of {args.steps} requested oracle IPM iterations (condense + Cholesky + "
+              f"__float128-refined solve) in {total:.1f} s (budget {args.ref_budget_s:.0f} s), "
+              f"{warm} warm-up" + ("; one instance per step, x512 for the batch" if nb > 1 else ""))
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(per),
+           "warmup": warm, "ms_per_step": v, "higher_is_better": False,
+           "scaling": "strong" if nb > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generator, synth/)",
+           "config": config_of(args, inst0, world), "impl": "reference",
+           "phases_ms": phases, "oracle_analysis_ms": ana,
+           "cpu_baseline": dict({"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                 "sample": sample}, **cpu_info()),
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 # ------------------------------------------------------------------------------ ours
-def algorithmic_work(S, inst, refine_iters):
+def algorithmic_work(info, inst, refine_iters):
     """SURVEY §8(d) algorithmic work per instance."""
     n, m, nnzW, nnzJ = inst.n, inst.m, inst.nnzW, inst.nnzJ
-    nnzK, nnzL = int(S.info["nnzK"]), int(S.info["nnzL"])
+    nnzK, nnzL = int(info["nnzK"]), int(info["nnzL"])
     condense_bytes = 8 * (nnzW + nnzJ + n + m) + 8 * nnzK
     trsv_bytes = 16 * nnzL + 24 * n
     resid_bytes = 24 * nnzW + 24 * nnzJ + 8 * (2 * n + m)
     pairs = 1 + refine_iters
     solve_bytes = pairs * trsv_bytes + (refine_iters + 1) * resid_bytes
-    return dict(condense_bytes=condense_bytes, factor_flops=float(S.info["flops"]),
+    return dict(condense_bytes=condense_bytes, factor_flops=float(info["flops"]),
+                factor_flops_large=float(info["flops_huge"]),
                 trsv_bytes=trsv_bytes, resid_bytes=resid_bytes, solve_bytes=solve_bytes,
                 trsv_pairs=pairs)
 
@@ -231,37 +292,37 @@ def run_ours(args, rank, world):
                          r2=d(it.rbar2) if hykkt else None, inst=it))
     x = torch.zeros((B, inst.n) if B > 1 else (inst.n,), dtype=torch.float64, device=dev)
     dy = torch.zeros(max(inst.m_eq, 1), dtype=torch.float64, device=dev)
-    gathered = None
+    gather_list = None
     if dist is not None and batched:
         from synth.generator import partition
         counts = [partition(C5_TOTAL, world, r)[1] - partition(C5_TOTAL, world, r)[0] for r in range(world)]
         assert len(set(counts)) == 1, "C5 multi-GPU run needs world | 512"
-        gathered = torch.empty((C5_TOTAL, inst.n), dtype=torch.float64, device=dev)
+        if rank == 0:   # x of every rank lands here: the only cross-GPU step (final gather)
+            gather_list = [torch.empty_like(x) for _ in range(world)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
     def step(v, evs=None):
         if evs: evs[0].record(stream)
         S.condense(v["W"], v["J"], v["Sx"], v["Ss"], None, inst.delta_w, inst.delta_c, inst.gamma)
-        n1 = S.launch_count()
         if evs: evs[1].record(stream)
         S.factor()
+        n1 = S.launch_count()       # condense + factor kernels (the counter restarts at condense)
         if evs: evs[2].record(stream)
         if hykkt:
             S.hykkt_solve(v["r1"], v["r2"], x, dy, 1e-12, 0, 2)
         else:
             S.solve(v["b"], x, args.max_refine, 0.0)
-        if gathered is not None:     # the only cross-GPU step: final gather of x (NCCL)
-            dist.all_gather_into_tensor(gathered, x)
+        if dist is not None and batched:
+            dist.gather(x, gather_list, dst=0)
         if evs: evs[3].record(stream)
-        return n1 + 2
+        return n1
 
-    # kernels per step: condense + factor counted at enqueue; the solve graph's refinement loop
-    # runs a data-dependent number of sweeps, so its count is read back after each warm-up step
-    # (per value set) and reused for the timed steps, which stay free of host synchronisation
+    # kernels per step: condense + factor counted at enqueue; the solve's data-dependent part is
+    # read back after each warm-up step (per value set) and reused for the timed steps, which
+    # stay free of host synchronisation
     per_set = {}
-
-    for k in range(args.warmup):
+    for k in range(max(args.warmup, len(sets))):
         pre = step(sets[k % len(sets)])
         torch.cuda.synchronize()
         per_set[k % len(sets)] = pre + S.launch_count()
@@ -271,6 +332,7 @@ def run_ours(args, rank, world):
         raise RuntimeError(f"warm-up solve failed: {info}")
     # ---------------- timed region ----------------
     evs = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    fph = []
     launches = 0
     if dist: dist.barrier()
     torch.cuda.synchronize()
@@ -279,7 +341,7 @@ def run_ours(args, rank, world):
         for k in range(args.steps):
             flush.fill_(float(k))                  # L2 flush, outside the event window
             step(sets[k % len(sets)], evs[k])
-            launches += per_set.get(k % len(sets), max(per_set.values()))
+            launches += per_set[k % len(sets)]
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
     if dist: dist.barrier()
@@ -288,13 +350,20 @@ def run_ours(args, rank, world):
                     evs[k][2].elapsed_time(evs[k][3])] for k in range(args.steps)])
     total_ms = float(ph.sum())
     info = S.sync_info()
+    # factor split by supernode class (events inside kkt_factor), measured on the last step and
+    # on separate timed factor calls with the same flush discipline
+    for k in range(min(args.steps, 10)):
+        flush.fill_(float(k))
+        S.condense(sets[k % len(sets)]["W"], sets[k % len(sets)]["J"], sets[k % len(sets)]["Sx"],
+                   sets[k % len(sets)]["Ss"], None, inst.delta_w, inst.delta_c, inst.gamma)
+        S.factor()
+        fph.append(S.factor_phase_ms())
+    fph = np.array(fph)
     if dist:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    # batch: one step = one IPM iteration of the whole 512-instance batch (strong scaling);
-    # otherwise every rank solves its own instance (weak scaling)
-    value = total_ms / args.steps if batched else total_ms / (args.steps * world)
+    value = total_ms / args.steps     # ms per IPM iteration (C5: per batch iteration)
     # ---------------- e2e through host buffers (pinned) ----------------
     v0 = sets[0]["inst"]
     pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
@@ -321,68 +390,96 @@ def run_ours(args, rank, world):
             t = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
-        e2e_ms = e2e_tot / args.steps if batched else e2e_tot / (args.steps * world)
+        e2e_ms = e2e_tot / args.steps
         h2d = 8 * B * (inst.nnzW + inst.nnzJ + inst.n + (inst.m - inst.m_eq) + inst.n)
         d2h = 8 * B * inst.n
     # ---------------- roofline ----------------
     ph_mean = ph.mean(0)
-    work = algorithmic_work(S, inst, max(info["refine_iters"], 0))
+    work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0))
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     pk = json.load(open(pk_path)) if os.path.exists(pk_path) else {}
     fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    hbm_note = "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback 6650 GB/s"
+    hbm_note = ("MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else
+                "fallback 6650 GB/s (B200_PROFILING.md)")
+    dmma_note = "FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4) measured by tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json"
     f_ach = B * work["factor_flops"] / (ph_mean[1] * 1e-3) / 1e12
-    roof_factor = {"bound": "tensor", "achieved": f_ach, "peak": fp64["dmma_tflops"], "unit": "TFLOP/s",
-                   "frac": f_ach / fp64["dmma_tflops"], "traffic": None,
-                   "kernel": "kkt_factor (factor_small_kernel + factor_big_kernel)",
-                   "work": "B x sum_j c_j^2 flops per call",
-                   "peak_note": "FP64 DMMA (mma.sync m8n8k4) measured by tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json"}
-    s_ach = B * work["solve_bytes"] / (ph_mean[2] * 1e-3) / 1e9
-    roof_solve = {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak, "unit": "GB/s",
-                  "frac": s_ach / hbm_peak, "traffic": None,
-                  "kernel": ("hykkt_solve" if hykkt else "kkt_solve") + " (fwd/bwd trsv kernels + dd residual)",
-                  "work": f"B x [{work['trsv_pairs']} trsv pairs x 16 nnz(L) + residual passes] bytes",
-                  "peak_note": hbm_note}
-    c_ach = B * work["condense_bytes"] / (ph_mean[0] * 1e-3) / 1e9
-    roof_cond = {"bound": "hbm", "achieved": c_ach, "peak": hbm_peak, "unit": "GB/s", "frac": c_ach / hbm_peak,
-                 "traffic": None, "kernel": "condense_kernel (+dweights_kernel)"}
-    roofs = {"condense": roof_cond, "factor": roof_factor, "solve": roof_solve}
-    tpath = os.path.join(ROOT, "profiles", f"r01_traffic_{args.workload}.json")
-    if os.path.exists(tpath):  # DRAM bytes per phase from one ncu capture (cold caches per launch)
+    roofs = {}
+    roofs["condense"] = {"bound": "hbm", "achieved": B * work["condense_bytes"] / (ph_mean[0] * 1e-3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s", "traffic": None,
+                         "kernel": "condense_kernel (+dweights_kernel)",
+                         "work": "B x [8 (nnzW+nnzJ+n+m) + 8 nnzK] bytes", "peak_note": hbm_note}
+    roofs["factor"] = {"bound": "tensor", "achieved": f_ach, "peak": fp64["dmma_tflops"], "unit": "TFLOP/s",
+                       "traffic": None, "kernel": "kkt_factor (all supernode classes)",
+                       "work": "B x sum_j c_j^2 flops", "peak_note": dmma_note}
+    fl_ms = fph.mean(0) if len(fph) else np.zeros(2)
+    if work["factor_flops_large"] > 0 and fl_ms[1] > 0:
+        ach = B * work["factor_flops_large"] / (fl_ms[1] * 1e-3) / 1e12
+        roofs["factor_large"] = {
+            "bound": "tensor", "achieved": ach, "peak": fp64["dmma_tflops"], "unit": "TFLOP/s",
+            "traffic": None, "kernel": "factor_huge_kernel (large supernodes)",
+            "work": f"B x {work['factor_flops_large']:.4g} flops (sum over large supernodes of "
+                    "sum_t (r - t)^2)",
+            "threshold": "front > 25600 doubles (beyond one CTA's shared memory) and ancestors; "
+                         f"{S.info['nsuper_huge']} supernodes",
+            "flop_share": work["factor_flops_large"] / max(work["factor_flops"], 1.0),
+            "time_ms": float(fl_ms[1]), "time_share": float(fl_ms[1] / max(fl_ms.sum(), 1e-9)),
+            "peak_note": dmma_note}
+    roofs["solve"] = {"bound": "hbm", "achieved": B * work["solve_bytes"] / (ph_mean[2] * 1e-3) / 1e9,
+                      "peak": hbm_peak, "unit": "GB/s", "traffic": None,
+                      "kernel": ("hykkt_solve" if hykkt else "kkt_solve") + " (fwd/bwd trsv kernels + dd residual)",
+                      "work": f"B x [{work['trsv_pairs']} trsv pairs x (16 nnz(L) + 24 n) + "
+                              f"{work['trsv_pairs']} dd residual passes] bytes",
+                      "peak_note": hbm_note}
+    for r_ in roofs.values():
+        r_["frac"] = r_["achieved"] / r_["peak"]
+    tpath = os.path.join(ROOT, "profiles", f"r02_traffic_{args.workload}.json")
+    if os.path.exists(tpath):  # DRAM bytes per phase / kernel from one ncu capture (cold caches)
         tr = json.load(open(tpath))
         for k_, r_ in roofs.items():
-            r_["traffic"] = tr["dram_bytes_per_step"].get(k_) / max(B, 1) if tr["dram_bytes_per_step"].get(k_) else None
-            r_["traffic_note"] = "ncu dram__bytes_read+write per step of this phase (" + tr["source"] + ")"
+            v_ = tr.get("dram_bytes_per_step", {}).get(k_)
+            r_["traffic"] = v_ / max(B, 1) if v_ else None
+            r_["traffic_note"] = "ncu dram__bytes_read+write per step (" + tr["source"] + ")"
     dom = ["condense", "factor", "solve"][int(np.argmax(ph_mean))]
+    if dom == "factor" and "factor_large" in roofs and roofs["factor_large"]["time_share"] > 0.5:
+        dom = "factor_large"     # the dominant KERNEL is the large-supernode DMMA kernel
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": value,
            "higher_is_better": False, "scaling": "strong" if batched else "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, synth/)",
-           "config": {"workload": f"{args.workload}: {describe(args.workload)}", "n": inst.n,
-                      "m": inst.m, "m_eq": inst.m_eq, "batch_per_gpu": B,
-                      "nnzK": int(S.info["nnzK"]), "nnzL": int(S.info["nnzL"]),
-                      "flops": S.info["flops"], "nsuper": S.info["nsuper"],
-                      "tree_height": S.info["tree_height"],
-                      "l2": "flushed (256 MiB write) before every step, outside the event window",
-                      "max_refine": args.max_refine,
-                      "parallelism": f"{'batch partition' if batched else 'instance per GPU'} x{world}"},
+           "config": config_of(args, inst, world),
+           "analysis": {"nnzK": int(S.info["nnzK"]), "nnzL": int(S.info["nnzL"]),
+                        "flops": S.info["flops"], "flops_large": S.info["flops_huge"],
+                        "nsuper": S.info["nsuper"], "tree_height": S.info["tree_height"],
+                        "max_front": S.info["max_front"], "analyze_ms": S.info["analyze_ms"],
+                        "order_ms": S.info["order_ms"], "batch_per_gpu": B},
            "phases_ms": {n_: float(v_) for n_, v_ in zip(["condense", "factor", "solve"], ph_mean)},
+           "factor_split_ms": {"small_big": float(fl_ms[0]), "large": float(fl_ms[1])},
+           "instances_per_s": (C5_TOTAL if batched else world) / (value * 1e-3),
            "refine_iters": info["refine_iters"], "cg_iters": info["cg_iters"],
-           "bwd_err": info["bwd_err"], "analyze_ms": S.info["analyze_ms"],
-           "wall_s_timed": t_wall,
+           "bwd_err": info["bwd_err"], "wall_s_timed": t_wall,
            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
            "gpu_launches": launches,
            "roofline": dict(roofs[dom], phase=dom),
            "roofline_phases": roofs,
            "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        one = inst.instance(0) if B > 1 else inst
-        ms, cnt, _ = oracle_time(one, args.cpu_sample_s)
-        out["cpu_baseline"] = {"value": ms * B, "unit": UNIT, "cores": 1, "kind": "oracle",
-                               "sample": f"{cnt} oracle IPM iterations of one {args.workload} instance "
-                                         f"(condense + Cholesky + __float128 refined solve), "
-                                         f"~{args.cpu_sample_s:.0f} s budget" + (f"; x{B} for the batch" if B > 1 else "")}
+        threads = os.cpu_count() or 1
+        ob = oracle_baseline(args, inst, args.cpu_sample_s, threads if batched else 1)
+        if batched:
+            val = ob["parallel"]["ms_per_instance"] * C5_TOTAL
+            cores = ob["parallel"]["threads"]
+            sample = (f"{ob['parallel']['instances']} C5 instances, one per thread on {cores} threads "
+                      f"({ob['parallel']['wall_s']:.1f} s), scaled to the 512-instance batch; "
+                      f"single-thread: {ob['iters']} iterations of one instance")
+        else:
+            val, cores = ob["iter_ms"], 1
+            sample = (f"{ob['iters']} oracle IPM iterations of one {args.workload} instance (condense + "
+                      f"Cholesky + __float128-refined solve), ~{args.cpu_sample_s:.0f} s budget after "
+                      f"the once-per-pattern oracle analysis")
+        out["cpu_baseline"] = dict({"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": sample, "phases_ms_1thread": ob["phases_ms"],
+                                    "analysis_ms": ob["analysis_ms"]}, **cpu_info())
     if rank == 0:
         print(json.dumps(out), flush=True)
     S.close()
@@ -390,12 +487,22 @@ def run_ours(args, rank, world):
         dist.destroy_process_group()
 
 
+def relaunch(args):
+    """`--gpus N` without a torchrun environment: run this script under torch.distributed.run."""
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(relaunch(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    if world != args.gpus and "WORLD_SIZE" not in os.environ:
-        world = 1
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

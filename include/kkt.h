@@ -69,6 +69,10 @@ typedef struct {
   double analyze_ms;     /* host time of kkt_analyze                                      */
   double order_ms;       /* of which: MD-exact-v1 ordering                                */
   long long update_doubles; /* per-instance multifrontal update-matrix storage            */
+  double flops_huge;     /* factor flops of the "large" supernodes: fronts beyond one CTA's
+                            shared memory (> 25600 doubles) and their ancestors, factorised by
+                            the whole-GPU DMMA kernel; sum_s sum_{t<w_s} (r_s - t)^2        */
+  int nsuper_huge;       /* number of those supernodes                                     */
 } kkt_analysis_info;
 
 /* Fill *opt with defaults (MD-exact-v1, LL^T, relax 4/64/0.05, batch 1). */
@@ -128,9 +132,13 @@ kkt_status kkt_factor(kkt_handle h);
  * kkt_solve -- x = K^-1 b by forward/backward supernodal triangular solves,
  * then up to max_refine Richardson sweeps whose residual b - K x is evaluated
  * with the UNASSEMBLED operator W x + (Sigma_x+dw) x + J^T(D o (J x)) in double-double
- * (R8/R9).  A sweep stops the loop when the componentwise backward error
- * omega <= tol_bwd (tol_bwd <= 0 -> 1e-15), when ||dx|| <= 2u ||x||, or when omega grows
- * twice.  [device] b[n], x[n] (batch-strided; may not alias).  Non-blocking.
+ * (R8/R9).  Per instance the loop stops (R9) when the correction just applied was negligible
+ * (||dx_k|| <= 1e-14 ||x||), when two successive corrections converge geometrically
+ * (rho = ||dx_k||/||dx_k-1|| < 1/2 and rho ||dx_k||/(1-rho) <= 1e-14 ||x||), when the
+ * componentwise backward error omega grew in two consecutive sweeps, when omega <= tol_bwd
+ * (only if tol_bwd > 0; tol_bwd <= 0 disables this test, the default, because a small omega
+ * does not bound the forward error of an ill-conditioned K), or after max_refine corrections.
+ * [device] b[n], x[n] (batch-strided; may not alias).  Non-blocking.
  */
 kkt_status kkt_solve(kkt_handle h, const double *b, double *x, int max_refine, double tol_bwd);
 
@@ -201,8 +209,19 @@ kkt_status kkt_get_supernodes(kkt_handle h, int *nsuper, int *sn_first, int *sn_
  * (row 1) and backward (row 2) solve.  Blocking.  KKT_ERR_STATE when tracing is off. */
 kkt_status kkt_get_trace(kkt_handle h, long long *stamps);
 
+/* Device time of the last kkt_factor split by supernode class (CUDA events on the handle's
+ * stream): [host] ms[0] = warp + CTA phases (small and big supernodes, incl. the L11^-1
+ * products), ms[1] = whole-GPU phase of the large supernodes (0 if there are none).
+ * Blocking (waits for the events).  KKT_ERR_STATE before the first kkt_factor. */
+kkt_status kkt_factor_phase_ms(kkt_handle h, double *ms);
+
 /* Number of kernel launches the last per-iteration call enqueued (evidence counter). */
 kkt_status kkt_launch_count(kkt_handle h, long long *launches);
+
+/* Debug export (KKT_TRACE=2 at kkt_bind): copies up to n stamps [host] out[n] of the root
+ * front's per-step globaltimer record of the whole-GPU factorization (8 per 32-column step).
+ * Returns 0 on success, -1 when the record is off, -2 on a CUDA error.  Blocking. */
+int kkt_debug_steps(kkt_handle h, long long *out, int n);
 
 /* Last error message (static storage, thread-local). */
 const char *kkt_last_error(void);

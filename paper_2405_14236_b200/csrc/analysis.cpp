@@ -599,6 +599,12 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
         if (big[s] && !huge[s] && (par < 0 || huge[par])) P.dn_b.push_back(s);
         if (huge[s]) P.order_h.push_back(s);  // postorder = topological
       }
+      P.flops_huge = 0.0;
+      P.n_huge = (int)P.order_h.size();
+      for (int s : P.order_h) {
+        const double r = P.sn_rp[s + 1] - P.sn_rp[s], w = snf[s + 1] - snf[s];
+        for (int t = 0; t < (int)w; t++) P.flops_huge += (r - t) * (r - t);
+      }
       std::sort(P.dn_b.begin(), P.dn_b.end(), by_height);
     }
     P.sn.resize(ns);

@@ -18,9 +18,10 @@ __global__ void refine_init_kernel(int batch, DevCtrl C) {
   C.dxn[b] = 0ULL; C.xn[b] = 0ULL; C.dxprev[b] = INFINITY;
 }
 
-// Stopping rules (R9): omega <= tol (only if tol > 0); ||dx|| <= 2u ||x|| after the previous
-// correction;
-// omega grew in two consecutive sweeps; last sweep (measurement only).
+// Stopping rules (R9): omega <= tol (only if tol > 0); the correction just applied was
+// negligible, ||dx_k|| <= 1e-14 ||x||; geometric convergence over the last two corrections
+// (rho = ||dx_k|| / ||dx_k-1|| < 1/2) predicts rho ||dx_k|| / (1 - rho) <= 1e-14 ||x||; omega grew
+// in two consecutive sweeps; max_refine corrections applied (the last check only measures).
 __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int max_refine) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
@@ -36,10 +37,13 @@ __global__ void refine_decide_kernel(int batch, DevCtrl C, double tol, int max_r
     C.dxn[b] = 0ULL; C.xn[b] = 0ULL;
     // the last correction was negligible, or (geometric convergence, rate rho = ||dx_k|| /
     // ||dx_k-1|| < 1/2) the next one would be: rho ||dx_k|| / (1 - rho) <= 1e-14 ||x||   (R9)
-    const double rho = dxn / C.dxprev[b];
+    // the rate test needs two corrections: after the first one dxprev is still +inf (rho = 0
+    // would stop every instance after one correction whatever its convergence state)
+    const bool have_prev = isfinite(C.dxprev[b]);
+    const double rho = have_prev ? dxn / C.dxprev[b] : 1.0;
     C.dxprev[b] = dxn;
     if (dxn <= 1e-14 * xn) stop = true;
-    if (rho < 0.5 && rho * dxn / (1.0 - rho) <= 1e-14 * xn) stop = true;
+    if (have_prev && rho < 0.5 && rho * dxn / (1.0 - rho) <= 1e-14 * xn) stop = true;
     if (om > C.omega_prev[b]) { if (++C.grow[b] >= 2) stop = true; }
     else C.grow[b] = 0;
   }
@@ -59,18 +63,21 @@ __global__ void refine_cond_kernel(int batch, DevCtrl C, cudaGraphConditionalHan
   if (use_handle) cudaGraphSetConditional(handle, C.done[batch] > 0 ? 1u : 0u);
 }
 
+// x += dx for the instances still refining; ||dx||_inf, ||x||_inf by block reductions.
+// grid (gx, batch): the instance is block-uniform.
 __global__ void refine_update_kernel(int batch, int n, double* x, const double* __restrict__ dx, DevCtrl C) {
-  if (C.done[batch] == 0) return;  // every instance has finished refining
-  long long total = (long long)batch * n;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int b = (int)(idx / n);
-    if (C.done[b]) continue;
-    double d = dx[idx], xv = x[idx] + d;
-    x[idx] = xv;
-    atomic_max_pos(C.dxn + b, fabs(d));
-    atomic_max_pos(C.xn + b, fabs(xv));
+  const int b = blockIdx.y;
+  if (C.done[batch] == 0 || C.done[b]) return;  // block-uniform exits
+  double mdx = 0.0, mx = 0.0;
+  const long long o = (long long)b * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double d = dx[o + i], xv = x[o + i] + d;
+    x[o + i] = xv;
+    mdx = (isnan(d) || isnan(mdx)) ? NAN : fmax(mdx, fabs(d));  // NaN propagates
+    mx = (isnan(xv) || isnan(mx)) ? NAN : fmax(mx, fabs(xv));
   }
+  block_max_atomic(C.dxn + b, mdx);
+  block_max_atomic(C.xn + b, mx);
 }
 
 // ---------------------------------------------------------------- G^T and G products

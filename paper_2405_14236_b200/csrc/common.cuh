@@ -128,6 +128,29 @@ __device__ __forceinline__ void atomic_max_pos(unsigned long long* a, double v) 
   atomicMax(a, b);
 }
 
+// Block-wide max of non-negative doubles (NaN propagates as the largest value), then ONE
+// atomic per block: every thread of the block must call it (block-uniform destination).  A
+// per-element atomic on one address serialises ~n atomics in the L2 (measured on C4: the
+// refinement update took 0.5 ms for n = 674k).
+__device__ __forceinline__ void block_max_atomic(unsigned long long* a, double v) {
+  __shared__ unsigned long long red_max[32];
+  unsigned long long b = isnan(v) ? 0x7ff8000000000000ULL : (unsigned long long)__double_as_longlong(v);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+    b = t > b ? t : b;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) red_max[warp] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = 0ULL;
+    for (int k = 0; k < nw; k++) m = red_max[k] > m ? red_max[k] : m;
+    if (m) atomicMax(a, m);
+  }
+}
+
 // ------------------------------------------------------------------ double-double
 struct dd { double hi, lo; };
 __device__ __forceinline__ dd two_sum(double a, double b) {

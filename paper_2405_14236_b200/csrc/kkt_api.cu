@@ -113,6 +113,9 @@ struct kkt_plan {
   int linv_smem = 0, g_linv = 1;
   int fsmall_occ = 1;                // factor_small variant (resident CTAs/SM the registers allow)
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
+  std::vector<cudaGraphExec_t> extra_exec;  // further instantiated graphs (HyKKT loop)
+  cudaEvent_t fev[3] = {nullptr, nullptr, nullptr};  // factor phase events (start, before huge, end)
+  bool fev_valid = false;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -253,6 +256,8 @@ kkt_status kkt_analyze(int n, int m, int m_eq, const int* W_rowptr, const int* W
     info->analyze_ms = P.analyze_ms;
     info->order_ms = P.order_ms;
     info->update_doubles = P.update_doubles;
+    info->flops_huge = P.flops_huge;
+    info->nsuper_huge = P.n_huge;
   }
   *handle = h;
   return KKT_OK;
@@ -357,10 +362,53 @@ static kkt_status build_huge_sched(kkt_plan* h, int G, bool tiles, HugeSched* ou
   return KKT_OK;
 }
 
+// Free every device/host resource the handle holds (bound or partially bound) and return it to
+// the unbound state; safe to call twice.
+static void release_device(kkt_plan* h) {
+  if (h->device >= 0) cudaSetDevice(h->device);
+  if (h->stream || h->bound) cudaStreamSynchronize(h->stream);
+  auto fr = [](auto*& p) { if (p) cudaFree((void*)p); p = nullptr; };
+  fr(h->plan_mem); fr(h->dps_mem); fr(h->nbig_mem);
+  if (h->ws_owned) fr(h->ws);
+  h->ws = nullptr; h->ws_owned = false;
+  fr(h->hW); fr(h->hJ); fr(h->hSx); fr(h->hSs); fr(h->hD); fr(h->hb); fr(h->hx);
+  if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
+  h->pinned_flags = nullptr;
+  fr(h->trace_buf); fr(h->dbg_buf); fr(h->huge_mem); fr(h->hsolve_mem);
+  if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
+  h->solve_exec = nullptr;
+  for (auto& ge : h->extra_exec) if (ge) cudaGraphExecDestroy(ge);
+  h->extra_exec.clear();
+  if (h->cap) cudaStreamDestroy(h->cap);
+  h->cap = nullptr;
+  for (auto& e : h->fev) { if (e) cudaEventDestroy(e); e = nullptr; }
+  h->fev_valid = false;
+  h->bound = false;
+  h->condensed = h->factored = false;
+}
+
+static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t bytes, kkt_stream_t stream);
+
 extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size_t bytes,
                                kkt_stream_t stream) {
   if (!h) return KKT_ERR_ARG;
   if (h->bound) { g_err = "already bound"; return KKT_ERR_STATE; }
+  if (d_workspace) {  // size check before any allocation
+    size_t need = 0;
+    kkt_workspace_size(h, &need);
+    if (bytes < need) { g_err = "workspace too small"; return KKT_ERR_ALLOC; }
+  }
+  kkt_status st = bind_impl(h, device, d_workspace, bytes, stream);
+  if (st != KKT_OK) {
+    const std::string msg = g_err;
+    release_device(h);  // no partial allocations survive a failed bind
+    g_err = msg;
+  }
+  return st;
+}
+
+static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t bytes,
+                            kkt_stream_t stream) {
   CUDA_TRY(cudaSetDevice(device));
   h->device = device;
   h->stream = (cudaStream_t)stream;
@@ -595,6 +643,7 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
     }
   }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
+  for (auto& e : h->fev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->bound = true;
   return KKT_OK;
@@ -623,6 +672,13 @@ static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int bl
 static int grid_for(long long total, int threads, int sms) {
   long long g = (total + threads - 1) / threads;
   return (int)std::max(1LL, std::min(g, (long long)sms * 16));
+}
+
+// (blocks per instance, batch) grid of 256-thread blocks for the per-instance reductions
+static dim3 grid_2d(long long n, int batch, int sms) {
+  long long gx = (n + 255) / 256;
+  const long long cap = std::max(1LL, (long long)sms * 8 / std::max(1, batch));
+  return dim3((unsigned)std::max(1LL, std::min(gx, cap)), (unsigned)batch);
 }
 
 extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const double* J_vals,
@@ -659,6 +715,8 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
   if (!h) return KKT_ERR_ARG;
   if (!h->condensed) { g_err = "kkt_condense first"; return KKT_ERR_STATE; }
   const Plan& P = h->P;
+  const bool ev = h->ls == h->stream;  // not while recording a graph
+  if (ev) CUDA_TRY(cudaEventRecord(h->fev[0], h->ls));
   if (!P.order_s.empty()) {
     if (h->fsmall_occ == 3)
       factor_small_kernel<3><<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
@@ -680,6 +738,7 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     LAUNCH_CHECK();
     h->launches++;
   }
+  if (ev) CUDA_TRY(cudaEventRecord(h->fev[1], h->ls));
   if (!P.order_h.empty()) {
     DevPlan dp = h->dp;
     const double* kv = h->Kv;
@@ -691,7 +750,21 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
                                          (size_t)h->huge_smem, h->ls));
     h->launches++;
   }
+  if (ev) CUDA_TRY(cudaEventRecord(h->fev[2], h->ls));
+  h->fev_valid = ev;
   h->factored = true;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_factor_phase_ms(kkt_handle h, double* ms) {
+  if (!h || !ms) return KKT_ERR_ARG;
+  if (!h->fev_valid) { g_err = "no timed kkt_factor yet"; return KKT_ERR_STATE; }
+  float a = 0.f, b = 0.f;
+  CUDA_TRY(cudaEventSynchronize(h->fev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&a, h->fev[0], h->fev[1]));
+  CUDA_TRY(cudaEventElapsedTime(&b, h->fev[1], h->fev[2]));
+  ms[0] = a;
+  ms[1] = b;
   return KKT_OK;
 }
 
@@ -755,7 +828,7 @@ static kkt_status launch_resid(kkt_plan* h, const double* x, const double* rhs, 
     LAUNCH_CHECK();
     h->launches++;
   }
-  resid_cols_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
+  resid_cols_kernel<<<grid_2d(P.n, P.batch, h->sms), 256, 0, h->ls>>>(
       h->dp, h->Wv, h->Jv, h->Sx, h->dw, x, P.n, rhs, P.n, h->T, h->A, res, omega, done);
   LAUNCH_CHECK();
   h->launches++;
@@ -781,7 +854,7 @@ static kkt_status enqueue_check(kkt_plan* h, const double* b, double* x, int max
 static kkt_status enqueue_correction(kkt_plan* h, double* x) {
   const Plan& P = h->P;
   TRY(launch_solve(h, h->res, P.n, h->dxv, P.n, h->C.done));
-  refine_update_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(
+  refine_update_kernel<<<grid_2d(P.n, P.batch, h->sms), 256, 0, h->ls>>>(
       P.batch, P.n, x, h->dxv, h->C);
   LAUNCH_CHECK();
   h->launches++;
@@ -1112,7 +1185,7 @@ extern "C" kkt_status kkt_step_host(kkt_handle h, const double* W_vals, const do
     CUDA_TRY(cudaMemcpyAsync(h->hSs, Sigma_s, B * (P.m - P.m_eq) * 8, cudaMemcpyHostToDevice, s));
   if (D && P.m) CUDA_TRY(cudaMemcpyAsync(h->hD, D, B * P.m * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(h->hb, b, B * P.n * 8, cudaMemcpyHostToDevice, s));
-  TRY(kkt_condense(h, h->hW, h->hJ, h->hSx, h->hSs, D ? h->hD : nullptr, delta_w, delta_c, gamma));
+  TRY(kkt_condense(h, h->hW, h->hJ, h->hSx, Sigma_s ? h->hSs : nullptr, D ? h->hD : nullptr, delta_w, delta_c, gamma));
   TRY(kkt_factor(h));
   TRY(kkt_solve(h, h->hb, h->hx, max_refine, tol_bwd));
   CUDA_TRY(cudaMemcpyAsync(x, h->hx, B * P.n * 8, cudaMemcpyDeviceToHost, s));
@@ -1225,23 +1298,7 @@ extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
 
 extern "C" kkt_status kkt_destroy(kkt_handle h) {
   if (!h) return KKT_ERR_ARG;
-  if (h->bound) {
-    cudaSetDevice(h->device);
-    cudaStreamSynchronize(h->stream);
-    if (h->plan_mem) cudaFree(h->plan_mem);
-    if (h->dps_mem) cudaFree(h->dps_mem);
-    if (h->nbig_mem) cudaFree(h->nbig_mem);
-    if (h->ws_owned && h->ws) cudaFree(h->ws);
-    for (double* p : {h->hW, h->hJ, h->hSx, h->hSs, h->hD, h->hb, h->hx})
-      if (p) cudaFree(p);
-    if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
-    if (h->trace_buf) cudaFree(h->trace_buf);
-    if (h->dbg_buf) cudaFree(h->dbg_buf);
-    if (h->huge_mem) cudaFree(h->huge_mem);
-    if (h->hsolve_mem) cudaFree(h->hsolve_mem);
-    if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
-    if (h->cap) cudaStreamDestroy(h->cap);
-  }
+  release_device(h);
   delete h;
   return KKT_OK;
 }

@@ -75,6 +75,8 @@ struct Plan {
   // ---- stats ----
   long long nnzL = 0, nnzL_stored = 0, nprod = 0, update_doubles = 0, uvec_doubles = 0, linv_doubles = 0;
   double flops = 0.0, analyze_ms = 0.0, order_ms = 0.0;
+  double flops_huge = 0.0;   // sum over huge supernodes of sum_t (r - t)^2, t < w (stored structure)
+  int n_huge = 0;
 };
 
 struct Options {

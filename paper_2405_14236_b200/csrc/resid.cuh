@@ -47,22 +47,22 @@ __global__ void resid_rows_kernel(DevPlan P, const double* __restrict__ Jv, cons
   }
 }
 
+// grid (gx, batch): the instance is block-uniform, so omega is reduced per block (one atomic).
 __global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, const double* __restrict__ Jv,
                                   const double* __restrict__ Sx, double dw, const double* __restrict__ x,
                                   long long xs, const double* __restrict__ rhs, long long rs,
                                   const double2* __restrict__ T, const double* __restrict__ A,
                                   double* res, unsigned long long* omega, const int* __restrict__ done) {
-  long long total = (long long)P.batch * P.n;
-  if (done && done[P.batch] == 0) return;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int b = (int)(idx / P.n), i = (int)(idx % P.n);
-    if (done && done[b]) continue;
-    const double* W = Wv + (long long)b * P.nnzW;
-    const double* J = Jv + (long long)b * P.nnzJ;
-    const double* xb = x + (long long)b * xs;
-    const double2* Tb = T + (long long)b * P.m;
-    const double* Ab = A + (long long)b * P.m;
+  const int b = blockIdx.y;
+  if (done && (done[P.batch] == 0 || done[b])) return;  // block-uniform exits
+  const double* W = Wv + (long long)b * P.nnzW;
+  const double* J = Jv + (long long)b * P.nnzJ;
+  const double* xb = x + (long long)b * xs;
+  const double2* Tb = T + (long long)b * P.m;
+  const double* Ab = A + (long long)b * P.m;
+  double ommax = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+    const long long idx = (long long)b * P.n + i;
     double xi = xb[i];
     dd s = two_sum(Sx[idx], dw);
     dd y = dd_mul_d(s, xi);
@@ -84,11 +84,10 @@ __global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, cons
     double rv = rr.hi + rr.lo;
     res[idx] = rv;
     den += fabs(bi);
-    if (omega) {
-      double om = (den > 0.0) ? fabs(rv) / den : (rv != 0.0 ? INFINITY : 0.0);
-      atomic_max_pos(omega + b, om);
-    }
+    const double om = (den > 0.0) ? fabs(rv) / den : (rv != 0.0 ? INFINITY : 0.0);
+    ommax = (isnan(om) || isnan(ommax)) ? NAN : fmax(ommax, om);
   }
+  if (omega) block_max_atomic(omega + b, ommax);
 }
 
 }  // namespace kkt

@@ -22,7 +22,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve",
            "kkt_sync_info", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
-           "kkt_last_error", "kkt_destroy"]
+           "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_last_error", "kkt_destroy"]
 
 
 class KKTError(RuntimeError):
@@ -41,7 +41,8 @@ class KKTAnalysisInfo(C.Structure):
     _fields_ = [("nnzK", C.c_longlong), ("nnzL", C.c_longlong), ("nnzL_stored", C.c_longlong),
                 ("flops", C.c_double), ("nprod", C.c_longlong), ("nsuper", C.c_int),
                 ("tree_height", C.c_int), ("max_front", C.c_int), ("analyze_ms", C.c_double),
-                ("order_ms", C.c_double), ("update_doubles", C.c_longlong)]
+                ("order_ms", C.c_double), ("update_doubles", C.c_longlong),
+                ("flops_huge", C.c_double), ("nsuper_huge", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -82,6 +83,8 @@ def lib(build_if_missing: bool = True):
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
             "kkt_get_trace": [P, P],
+            "kkt_factor_phase_ms": [P, P],
+            "kkt_debug_steps": [P, P, I],
             "kkt_destroy": [P],
         }
         for name, args in sig.items():
@@ -219,6 +222,12 @@ def kkt_launch_count(h):
     return v.value
 
 
+def kkt_factor_phase_ms(h):
+    ms = np.zeros(2)
+    _chk(lib().kkt_factor_phase_ms(h, ms.ctypes.data), "kkt_factor_phase_ms")
+    return float(ms[0]), float(ms[1])
+
+
 def kkt_destroy(h):
     _chk(lib().kkt_destroy(h), "kkt_destroy")
 
@@ -289,6 +298,9 @@ class KKTSolver:
 
     def launch_count(self):
         return kkt_launch_count(self.h)
+
+    def factor_phase_ms(self):
+        return kkt_factor_phase_ms(self.h)
 
     def close(self):
         if self.h:

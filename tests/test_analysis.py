@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_library_exports_every_header_symbol():
     hdr = open(os.path.join(ROOT, "include", "kkt.h")).read()
-    decl = set(re.findall(r"^(?:kkt_status|const char \*)\s*(\w+)\s*\(", hdr, re.M))
+    decl = set(re.findall(r"^(?:kkt_status|const char \*|int)\s*(\w+)\s*\(", hdr, re.M))
     assert decl, "no declarations parsed"
     L = K.lib()
     for name in decl:
@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     assert decl == set(K.EXPORTS)
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C5", "C3"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C5", "C3", "C4"])
 def test_ordering_etree_colcounts_bitexact(cfg):
     inst = make_config(cfg) if cfg != "C5" else make_config("C5", batch=1)
     S = K.KKTSolver.from_instance(inst)

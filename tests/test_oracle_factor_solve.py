@@ -101,6 +101,61 @@ def test_backward_error_of_exact_solution_is_tiny_and_of_perturbed_is_not():
     assert om2 > 1e-10
 
 
+@pytest.mark.parametrize("seed", [51, 52])
+def test_backward_error_equals_exact_rational_definition(seed):
+    """R7 pinned exactly: eta = ||b - K x||_inf / (||K||_inf ||x||_inf + ||b||_inf) and
+    omega = max_i |b - K x|_i / (|W||x| + |Sx+dw||x| + |J|^T |D| |J| |x| + |b|)_i, both written out
+    here in exact rationals from dense matrices (both triangles of W, D of P:417-420), compared
+    with the oracle's __float128 evaluation.  A dropped ||b||, a one-triangle ||K||, a missing
+    W or J term in either denominator or a sign error in the residual all fail this test."""
+    from fractions import Fraction as F
+    inst = tiny_random(9, 7, 2, seed=seed, Xi=1e-3, hykkt_gamma=1e2, delta_w=1e-3, delta_c=1e-2)
+    R = oracle.reference_solve(inst)
+    rng = np.random.default_rng(seed)
+    x = R["x"] * (1 + 1e-6 * rng.standard_normal(inst.n))     # residual well above rounding
+    eta, om = oracle.backward_error(inst, R["K"], inst.b, x)
+    n = inst.n
+    Kx = dense.exact_condensed(inst)                          # exact K of the exact inputs
+    xf = [F(float(v)) for v in x]
+    bf = [F(float(v)) for v in inst.b]
+    res = [bf[i] - sum(Kx[i][j] * xf[j] for j in range(n)) for i in range(n)]
+    # ||K||_inf of the K that was passed (the oracle's correctly rounded K), both triangles
+    Kp, Ki, Kv = R["K"]
+    rs = [F(0)] * n
+    for j in range(n):
+        for p in range(Kp[j], Kp[j + 1]):
+            a = abs(F(float(Kv[p])))
+            rs[Ki[p]] += a
+            if Ki[p] != j:
+                rs[j] += a
+    eta_ex = max(abs(v) for v in res) / (max(rs) * max(abs(v) for v in xf) + max(abs(v) for v in bf))
+    # componentwise denominators of the unassembled operator
+    W = [[F(0)] * n for _ in range(n)]
+    for i in range(n):
+        for p in range(inst.W_rowptr[i], inst.W_rowptr[i + 1]):
+            j = int(inst.W_colind[p]); w = F(float(inst.W_vals[p]))
+            W[i][j] += w
+            if j != i:
+                W[j][i] += w
+    den = [abs(F(float(inst.Sigma_x[i])) + F(float(inst.delta_w))) * abs(xf[i]) + abs(bf[i]) +
+           sum(abs(W[i][j]) * abs(xf[j]) for j in range(n)) for i in range(n)]
+    for r in range(inst.m):
+        if r < inst.m_eq:
+            D = F(float(inst.gamma))
+        else:
+            t = F(float(inst.Sigma_s[r - inst.m_eq])) + F(float(inst.delta_w))
+            D = t / (1 + F(float(inst.delta_c)) * t)
+        cols = [(int(inst.J_colind[p]), F(float(inst.J_vals[p])))
+                for p in range(inst.J_rowptr[r], inst.J_rowptr[r + 1])]
+        t = abs(D) * sum(abs(v) * abs(xf[c]) for c, v in cols)
+        for c, v in cols:
+            den[c] += abs(v) * t
+    om_ex = max(abs(res[i]) / den[i] for i in range(n))
+    assert eta > 0 and om > 0
+    assert abs(eta - float(eta_ex)) <= 1e-13 * float(eta_ex)
+    assert abs(om - float(om_ex)) <= 1e-13 * float(om_ex)
+
+
 def test_plain_fp64_solve_is_not_enough_in_stress_regime():
     """Appendix-A probe: in the 0 < l < n regime the unrefined FP64 solve misses x_ref
     by far more than 1e-8 -- the reason kkt_solve refines with a double-double residual."""
