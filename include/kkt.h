@@ -148,12 +148,26 @@ kkt_status kkt_solve(kkt_handle h, const double *b, double *x, int max_refine, d
  * and kkt_factor:
  *   s = rbar1 + gamma G^T rbar2;  CG on S_gamma dy = G K_gamma^-1 s - rbar2 (eq. 14,
  *   x0 = 0, stop ||r_k||_2 <= cg_rtol ||r_0||_2, R10);  dx = K_gamma^-1 (s - G^T dy);
- * then max_outer_refine sweeps of refinement on the saddle system [K G^T; G 0]
- * with a double-double residual.  [device] rbar1[n], rbar2[m_eq] in; dx[n], dy[m_eq] out.
- * Non-blocking; KKT_ERR_NOT_CONVERGED is reported through kkt_sync_info.
+ * then up to max_outer_refine correction passes of refinement on the saddle system
+ * [K G^T; G 0] with a double-double residual; per instance the outer loop stops
+ * on the device when the relative correction max(||ddx||/||dx||, ||ddy||/||dy||) just applied
+ * is <= 1e-14 or two corrections converge geometrically below it (R9 analogue).  The Krylov
+ * loop and the outer loop run on the device (one CUDA graph with WHILE nodes, recorded on the
+ * first call and re-used while the value pointers, gamma and delta_w are unchanged): no host
+ * synchronisation.  cg_rtol <= 0 -> 1e-12; cg_maxit <= 0 -> min(m_eq, 2000).
+ * [device] rbar1[n], rbar2[m_eq] in; dx[n], dy[m_eq] out.  Non-blocking;
+ * KKT_ERR_NOT_CONVERGED (maxit reached) is reported through kkt_sync_info.
  */
 kkt_status hykkt_solve(kkt_handle h, const double *rbar1, const double *rbar2, double *dx,
                        double *dy, double cg_rtol, int cg_maxit, int max_outer_refine);
+
+/* hykkt_solve with the Krylov method chosen: krylov = 0 conjugate gradients (as hykkt_solve),
+ * 1 conjugate residuals (CR: "Cr ... ensure a monotonic decrease in the residual
+ * norm"; Hestenes-Stiefel form, one S_gamma product per iteration like CG).  Same stopping rule
+ * ||r_k||_2 <= cg_rtol ||r_0||_2 (R10).  KKT_ERR_ARG for another value. */
+kkt_status hykkt_solve_krylov(kkt_handle h, const double *rbar1, const double *rbar2, double *dx,
+                              double *dy, double cg_rtol, int cg_maxit, int max_outer_refine,
+                              int krylov);
 
 /* Block the host until the handle's stream is idle; report and clear the device status.
  * Any out pointer may be NULL.  status: a kkt_status value; fail_col: original column of

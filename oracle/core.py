@@ -59,6 +59,7 @@ def _load():
             lib.oracle_backward_error.restype = C.c_double
             lib.oracle_backward_error.argtypes = [C.POINTER(OracleSystem), P, P, P, P, P, P]
             lib.oracle_cg_dense.argtypes = [C.c_int, P, P, P, C.c_double, C.c_int, P]
+            lib.oracle_cr_dense.argtypes = [C.c_int, P, P, P, C.c_double, C.c_int, P, P]
             lib.oracle_hykkt.argtypes = [C.POINTER(OracleSystem), P, P, P, P, P, P, P, P,
                                          C.c_double, C.c_int, C.c_int, P, P]
             _lib = lib
@@ -188,6 +189,19 @@ def cg_dense(A, b, rtol=1e-12, maxit=1000):
     it = C.c_int(0)
     st = lib.oracle_cg_dense(n, _p(A), _p(_f64(b)), _p(x), float(rtol), int(maxit), C.byref(it))
     return x[:n], st, it.value
+
+
+def cr_dense(A, b, rtol=1e-12, maxit=1000):
+    """Conjugate residuals (Hestenes-Stiefel) on a dense SPD matrix.
+    Returns (x, status, iters, residual-norm history [iters + 1])."""
+    lib = _load()
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    x = np.zeros(max(n, 1))
+    hist = np.zeros(maxit + 1)
+    it = C.c_int(0)
+    st = lib.oracle_cr_dense(n, _p(A), _p(_f64(b)), _p(x), float(rtol), int(maxit), C.byref(it), _p(hist))
+    return x[:n], st, it.value, hist[:it.value + 1]
 
 
 def hykkt(inst, Lp, Li, Lx, perm, rbar1, rbar2, cg_rtol=1e-12, cg_maxit=2000, max_outer=30):

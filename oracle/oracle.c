@@ -538,6 +538,48 @@ done:
   return status;
 }
 
+/* Conjugate residuals (Hestenes & Stiefel 1952; P:534-535 names CR as the alternative to CG
+ * for S_gamma): for SPD A, x0 = 0, r0 = b, p0 = r0, s0 = q0 = A r0;
+ *   alpha = (r, s) / (q, q);  x += alpha p;  r -= alpha q;  s' = A r;
+ *   beta = (r, s') / (r_old, s_old);  p = r + beta p;  q = s' + beta q.
+ * Same stop rule as oracle_cg (R10).  hist (optional, maxit + 1): ||r_k||_2 for k = 0.. */
+int oracle_cr(int n, oracle_op A, void *ctx, const double *b, double *x, double rtol, int maxit,
+              int *iters, double *hist) {
+  size_t sz = sizeof(double) * (n > 0 ? n : 1);
+  double *r = malloc(sz), *p = malloc(sz), *q = malloc(sz), *sv = malloc(sz);
+  double rr = 0;
+  for (int i = 0; i < n; i++) { x[i] = 0; r[i] = b[i]; p[i] = b[i]; rr += b[i] * b[i]; }
+  double r0 = sqrt(rr);
+  if (hist) hist[0] = r0;
+  int k = 0, status = 1;
+  if (r0 == 0.0) { status = 0; goto done; }
+  A(ctx, r, sv);
+  double rs = 0;
+  for (int i = 0; i < n; i++) { q[i] = sv[i]; rs += r[i] * sv[i]; }
+  for (k = 0; k < maxit;) {
+    double qq = 0;
+    for (int i = 0; i < n; i++) qq += q[i] * q[i];
+    double alpha = rs / qq;
+    if (!isfinite(alpha)) { status = 2; break; }
+    double rr2 = 0;
+    for (int i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; rr2 += r[i] * r[i]; }
+    k++;
+    if (hist) hist[k] = sqrt(rr2);
+    if (!isfinite(rr2)) { status = 2; break; }
+    if (sqrt(rr2) <= rtol * r0) { status = 0; break; }
+    A(ctx, r, sv);
+    double rs2 = 0;
+    for (int i = 0; i < n; i++) rs2 += r[i] * sv[i];
+    double beta = rs2 / rs;
+    rs = rs2;
+    for (int i = 0; i < n; i++) { p[i] = r[i] + beta * p[i]; q[i] = sv[i] + beta * q[i]; }
+  }
+done:
+  if (iters) *iters = k;
+  free(r); free(p); free(q); free(sv);
+  return status;
+}
+
 typedef struct { int n; const double *A; } dense_ctx;
 static void dense_op(void *c, const double *x, double *y) {
   dense_ctx *d = c;
@@ -551,6 +593,11 @@ int oracle_cg_dense(int n, const double *A, const double *b, double *x, double r
                     int *iters) {
   dense_ctx c = {n, A};
   return oracle_cg(n, dense_op, &c, b, x, rtol, maxit, iters);
+}
+int oracle_cr_dense(int n, const double *A, const double *b, double *x, double rtol, int maxit,
+                    int *iters, double *hist) {
+  dense_ctx c = {n, A};
+  return oracle_cr(n, dense_op, &c, b, x, rtol, maxit, iters, hist);
 }
 
 /* =====================================================================================

@@ -111,19 +111,24 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// Returns true in thread 0 of the last-arriving block of instance b; *sum = ordered sum.
-__device__ __forceinline__ bool finish_dot(DevCtrl C, int b, double part, double* sum) {
+// Ordered sums over the KKT_NPART blocks of instance b of NV values per block: returns true in
+// thread 0 of the last-arriving block, with sum[v] = partials summed in block order (no
+// floating-point atomics: deterministic).
+template <int NV>
+__device__ __forceinline__ bool finish_dots(DevCtrl C, int b, const double* part, double* sum) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    C.partial[b * KKT_NPART + blockIdx.x] = part;
+    for (int v = 0; v < NV; v++) C.partial[((long long)b * 2 + v) * KKT_NPART + blockIdx.x] = part[v];
     __threadfence();
     unsigned int a = atomicAdd(C.part_cnt + b, 1u);
     last = (a == KKT_NPART - 1);
     if (last) {
       __threadfence();
-      double s = 0.0;
-      for (int k = 0; k < KKT_NPART; k++) s += __ldcg(C.partial + b * KKT_NPART + k);
-      *sum = s;
+      for (int v = 0; v < NV; v++) {
+        double s = 0.0;
+        for (int k = 0; k < KKT_NPART; k++) s += __ldcg(C.partial + ((long long)b * 2 + v) * KKT_NPART + k);
+        sum[v] = s;
+      }
       C.part_cnt[b] = 0u;
     }
   }
@@ -131,53 +136,98 @@ __device__ __forceinline__ bool finish_dot(DevCtrl C, int b, double part, double
   return last && threadIdx.x == 0;
 }
 
-// mode 0 (CG start):  r = G z - rbar2 ; p = r ; dy = 0 ; rr = rr0 = r.r
-// mode 1 (CG step c): q = G z ; pq = p.q ; alpha = rr / pq
+// Krylov state of one HyKKT pass, per instance: cg_done[b] = 0 running, 1 converged, 2 maxit
+// reached, 3 skipped (outer refinement already finished); cg_done[batch] = instances running
+// (the solve kernels and the graph WHILE node test it).
+__device__ __forceinline__ void cg_mark_done(DevCtrl C, int batch, int b, int code) {
+  C.cg_done[b] = code;
+  atomicSub(C.cg_done + batch, 1);
+}
+
+// Start of a pass: instances whose outer refinement finished are skipped for the whole pass.
+__global__ void cg_init_kernel(int batch, DevCtrl C, int use_odone) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < batch; b += blockDim.x) {
+    const int skip = use_odone && C.odone[b];
+    C.cg_done[b] = skip ? 3 : 0;
+    C.cg_iters[b] = 0;
+    if (!skip) atomicAdd(&cnt, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) C.cg_done[batch] = cnt;
+}
+
+// mode 0 (start):       r = G z - rbar2 ; p = r ; dy = 0 ; rr = rr0 = r.r
+// mode 1 (CG step):     q = G z ; alpha = rr / p.q
+// mode 2 (CR start):    s = q = G z (= S r0) ; rs = r.s ; qq = s.s ; alpha = rs / qq
+// mode 3 (CR step):     s = G z (= S r) ; beta = r.s / rs ; rs = r.s
 // grid (KKT_NPART, batch)
 __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ z,
                          const double* __restrict__ sub, double* out, double* p, double* dy,
-                         DevCtrl C, int mode, int first) {
+                         DevCtrl C, int mode, int first, double* q) {
   __shared__ double red[32];
   const int b = blockIdx.y;
-  if (mode == 1 && C.cg_done[b]) return;
+  if (C.cg_done[b]) return;   // converged, or skipped for this pass (block-uniform)
   const int me = P.m_eq;
   const double* J = Jv + (long long)b * P.nnzJ;
   const double* zb = z + (long long)b * P.n;
-  double part = 0.0;
+  double part[2] = {0.0, 0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < me; r += KKT_NPART * blockDim.x) {
     double acc = 0.0;
-    for (int q = P.Jrp[r]; q < P.Jrp[r + 1]; q++) acc = fma(J[q], zb[P.Jci[q]], acc);
-    long long o = (long long)b * me + r;
+    for (int t = P.Jrp[r]; t < P.Jrp[r + 1]; t++) acc = fma(J[t], zb[P.Jci[t]], acc);
+    const long long o = (long long)b * me + r;
     if (mode == 0) {
       acc -= sub[o];
       out[o] = acc;
       p[o] = acc;
       dy[o] = 0.0;
-      part = fma(acc, acc, part);
-    } else {
+      part[0] = fma(acc, acc, part[0]);
+    } else if (mode == 1) {
       out[o] = acc;
-      part = fma(p[o], acc, part);
+      part[0] = fma(p[o], acc, part[0]);
+    } else if (mode == 2) {        // out = s, q = s ; p (= r) holds r0
+      out[o] = acc;
+      q[o] = acc;
+      part[0] = fma(p[o], acc, part[0]);
+      part[1] = fma(acc, acc, part[1]);
+    } else {                       // mode 3: out = s ; sub = r
+      out[o] = acc;
+      part[0] = fma(sub[o], acc, part[0]);
     }
   }
-  double s = block_sum(part, red), tot;
-  if (finish_dot(C, b, s, &tot)) {
+  double sv[2];
+  sv[0] = block_sum(part[0], red);
+  if (mode == 2) sv[1] = block_sum(part[1], red);
+  double tot[2];
+  const bool last = (mode == 2) ? finish_dots<2>(C, b, sv, tot) : finish_dots<1>(C, b, sv, tot);
+  if (last) {
     if (mode == 0) {
-      C.rr[b] = tot; C.rr0[b] = tot; C.cg_iters[b] = 0;
-      if (first) C.rr0_first[b] = tot;
-      C.cg_done[b] = (tot == 0.0) ? 1 : 0;
+      C.rr[b] = tot[0]; C.rr0[b] = tot[0];
+      if (first) C.rr0_first[b] = tot[0];
+      if (tot[0] == 0.0) cg_mark_done(C, P.batch, b, 1);
+    } else if (mode == 1) {
+      C.pq[b] = tot[0];
+      C.alpha[b] = C.rr[b] / tot[0];
+    } else if (mode == 2) {
+      C.rs[b] = tot[0]; C.qq[b] = tot[1];
+      C.alpha[b] = tot[0] / tot[1];
     } else {
-      C.pq[b] = tot;
-      C.alpha[b] = C.rr[b] / tot;
+      C.beta[b] = tot[0] / C.rs[b];
+      C.rs[b] = tot[0];
     }
   }
 }
 
-// dy += alpha p ; r -= alpha q ; rr_new = r.r ; convergence ||r|| <= rtol ||r0|| (R10).
+// dy += alpha p ; r -= alpha q ; rr_new = r.r ; convergence ||r|| <= rtol ||r0|| (R10);
+// maxit iterations -> stop (reported as KKT_ERR_NOT_CONVERGED by cg_finish_kernel).
 // Correction passes of the outer refinement (first == 0) stop at the absolute level
 // rtol ||r0 of the first pass|| -- the correction only has to be accurate relative to the
 // solution it corrects, not relative to its own (small) right-hand side.
 __global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const double* __restrict__ p,
-                                 const double* __restrict__ q, DevCtrl C, double rtol, int* status, int first) {
+                                 const double* __restrict__ q, DevCtrl C, double rtol, int* status, int first,
+                                 int maxit) {
   __shared__ double red[32];
   const int b = blockIdx.y;
   if (C.cg_done[b]) return;
@@ -191,40 +241,114 @@ __global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const
     part = fma(rv, rv, part);
   }
   double s = block_sum(part, red), tot;
-  if (finish_dot(C, b, s, &tot)) {
-    C.cg_iters[b] += 1;
+  if (finish_dots<1>(C, b, &s, &tot)) {
+    const int it = (C.cg_iters[b] += 1);
     if (!isfinite(tot) || !isfinite(a)) {
-      C.cg_done[b] = 1;
+      cg_mark_done(C, batch, b, 1);
       atomicCAS(status, 0, 5 /* KKT_ERR_NONFINITE */);
     } else if (sqrt(tot) <= rtol * sqrt(first ? C.rr0[b] : fmax(C.rr0[b], C.rr0_first[b]))) {
-      C.cg_done[b] = 1;
+      cg_mark_done(C, batch, b, 1);
+    } else if (it >= maxit) {
+      cg_mark_done(C, batch, b, 2);
     }
-    C.beta[b] = tot / C.rr[b];
+    C.beta[b] = tot / C.rr[b];   // CG's beta (CR overwrites it in g mode 3)
     C.rr[b] = tot;
   }
 }
 
+// CG: p = r + beta p
 __global__ void cg_p_kernel(int batch, int me, double* p, const double* __restrict__ r, DevCtrl C) {
-  long long total = (long long)batch * me;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int b = (int)(idx / me);
-    if (C.cg_done[b]) continue;
-    p[idx] = fma(C.beta[b], p[idx], r[idx]);
+  const int b = blockIdx.y;
+  if (C.cg_done[b]) return;
+  const double be = C.beta[b];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < me; i += gridDim.x * blockDim.x) {
+    const long long o = (long long)b * me + i;
+    p[o] = fma(be, p[o], r[o]);
   }
 }
 
-__global__ void axpy_kernel(long long total, double* y, const double* __restrict__ x) {
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x)
-    y[idx] += x[idx];
+// CR: p = r + beta p ; q = s + beta q ; qq = q.q ; alpha = rs / qq.  grid (KKT_NPART, batch)
+__global__ void cr_pq_kernel(int batch, int me, double* p, double* q, const double* __restrict__ r,
+                             const double* __restrict__ sv, DevCtrl C) {
+  __shared__ double red[32];
+  const int b = blockIdx.y;
+  if (C.cg_done[b]) return;
+  const double be = C.beta[b];
+  double part = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < me; i += KKT_NPART * blockDim.x) {
+    const long long o = (long long)b * me + i;
+    p[o] = fma(be, p[o], r[o]);
+    const double qv = fma(be, q[o], sv[o]);
+    q[o] = qv;
+    part = fma(qv, qv, part);
+  }
+  double s = block_sum(part, red), tot;
+  if (finish_dots<1>(C, b, &s, &tot)) {
+    C.qq[b] = tot;
+    C.alpha[b] = C.rs[b] / tot;
+  }
+}
+
+// WHILE-node condition of the Krylov loop: another iteration iff some instance is running.
+// count_run: called at the end of the body (counts body executions), not before the node.
+__global__ void cg_cond_kernel(int batch, DevCtrl C, cudaGraphConditionalHandle handle, int count_run) {
+  if (count_run) *C.cg_runs += 1;
+  cudaGraphSetConditional(handle, C.cg_done[batch] > 0 ? 1u : 0u);
 }
 
 __global__ void cg_finish_kernel(int batch, DevCtrl C, int first, int* status) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
+  if (C.cg_done[b] == 3) return;   // skipped pass
   if (first) C.cg_iters_first[b] = C.cg_iters[b];
-  if (!C.cg_done[b]) atomicCAS(status, 0, 4 /* KKT_ERR_NOT_CONVERGED */);
+  if (C.cg_done[b] == 2) atomicCAS(status, 0, 4 /* KKT_ERR_NOT_CONVERGED */);
+}
+
+// ---------------------------------------------------------------- HyKKT outer refinement
+__global__ void outer_init_kernel(int batch, DevCtrl C) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) { C.odone[batch] = batch; *C.cg_runs = 0; }
+  if (b >= batch) return;
+  C.odone[b] = 0; C.opass[b] = 0; C.oprev[b] = INFINITY;
+  for (int k = 0; k < 4; k++) C.onrm[4 * b + k] = 0ULL;
+}
+
+// v += dv for instances still refining, with ||dv||_inf -> onrm[4b + k], ||v||_inf -> onrm[4b + k + 1].
+// grid (gx, batch)
+__global__ void outer_update_kernel(int batch, long long len, double* v, const double* __restrict__ dv,
+                                    DevCtrl C, int k) {
+  const int b = blockIdx.y;
+  if (C.odone[b]) return;
+  double mdv = 0.0, mv = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
+    const long long o = (long long)b * len + i;
+    const double d = dv[o], nv = v[o] + d;
+    v[o] = nv;
+    mdv = (isnan(d) || isnan(mdv)) ? NAN : fmax(mdv, fabs(d));
+    mv = (isnan(nv) || isnan(mv)) ? NAN : fmax(mv, fabs(nv));
+  }
+  block_max_atomic(C.onrm + 4 * b + k, mdv);
+  block_max_atomic(C.onrm + 4 * b + k + 1, mv);
+}
+
+// Stop rule of the saddle-system refinement (R9 analogue on (dx, dy)): the relative correction
+// c_k = max(||ddx||/||dx||, ||ddy||/||dy||) just applied is <= 1e-14, or two corrections converge
+// geometrically (rho = c_k / c_k-1 < 1/2) with rho c_k / (1 - rho) <= 1e-14.
+__global__ void outer_decide_kernel(int batch, DevCtrl C) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch || C.odone[b]) return;
+  const double ddx = bits2d(C.onrm[4 * b]), xn = bits2d(C.onrm[4 * b + 1]);
+  const double ddy = bits2d(C.onrm[4 * b + 2]), yn = bits2d(C.onrm[4 * b + 3]);
+  for (int k = 0; k < 4; k++) C.onrm[4 * b + k] = 0ULL;
+  const double c = fmax(xn > 0 ? ddx / xn : ddx, yn > 0 ? ddy / yn : ddy);
+  C.opass[b] += 1;
+  bool stop = !(c > 1e-14);   // also stops on NaN (reported by the Krylov status)
+  if (isfinite(C.oprev[b])) {
+    const double rho = c / C.oprev[b];
+    if (rho < 0.5 && rho * c / (1.0 - rho) <= 1e-14) stop = true;
+  }
+  C.oprev[b] = c;
+  if (stop) { C.odone[b] = 1; atomicSub(C.odone + batch, 1); }
 }
 
 // ---------------------------------------------------------------- NEXT-1 recovery

@@ -81,8 +81,16 @@ struct DevCtrl {
   double* pq;                // p.q
   double* alpha;
   double* beta;
-  double* partial;           // [batch][NPART] reduction partials
+  double* partial;           // [batch][2][NPART] reduction partials
   unsigned int* part_cnt;    // [batch] arrival counters for last-block reductions
+  double* rs;                // CR: r.S r
+  double* qq;                // CR: q.q
+  // HyKKT outer refinement on the saddle system (device-side stop, R9 analogue)
+  int* odone;                // [batch+1] instance finished ([batch] = instances still refining)
+  unsigned long long* onrm;  // [batch][4] bits of ||ddx||, ||dx||, ||ddy||, ||dy|| (inf norms)
+  double* oprev;             // [batch] previous relative correction
+  int* opass;                // [batch] correction passes applied
+  int* cg_runs;              // executions of the Krylov WHILE body in the last HyKKT solve
 };
 
 }  // namespace kkt

@@ -73,6 +73,14 @@ struct kkt_plan {
   double2* T = nullptr;
   double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
+  double *cs = nullptr;                                    // CR: s = S r
+  double *g_r1 = nullptr, *g_r2 = nullptr, *g_dx = nullptr, *g_dy = nullptr;  // HyKKT graph I/O
+  cudaGraphExec_t hy_exec = nullptr;                       // recorded HyKKT solve
+  double hy_rtol = -1, hy_gamma = 0, hy_dw = 0;
+  int hy_maxit = -1, hy_outer = -1, hy_krylov = -1;
+  long long hy_fixed = 0, hy_body = 0;   // launches outside / per execution of the Krylov body
+  bool hy_pending = false;               // last call was a HyKKT graph (launch count unread)
+  const void *hy_W = nullptr, *hy_J = nullptr, *hy_Sx = nullptr;
   TaskQueue TQ{}, TQs{};  // work queues of bwd_big / bwd_small (separate: the two may overlap)
   double* Li = nullptr;   // [batch][linv_doubles] L11^-1 of the big (CTA) supernodes (solve operator)
   int *bflag = nullptr;  // [batch][ns] backward hand-off big parent -> small children (PDL overlap)
@@ -191,8 +199,20 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.pq = c.take<double>(B);
   h->C.alpha = c.take<double>(B);
   h->C.beta = c.take<double>(B);
-  h->C.partial = c.take<double>(B * KKT_NPART);
+  h->C.partial = c.take<double>(B * 2 * KKT_NPART);
   h->C.part_cnt = c.take<unsigned int>(B);
+  h->C.rs = c.take<double>(B);
+  h->C.qq = c.take<double>(B);
+  h->C.odone = c.take<int>(B + 1);
+  h->C.onrm = c.take<unsigned long long>(4 * B);
+  h->C.oprev = c.take<double>(B);
+  h->C.opass = c.take<int>(B);
+  h->C.cg_runs = c.take<int>(1);
+  h->cs = c.take<double>(B * me);
+  h->g_r1 = c.take<double>(B * n);
+  h->g_dx = c.take<double>(B * n);
+  h->g_r2 = c.take<double>(B * me);
+  h->g_dy = c.take<double>(B * me);
 }
 
 // ------------------------------------------------------------------------------ C-ABI
@@ -377,6 +397,8 @@ static void release_device(kkt_plan* h) {
   fr(h->trace_buf); fr(h->dbg_buf); fr(h->huge_mem); fr(h->hsolve_mem);
   if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
   h->solve_exec = nullptr;
+  if (h->hy_exec) cudaGraphExecDestroy(h->hy_exec);
+  h->hy_exec = nullptr;
   for (auto& ge : h->extra_exec) if (ge) cudaGraphExecDestroy(ge);
   h->extra_exec.clear();
   if (h->cap) cudaStreamDestroy(h->cap);
@@ -548,8 +570,6 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   CUDA_TRY(cudaMemsetAsync(h->ws, 0, need, h->stream));
   int big = INT_MAX;
   CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  static const int one = 1;
-  CUDA_TRY(cudaMemcpyAsync(h->C.cg_done + P.batch, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   // ---- launch configuration ----
   long long maxneed = 0;
   for (int s : P.order_b) {
@@ -695,6 +715,7 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
   h->dw = delta_w; h->dc = delta_c; h->gamma = gamma;
   h->launches = 0;
   h->graph_solve_pending = false;
+  h->hy_pending = false;
   if (P.m > 0) {
     dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
@@ -1032,6 +1053,7 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   max_refine = std::max(0, max_refine);
   h->launches = 0;
   h->graph_solve_pending = false;
+  h->hy_pending = false;
   if (!h->use_graph) return enqueue_solve(h, b, x, max_refine, tol_bwd);
   // one CUDA graph per (max_refine, tol, value pointers, delta_w), recorded on a private stream
   const bool stale = !h->solve_exec || h->g_max_refine != max_refine || h->g_tol != tol_bwd ||
@@ -1055,82 +1077,235 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   return KKT_OK;
 }
 
-// one HyKKT pass for right-hand side (r1, r2) -> (dxo, dyo)
-static kkt_status hykkt_pass(kkt_plan* h, const double* r1, const double* r2, double* dxo,
-                             double* dyo, double rtol, int maxit, bool first) {
-  const Plan& P = h->P;
-  const int gs = grid_for((long long)P.batch * P.n, 256, h->sms);
-  // s = rbar1 + gamma G^T rbar2
-  gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, nullptr);
-  LAUNCH_CHECK();
-  h->launches++;
-  // z = K_gamma^-1 s ; r = G z - rbar2 ; p = r ; dy = 0
-  TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, nullptr));
-  dim3 gg(KKT_NPART, P.batch);
-  g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0, first ? 1 : 0);
-  LAUNCH_CHECK();
-  h->launches++;
-  const int chunk = 8;
-  int it = 0;
-  while (it < maxit) {
-    int todo = std::min(chunk, maxit - it);
-    for (int q = 0; q < todo; q++) {
-      gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
-      LAUNCH_CHECK();
-      TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1, 0);
-      LAUNCH_CHECK();
-      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
-                                                   rtol, h->status, first ? 1 : 0);
-      LAUNCH_CHECK();
-      cg_p_kernel<<<grid_for((long long)P.batch * P.m_eq, 256, h->sms), 256, 0, h->ls>>>(
-          P.batch, P.m_eq, h->cp, h->cr, h->C);
-      LAUNCH_CHECK();
-      h->launches += 4;
-    }
-    it += todo;
-    // host check of the per-instance convergence flags between chunks
-    CUDA_TRY(cudaMemcpyAsync(h->pinned_flags, h->C.cg_done, P.batch * sizeof(int),
-                             cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
-    bool all = true;
-    for (int b = 0; b < P.batch; b++) all = all && h->pinned_flags[b];
-    if (all) break;
-  }
-  cg_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C, first ? 1 : 0, h->status);
-  LAUNCH_CHECK();
-  // dx = K_gamma^-1 (s - G^T dy)
-  gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, dyo, -1.0, h->sg, h->wv, nullptr);
-  LAUNCH_CHECK();
-  TRY(launch_solve(h, h->wv, P.n, dxo, P.n, nullptr));
-  h->launches += 2;
+static kkt_status graph_leaves(cudaGraph_t g, std::vector<cudaGraphNode_t>& leaves);
+
+// Record `body` on the capture stream into graph `into` after everything already in it (the
+// captured nodes depend on the graph's current leaves); kernels go to h->ls = h->cap.
+template <class F>
+static kkt_status capture_into_graph(kkt_plan* h, cudaGraph_t into, F&& body) {
+  std::vector<cudaGraphNode_t> deps;
+  TRY(graph_leaves(into, deps));
+  h->ls = h->cap;
+  cudaError_t ce = cudaStreamBeginCaptureToGraph(h->cap, into, deps.empty() ? nullptr : deps.data(), nullptr,
+                                                 deps.size(), cudaStreamCaptureModeThreadLocal);
+  if (ce != cudaSuccess) { h->ls = h->stream; g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
+  kkt_status st = body();
+  cudaGraph_t got = nullptr;
+  ce = cudaStreamEndCapture(h->cap, &got);
+  h->ls = h->stream;
+  if (st != KKT_OK) return st;
+  if (ce != cudaSuccess) { g_err = std::string("capture: ") + cudaGetErrorString(ce); return KKT_ERR_CUDA; }
   return KKT_OK;
 }
 
-extern "C" kkt_status hykkt_solve(kkt_handle h, const double* rbar1, const double* rbar2, double* dx,
-                                  double* dy, double cg_rtol, int cg_maxit, int max_outer_refine) {
+// Nodes of g without outgoing edges (the current tail of a recorded sequence).
+static kkt_status graph_leaves(cudaGraph_t g, std::vector<cudaGraphNode_t>& leaves) {
+  size_t nn = 0, ne = 0;
+  CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+  CUDA_TRY(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
+  std::vector<cudaGraphNode_t> nodes(nn), from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+  if (ne) CUDA_TRY(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
+  leaves.clear();
+  for (auto nd : nodes)
+    if (std::find(from.begin(), from.end(), nd) == from.end()) leaves.push_back(nd);
+  return KKT_OK;
+}
+
+// Append to graph g a WHILE node (after the current leaves) whose body is recorded by `body`;
+// the body's last kernel sets the condition through `hc`.
+template <class F>
+static kkt_status append_while(kkt_plan* h, cudaGraph_t g, cudaGraphConditionalHandle hc, F&& body) {
+  std::vector<cudaGraphNode_t> leaves;
+  TRY(graph_leaves(g, leaves));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CUDA_TRY(cudaGraphAddNode(&wn, g, leaves.data(), leaves.size(), &cp));
+  const bool pdl_saved = h->pdl;
+  h->pdl = false;  // programmatic launches are not captured into conditional bodies
+  kkt_status st = capture_into_graph(h, cp.conditional.phGraph_out[0], body);
+  h->pdl = pdl_saved;
+  return st;
+}
+
+// One HyKKT pass (eq. 14) for right-hand side (r1, r2) -> (dxo, dyo), recorded into
+// graph g (segments between WHILE nodes are captured in turn):
+//   s = r1 + gamma G^T r2 ;  z = K_gamma^-1 s ;  r = G z - r2 ;  p = r ; dy = 0
+//   Krylov loop on S_gamma dy = r (S_gamma = G K_gamma^-1 G^T), one graph WHILE node:
+//     CG (krylov 0):  q = S p ; alpha = r.r / p.q ; dy += alpha p ; r -= alpha q ; p = r + beta p
+//     CR (krylov 1, Hestenes-Stiefel conjugate residuals): with s = S r, q = S p,
+//                     alpha = r.s / q.q ; dy += alpha p ; r -= alpha q ; s = S r ;
+//                     beta = r.s_new / r.s_old ; p = r + beta p ; q = s + beta q
+//   dx = K_gamma^-1 (s - G^T dy)
+// Instances whose outer refinement has finished (skip != nullptr, C.odone) skip the whole pass.
+static kkt_status hykkt_pass(kkt_plan* h, cudaGraph_t g, cudaGraphConditionalHandle hc,
+                             const double* r1, const double* r2, double* dxo, double* dyo,
+                             double rtol, int maxit, bool first, int krylov) {
+  const Plan& P = h->P;
+  const int gs = grid_for((long long)P.batch * P.n, 256, h->sms);
+  const int* skip = first ? nullptr : h->C.odone;
+  dim3 gg(KKT_NPART, P.batch);
+  TRY(capture_into_graph(h, g, [&]() -> kkt_status {
+    cg_init_kernel<<<1, 256, 0, h->ls>>>(P.batch, h->C, first ? 0 : 1);
+    gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, skip);
+    LAUNCH_CHECK();
+    TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, skip));
+    g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0, first ? 1 : 0, nullptr);
+    LAUNCH_CHECK();
+    h->launches += 3;
+    if (krylov == 1) {  // s0 = q0 = S r0 (p0 = r0)
+      gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
+      LAUNCH_CHECK();
+      TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
+      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cs, h->cp, nullptr, h->C, 2, 0, h->cq);
+      LAUNCH_CHECK();
+      h->launches += 2;
+    }
+    cg_cond_kernel<<<1, 1, 0, h->ls>>>(P.batch, h->C, hc, 0);  // loop entry condition
+    LAUNCH_CHECK();
+    h->launches += 1;
+    return KKT_OK;
+  }));
+  const long long l0 = h->launches;
+  TRY(append_while(h, g, hc, [&]() -> kkt_status {
+    if (krylov == 0) {
+      gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
+      LAUNCH_CHECK();
+      TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
+      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1, 0, nullptr);
+      LAUNCH_CHECK();
+      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+                                               rtol, h->status, first ? 1 : 0, maxit);
+      LAUNCH_CHECK();
+      cg_p_kernel<<<dim3(std::max(1, std::min((P.m_eq + 255) / 256, 64)), P.batch), 256, 0, h->ls>>>(
+          P.batch, P.m_eq, h->cp, h->cr, h->C);
+      LAUNCH_CHECK();
+    } else {
+      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+                                               rtol, h->status, first ? 1 : 0, maxit);
+      LAUNCH_CHECK();
+      gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cr, 1.0, nullptr, h->wv, h->C.cg_done);
+      LAUNCH_CHECK();
+      TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
+      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, h->cr, h->cs, nullptr, nullptr, h->C, 3, 0, nullptr);
+      LAUNCH_CHECK();
+      cr_pq_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, h->cp, h->cq, h->cr, h->cs, h->C);
+      LAUNCH_CHECK();
+    }
+    cg_cond_kernel<<<1, 1, 0, h->ls>>>(P.batch, h->C, hc, 1);
+    LAUNCH_CHECK();
+    h->launches += 5;
+    return KKT_OK;
+  }));
+  h->hy_body = h->launches - l0;
+  return capture_into_graph(h, g, [&]() -> kkt_status {
+    cg_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C, first ? 1 : 0, h->status);
+    LAUNCH_CHECK();
+    // dx = K_gamma^-1 (s - G^T dy)
+    gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, dyo, -1.0, h->sg, h->wv, skip);
+    LAUNCH_CHECK();
+    TRY(launch_solve(h, h->wv, P.n, dxo, P.n, skip));
+    h->launches += 2;
+    return KKT_OK;
+  });
+}
+
+// The whole HyKKT solve as one graph: first pass, then max_outer_refine correction passes on
+// the saddle system [K_gamma-part G^T; G 0] with a double-double residual; the outer loop stops
+// per instance on the device (outer_decide_kernel), later passes skip finished instances.
+static kkt_status record_hykkt_graph(kkt_plan* h, double rtol, int maxit, int max_outer, int krylov,
+                                     cudaGraph_t* out) {
+  const Plan& P = h->P;
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  auto fail = [&](kkt_status st) { cudaGraphDestroy(g); return st; };
+  h->launches = 0;
+  kkt_status st = capture_into_graph(h, g, [&]() -> kkt_status {
+    outer_init_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C);
+    LAUNCH_CHECK();
+    return KKT_OK;
+  });
+  if (st != KKT_OK) return fail(st);
+  const long long mm = P.m_eq;
+  for (int k = 0; k <= max_outer; k++) {
+    cudaGraphConditionalHandle hc;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) { g_err = std::string("conditional handle: ") + cudaGetErrorString(e); return fail(KKT_ERR_CUDA); }
+    if (k == 0) {
+      st = hykkt_pass(h, g, hc, h->g_r1, h->g_r2, h->g_dx, h->g_dy, rtol, maxit, true, krylov);
+    } else {
+      // rho1 = rbar1 - K dx - G^T dy ; rho2 = rbar2 - G dx (double-double, K without gamma rows)
+      st = capture_into_graph(h, g, [&]() -> kkt_status {
+        return launch_resid(h, h->g_dx, h->g_r1, 1, h->g_dy, h->g_r2, h->hr1, nullptr, h->C.odone);
+      });
+      if (st == KKT_OK)
+        st = hykkt_pass(h, g, hc, h->hr1, h->res2, h->hdx, h->hdy, rtol, maxit, false, krylov);
+      if (st == KKT_OK)
+        st = capture_into_graph(h, g, [&]() -> kkt_status {
+          outer_update_kernel<<<grid_2d(P.n, P.batch, h->sms), 256, 0, h->ls>>>(P.batch, P.n, h->g_dx, h->hdx, h->C, 0);
+          LAUNCH_CHECK();
+          outer_update_kernel<<<grid_2d(mm, P.batch, h->sms), 256, 0, h->ls>>>(P.batch, mm, h->g_dy, h->hdy, h->C, 2);
+          LAUNCH_CHECK();
+          outer_decide_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, h->C);
+          LAUNCH_CHECK();
+          h->launches += 3;
+          return KKT_OK;
+        });
+    }
+    if (st != KKT_OK) return fail(st);
+  }
+  h->hy_fixed = h->launches - (long long)(max_outer + 1) * h->hy_body;
+  *out = g;
+  return KKT_OK;
+}
+
+extern "C" kkt_status hykkt_solve_krylov(kkt_handle h, const double* rbar1, const double* rbar2, double* dx,
+                                         double* dy, double cg_rtol, int cg_maxit, int max_outer_refine,
+                                         int krylov) {
   if (!h || !rbar1 || !dx) return KKT_ERR_ARG;
+  if (krylov != 0 && krylov != 1) { g_err = "krylov must be 0 (CG) or 1 (CR)"; return KKT_ERR_ARG; }
   const Plan& P = h->P;
   if (P.m_eq > 0 && (!rbar2 || !dy)) return KKT_ERR_ARG;
   if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
   if (cg_rtol <= 0) cg_rtol = 1e-12;
   if (cg_maxit <= 0) cg_maxit = std::max(1, std::min(P.m_eq, 2000));
+  max_outer_refine = std::max(0, max_outer_refine);
   h->launches = 0;
   h->graph_solve_pending = false;
+  h->hy_pending = false;
   if (P.m_eq == 0) return kkt_solve(h, rbar1, dx, max_outer_refine, 0.0);
-  TRY(hykkt_pass(h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, true));
-  const long long nn = (long long)P.batch * P.n, mm = (long long)P.batch * P.m_eq;
-  for (int k = 0; k < max_outer_refine; k++) {
-    // rho1 = rbar1 - K dx - G^T dy ; rho2 = rbar2 - G dx   (double-double, K without gamma rows)
-    TRY(launch_resid(h, dx, rbar1, 1, dy, rbar2, h->hr1, nullptr, nullptr));
-    CUDA_TRY(cudaMemcpyAsync(h->hr2, h->res2, mm * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    TRY(hykkt_pass(h, h->hr1, h->hr2, h->hdx, h->hdy, cg_rtol, cg_maxit, false));
-    axpy_kernel<<<grid_for(nn, 256, h->sms), 256, 0, h->ls>>>(nn, dx, h->hdx);
-    axpy_kernel<<<grid_for(mm, 256, h->sms), 256, 0, h->ls>>>(mm, dy, h->hdy);
-    LAUNCH_CHECK();
-    h->launches += 2;
+  const bool stale = !h->hy_exec || h->hy_rtol != cg_rtol || h->hy_maxit != cg_maxit ||
+                     h->hy_outer != max_outer_refine || h->hy_krylov != krylov || h->hy_W != h->Wv ||
+                     h->hy_J != h->Jv || h->hy_Sx != h->Sx || h->hy_gamma != h->gamma || h->hy_dw != h->dw;
+  if (stale) {
+    if (h->hy_exec) { cudaGraphExecDestroy(h->hy_exec); h->hy_exec = nullptr; }
+    cudaGraph_t g = nullptr;
+    TRY(record_hykkt_graph(h, cg_rtol, cg_maxit, max_outer_refine, krylov, &g));
+    cudaError_t e = cudaGraphInstantiate(&h->hy_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { g_err = std::string("hykkt graph instantiate: ") + cudaGetErrorString(e); return KKT_ERR_CUDA; }
+    h->hy_rtol = cg_rtol; h->hy_maxit = cg_maxit; h->hy_outer = max_outer_refine; h->hy_krylov = krylov;
+    h->hy_W = h->Wv; h->hy_J = h->Jv; h->hy_Sx = h->Sx; h->hy_gamma = h->gamma; h->hy_dw = h->dw;
   }
+  const size_t nb = (size_t)P.batch * P.n * sizeof(double), mb = (size_t)P.batch * P.m_eq * sizeof(double);
+  CUDA_TRY(cudaMemcpyAsync(h->g_r1, rbar1, nb, cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(h->g_r2, rbar2, mb, cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaGraphLaunch(h->hy_exec, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(dx, h->g_dx, nb, cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(dy, h->g_dy, mb, cudaMemcpyDeviceToDevice, h->stream));
+  h->launches = h->hy_fixed;
+  h->hy_pending = true;
   return KKT_OK;
+}
+
+extern "C" kkt_status hykkt_solve(kkt_handle h, const double* rbar1, const double* rbar2, double* dx,
+                                  double* dy, double cg_rtol, int cg_maxit, int max_outer_refine) {
+  return hykkt_solve_krylov(h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine, 0);
 }
 
 extern "C" kkt_status kkt_sync_info(kkt_handle h, int* status, int* fail_col, int* refine_iters,
@@ -1291,6 +1466,13 @@ extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
     if (h->solve_while) h->launches = h->g_pro + h->g_body * std::max(0, sw - (h->g_max_refine >= 1 ? 2 : 1));
     else h->launches = h->g_pro + (sw > 2 ? h->g_body : 0);  // IF body: all of sweeps 2.. or none
     h->graph_solve_pending = false;
+  }
+  if (h->hy_pending) {  // HyKKT graph: add the executed Krylov bodies
+    int runs = 0;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    CUDA_TRY(cudaMemcpy(&runs, h->C.cg_runs, sizeof(int), cudaMemcpyDeviceToHost));
+    h->launches = h->hy_fixed + h->hy_body * runs;
+    h->hy_pending = false;
   }
   *launches = h->launches;
   return KKT_OK;

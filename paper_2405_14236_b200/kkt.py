@@ -20,7 +20,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
               7: "KKT_ERR_ALLOC", 8: "KKT_ERR_STATE"}
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
-           "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve",
+           "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
            "kkt_sync_info", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
            "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_last_error", "kkt_destroy"]
 
@@ -74,6 +74,7 @@ def lib(build_if_missing: bool = True):
             "kkt_factor": [P],
             "kkt_solve": [P, P, P, I, D],
             "hykkt_solve": [P, P, P, P, P, D, I, I],
+            "hykkt_solve_krylov": [P, P, P, P, P, D, I, I, I],
             "kkt_sync_info": [P, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I),
                               C.POINTER(D)],
             "kkt_step_host": [P, P, P, P, P, P, D, D, D, P, P, I, D],
@@ -165,6 +166,11 @@ def kkt_solve(h, b, x, max_refine=10, tol_bwd=0.0):
 def hykkt_solve(h, rbar1, rbar2, dx, dy, cg_rtol=1e-12, cg_maxit=0, max_outer_refine=2):
     _chk(lib().hykkt_solve(h, _ptr(rbar1), _ptr(rbar2), _ptr(dx), _ptr(dy), float(cg_rtol),
                            int(cg_maxit), int(max_outer_refine)), "hykkt_solve")
+
+
+def hykkt_solve_krylov(h, rbar1, rbar2, dx, dy, cg_rtol=1e-12, cg_maxit=0, max_outer_refine=2, krylov=0):
+    _chk(lib().hykkt_solve_krylov(h, _ptr(rbar1), _ptr(rbar2), _ptr(dx), _ptr(dy), float(cg_rtol),
+                                  int(cg_maxit), int(max_outer_refine), int(krylov)), "hykkt_solve_krylov")
 
 
 def kkt_sync_info(h):
@@ -275,8 +281,11 @@ class KKTSolver:
     def solve(self, b, x, max_refine=10, tol_bwd=0.0):
         kkt_solve(self.h, b, x, max_refine, tol_bwd)
 
-    def hykkt_solve(self, rbar1, rbar2, dx, dy, cg_rtol=1e-12, cg_maxit=0, max_outer_refine=2):
-        hykkt_solve(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine)
+    def hykkt_solve(self, rbar1, rbar2, dx, dy, cg_rtol=1e-12, cg_maxit=0, max_outer_refine=2, krylov=0):
+        if krylov:
+            hykkt_solve_krylov(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine, krylov)
+        else:
+            hykkt_solve(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine)
 
     def recover(self, r2, r4, dx, dz, ds):
         kkt_recover(self.h, r2, r4, dx, dz, ds)

@@ -28,7 +28,7 @@ def run_lifted(inst, max_refine=10, tol_bwd=0.0, solver=None, device="cuda:0", D
     return x.cpu().numpy(), info, S
 
 
-def run_hykkt(inst, cg_rtol=1e-12, cg_maxit=0, max_outer=2, solver=None, device="cuda:0"):
+def run_hykkt(inst, cg_rtol=1e-12, cg_maxit=0, max_outer=2, solver=None, device="cuda:0", krylov=0):
     import torch
     S = solver or K.KKTSolver.from_instance(inst).bind(0)
     W, J, Sx, Ss, r1, r2 = [dev(a, device) for a in (inst.W_vals, inst.J_vals, inst.Sigma_x,
@@ -38,7 +38,7 @@ def run_hykkt(inst, cg_rtol=1e-12, cg_maxit=0, max_outer=2, solver=None, device=
     dy = torch.zeros_like(r2)
     S.condense(W, J, Sx, Ss, None, inst.delta_w, inst.delta_c, inst.gamma)
     S.factor()
-    S.hykkt_solve(r1, r2, dx, dy, cg_rtol, cg_maxit, max_outer)
+    S.hykkt_solve(r1, r2, dx, dy, cg_rtol, cg_maxit, max_outer, krylov=krylov)
     info = S.sync_info()
     return dx.cpu().numpy(), dy.cpu().numpy(), info, S
 

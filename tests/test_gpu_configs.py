@@ -181,3 +181,68 @@ def test_hykkt_C3_gamma_sweep(gamma, Xi):
     assert relerr(dx, R["dx"]) <= 1e-8 and relerr(dy, R["dy"]) <= 1e-8, \
         (relerr(dx, R["dx"]), relerr(dy, R["dy"]), info)
     S.close()
+
+
+def _dense_schur(inst):
+    """Dense K_gamma (oracle condensation), G and the HyKKT right-hand side of eq. 14."""
+    from oracle import dense
+    Kp, Ki, Kv = oracle.condense(inst)
+    n, me = inst.n, inst.m_eq
+    Kg = np.zeros((n, n))
+    for j in range(n):
+        for p in range(Kp[j], Kp[j + 1]):
+            Kg[Ki[p], j] = Kv[p]
+            Kg[j, Ki[p]] = Kv[p]
+    G = dense.dense_J(inst)[:me]
+    s = inst.rbar1 + inst.gamma * G.T @ inst.rbar2
+    Kinv_GT = np.linalg.solve(Kg, G.T)
+    return G @ Kinv_GT, G @ np.linalg.solve(Kg, s) - inst.rbar2
+
+
+@pytest.mark.parametrize("krylov", [0, 1])
+@pytest.mark.parametrize("seed,gamma", [(1, 1e3), (2, 1e6)])
+def test_hykkt_krylov_tiny_parity_and_counts(krylov, seed, gamma):
+    """CG (krylov 0) and CR (krylov 1) on the device loop: solution parity with the
+    oracle's refined saddle solution, and the first pass's iteration count within one of the
+    oracle's cg_dense / cr_dense on the explicitly formed S_gamma = G K_gamma^-1 G^T."""
+    from kkt_gpu import run_hykkt, relerr
+    from synth.generator import tiny_random
+    inst = tiny_random(60, 40, 15, seed=seed, Xi=1.0 / gamma, hykkt_gamma=gamma)
+    R = oracle.reference_hykkt(inst)
+    dx, dy, info, S = run_hykkt(inst, max_outer=3, krylov=krylov)
+    assert info["status"] == 0, info
+    assert relerr(dx, R["dx"]) <= 1e-8 and relerr(dy, R["dy"]) <= 1e-8
+    Sg, rhs = _dense_schur(inst)
+    if krylov == 0:
+        _, st, it = oracle.cg_dense(Sg, rhs, rtol=1e-12, maxit=2000)
+    else:
+        _, st, it, _ = oracle.cr_dense(Sg, rhs, rtol=1e-12, maxit=2000)
+    assert st == 0 and abs(info["cg_iters"] - it) <= 1, (info["cg_iters"], it)
+    S.close()
+
+
+@pytest.mark.parametrize("gamma", [1e4, 1e7])
+def test_hykkt_cr_C3(gamma):
+    """Conjugate residuals on C3 (HyKKT, 10k buses): parity with the oracle."""
+    from kkt_gpu import run_hykkt, relerr
+    inst = make_config("C3", gamma=gamma)
+    R = oracle.reference_hykkt(inst)
+    dx, dy, info, S = run_hykkt(inst, max_outer=3, krylov=1)
+    assert info["status"] == 0, info
+    assert relerr(dx, R["dx"]) <= 1e-8 and relerr(dy, R["dy"]) <= 1e-8, \
+        (relerr(dx, R["dx"]), relerr(dy, R["dy"]), info)
+    S.close()
+
+
+def test_hykkt_is_graph_launched_without_host_sync():
+    """hykkt_solve enqueues one recorded graph: a second call with the same pointers re-uses
+    it, and the launch counter (read after the fact) includes the executed Krylov bodies."""
+    import torch
+    from kkt_gpu import run_hykkt, relerr
+    inst = make_config("C3", gamma=1e6)
+    dx, dy, info, S = run_hykkt(inst, max_outer=2)
+    n1 = S.launch_count()
+    assert n1 > 10 * max(info["cg_iters"], 1)
+    dx2, dy2, info2, _ = run_hykkt(inst, max_outer=2, solver=S)
+    assert np.array_equal(dx, dx2) and np.array_equal(dy, dy2)     # deterministic
+    S.close()

@@ -1,4 +1,4 @@
-"""Pins for oracle.cg_dense and oracle.hykkt -- CPU only.
+"""Pins for oracle.cg_dense, oracle.cr_dense and oracle.hykkt -- CPU only.
 
 Pins: CG finite termination on constructed spectra; HyKKT equals the
 dense solve of the condensed saddle system with delta_c = 0; m_eq = 0 reduces to a
@@ -33,6 +33,49 @@ def test_cg_two_distinct_eigenvalues(seed):
     b = rng.standard_normal(10)
     x, st, it = oracle.cg_dense(A, b, rtol=1e-12)
     assert st == 0 and it <= 2 and np.allclose(A @ x, b, atol=1e-11)
+
+
+def test_cr_identity_one_iteration():
+    x, st, it, h = oracle.cr_dense(np.eye(7), np.arange(1.0, 8.0))
+    assert st == 0 and it == 1 and np.allclose(x, np.arange(1.0, 8.0), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_cr_two_distinct_eigenvalues(seed):
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    A = (Q * np.where(rng.random(10) < 0.5, 1.0, 7.0)) @ Q.T
+    b = rng.standard_normal(10)
+    x, st, it, h = oracle.cr_dense(A, b, rtol=1e-12)
+    assert st == 0 and it <= 2 and np.allclose(A @ x, b, atol=1e-11)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_cr_is_the_minimal_residual_krylov_method(seed):
+    """CR decreases the residual norm monotonically.  Stronger pin: its k-th
+    residual equals min over y in K_k(A, b) of ||b - A y||_2 (least squares over an explicit
+    orthonormal Krylov basis), and CR and CG reach the same solution."""
+    rng = np.random.default_rng(100 + seed)
+    n = 30
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (Q * np.logspace(0, 3, n)) @ Q.T
+    A = (A + A.T) / 2
+    b = rng.standard_normal(n)
+    x, st, it, hist = oracle.cr_dense(A, b, rtol=1e-12, maxit=500)
+    assert st == 0
+    assert np.all(np.diff(hist) <= 1e-12 * hist[0])           # monotone
+    V = np.zeros((n, 0))
+    v = b.copy()
+    for k in range(1, 7):
+        for _ in range(2):                                       # twice-orthogonalised basis
+            v = v - V @ (V.T @ v)
+        V = np.column_stack([V, v / np.linalg.norm(v)])
+        y, *_ = np.linalg.lstsq(A @ V, b, rcond=None)
+        rmin = np.linalg.norm(b - A @ (V @ y))
+        assert abs(hist[k] - rmin) <= 1e-9 * hist[0], (k, hist[k], rmin)
+        v = A @ V[:, -1]
+    xc, stc, itc = oracle.cg_dense(A, b, rtol=1e-12, maxit=500)
+    assert np.abs(x - xc).max() <= 1e-9 * np.abs(xc).max()
 
 
 def _split(inst):
