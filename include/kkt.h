@@ -237,6 +237,13 @@ kkt_status kkt_launch_count(kkt_handle h, long long *launches);
  * Returns 0 on success, -1 when the record is off, -2 on a CUDA error.  Blocking. */
 int kkt_debug_steps(kkt_handle h, long long *out, int n);
 
+/* Tracing export of the tile-task factorisation of the large fronts: returns the task count
+ * (or -1 when there is no tile plan / tracing is off, -2 on a CUDA error) and copies up to n
+ * entries: [host] tasks[n][4] (type | instance << 4, front, i | j << 16, k) in issue order,
+ * trace[n][4] (globaltimer ns at ticket, dependencies met, end; SM id) when KKT_TRACE=1 was set
+ * at kkt_bind; *est_us = the bind-time list-schedule estimate of the makespan.  Blocking. */
+int kkt_tile_trace(kkt_handle h, long long *trace, int *tasks, int n, double *est_us);
+
 /* Last error message (static storage, thread-local). */
 const char *kkt_last_error(void);
 

@@ -18,7 +18,9 @@
 #include "hsolve.cuh"
 #include "resid.cuh"
 #include "trsv.cuh"
+#include "tiles.cuh"
 #include "plan.h"
+#include "tile_plan.h"
 
 using namespace kkt;
 
@@ -123,6 +125,15 @@ struct kkt_plan {
   bool graph_solve_pending = false;  // last call was a graph solve whose sweep count is unread
   std::vector<cudaGraphExec_t> extra_exec;  // further instantiated graphs (HyKKT loop)
   cudaEvent_t fev[3] = {nullptr, nullptr, nullptr};  // factor phase events (start, before huge, end)
+  // tile-task factorisation of the huge fronts (tiles.cuh); KKT_HUGE_OLD=1: level kernel (huge.cuh)
+  bool tiles = true;
+  TilePlan tp{};
+  void* tile_mem = nullptr;   // fronts + tasks + hidx
+  void* tile_pool = nullptr;  // [batch][pool] + counters
+  size_t tile_cnt_bytes = 0;
+  int g_tile = 1;
+  double tile_est_us = 0.0;
+  long long* tile_trace = nullptr;  // KKT_TRACE: per-task stamps of the tile kernel
   bool fev_valid = false;
 };
 
@@ -395,6 +406,7 @@ static void release_device(kkt_plan* h) {
   if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
   h->pinned_flags = nullptr;
   fr(h->trace_buf); fr(h->dbg_buf); fr(h->huge_mem); fr(h->hsolve_mem);
+  fr(h->tile_mem); fr(h->tile_pool); fr(h->tile_trace);
   if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
   h->solve_exec = nullptr;
   if (h->hy_exec) cudaGraphExecDestroy(h->hy_exec);
@@ -661,6 +673,64 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       h->hsched.dbg = h->dbg_buf;
       TRY(build_huge_sched(h, h->g_hsolve, false, &h->hsched_s, &h->hsolve_mem));
     }
+    h->tiles = !(getenv("KKT_HUGE_OLD") && atoi(getenv("KKT_HUGE_OLD")) > 0);
+    if (!P.order_h.empty() && h->tiles) {
+      CUDA_TRY(cudaFuncSetAttribute(tile_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
+      int occ_t = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, tile_factor_kernel, TILE_THREADS, TILE_SMEM_BYTES));
+      if (occ_t < 1) { g_err = "tile_factor_kernel does not fit on an SM"; return KKT_ERR_CUDA; }
+      h->g_tile = occ_t * h->sms;
+      TilePlanHost tph;
+      build_tile_plan(P, h->g_tile, tph);
+      h->tile_est_us = tph.est_us;
+      if (!tph.ok) h->tiles = false;  // fall back to the level kernel (huge.cuh)
+    }
+    if (!P.order_h.empty() && h->tiles) {
+      TilePlanHost tph;
+      build_tile_plan(P, h->g_tile, tph);
+      const size_t B = P.batch;
+      std::vector<TTask> tasks;
+      tasks.reserve(tph.tasks.size() * B);
+      for (const TTask& t : tph.tasks)   // instances interleaved: topological per instance
+        for (size_t b = 0; b < B; b++) tasks.push_back(TTask{t.x | (int)(b << 4), t.y, t.z, t.w});
+      const size_t fb = align_up(tph.fr.size() * sizeof(TFrontHost)), tkb = align_up(tasks.size() * sizeof(TTask));
+      const size_t hb = align_up(tph.hidx.size() * sizeof(int));
+      const size_t chb = align_up(tph.tch.size() * sizeof(int)), cub = align_up(tph.tcut.size() * sizeof(int));
+      const size_t kpb = align_up(tph.tkptr.size() * sizeof(int)), kib = align_up(tph.tkidx.size() * sizeof(int));
+      CUDA_TRY(cudaMalloc(&h->tile_mem, fb + tkb + hb + chb + cub + kpb + kib));
+      char* base = (char*)h->tile_mem;
+      CUDA_TRY(cudaMemcpy(base, tph.fr.data(), tph.fr.size() * sizeof(TFrontHost), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(base + fb, tasks.data(), tasks.size() * sizeof(TTask), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(base + fb + tkb, tph.hidx.data(), tph.hidx.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(base + fb + tkb + hb, tph.tch.data(), tph.tch.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(base + fb + tkb + hb + chb, tph.tcut.data(), tph.tcut.size() * sizeof(int), cudaMemcpyHostToDevice));
+      char* kb_ = base + fb + tkb + hb + chb + cub;
+      CUDA_TRY(cudaMemcpy(kb_, tph.tkptr.data(), tph.tkptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(kb_ + kpb, tph.tkidx.data(), tph.tkidx.size() * sizeof(int), cudaMemcpyHostToDevice));
+      const size_t poolb = align_up(B * (size_t)tph.pool_doubles * sizeof(double));
+      h->tile_cnt_bytes = align_up((B * (size_t)tph.ncnt + 1) * sizeof(int));
+      CUDA_TRY(cudaMalloc(&h->tile_pool, poolb + h->tile_cnt_bytes));
+      TilePlan& T = h->tp;
+      T.fr = (const TFront*)base;
+      T.tasks = (const int4*)(base + fb);
+      T.hidx = (const int*)(base + fb + tkb);
+      T.tch = (const int2*)(base + fb + tkb + hb);
+      T.tcut = (const int*)(base + fb + tkb + hb + chb);
+      T.tkptr = (const int*)kb_;
+      T.tkidx = (const int*)(kb_ + kpb);
+      T.nf = (int)tph.fr.size();
+      T.ntask = (int)tasks.size();
+      T.ncnt = tph.ncnt;
+      T.pool_doubles = tph.pool_doubles;
+      T.pool = (double*)h->tile_pool;
+      T.cnt = (int*)((char*)h->tile_pool + poolb);
+      T.trace = nullptr;
+      if (getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
+        CUDA_TRY(cudaMalloc(&h->tile_trace, (size_t)T.ntask * 4 * sizeof(long long)));
+        CUDA_TRY(cudaMemset(h->tile_trace, 0, (size_t)T.ntask * 4 * sizeof(long long)));
+        T.trace = h->tile_trace;
+      }
+    }
   }
   CUDA_TRY(cudaHostAlloc(&h->pinned_flags, 64 * sizeof(int) + (size_t)P.batch * sizeof(int), cudaHostAllocDefault));
   for (auto& e : h->fev) CUDA_TRY(cudaEventCreate(&e));
@@ -760,7 +830,19 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     h->launches++;
   }
   if (ev) CUDA_TRY(cudaEventRecord(h->fev[1], h->ls));
-  if (!P.order_h.empty()) {
+  if (!P.order_h.empty() && h->tiles) {
+    CUDA_TRY(cudaMemsetAsync(h->tp.cnt, 0, h->tile_cnt_bytes, h->ls));
+    DevPlan dp = h->dp;
+    TilePlan tp = h->tp;
+    const double* kv = h->Kv;
+    double *lx = h->Lx, *dv = h->Dv;
+    const double* ub = h->Ub;
+    int* fail = h->fail;
+    void* args[] = {&dp, &tp, &kv, &lx, &ub, &dv, &fail};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_factor_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
+                                         (size_t)TILE_SMEM_BYTES, h->ls));
+    h->launches++;
+  } else if (!P.order_h.empty()) {
     DevPlan dp = h->dp;
     const double* kv = h->Kv;
     double *lx = h->Lx, *ub = h->Ub, *dv = h->Dv;
@@ -1483,6 +1565,21 @@ extern "C" kkt_status kkt_destroy(kkt_handle h) {
   release_device(h);
   delete h;
   return KKT_OK;
+}
+
+// tracing aid: per-task stamps of the tile-task factorisation (KKT_TRACE=1 at kkt_bind)
+extern "C" int kkt_tile_trace(kkt_handle h, long long* trace, int* tasks, int n, double* est_us) {
+  if (!h || !h->tiles || !h->tile_mem) return -1;
+  if (est_us) *est_us = h->tile_est_us;
+  const int nt = h->tp.ntask;
+  n = std::min(n, nt);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return -2;
+  if (tasks && n > 0 && cudaMemcpy(tasks, h->tp.tasks, (size_t)n * 16, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  if (trace && n > 0) {
+    if (!h->tile_trace) return -1;
+    if (cudaMemcpy(trace, h->tile_trace, (size_t)n * 32, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  }
+  return nt;
 }
 
 // debugging aid (not part of the public header): per-step stamps of the root front, KKT_TRACE=2

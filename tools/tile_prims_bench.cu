@@ -1,0 +1,74 @@
+// Micro-benchmark of the tile-task primitives of tiles.cuh (one CTA per SM, each repeats the
+// primitive; reports cycles per call).  Build: nvcc -std=c++17 -O3 -gencode
+// arch=compute_100a,code=sm_100a -o tools/tile_prims_bench tools/tile_prims_bench.cu
+#include <cstdio>
+#include <vector>
+#include <cmath>
+#include "../paper_2405_14236_b200/csrc/tiles.cuh"
+using namespace kkt;
+
+__global__ void __launch_bounds__(256, 1) bench(int which, int reps, double* g, double* dinv, long long* out) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int sf;
+  double* gt = g + (long long)blockIdx.x * 4 * TBD;
+  if (threadIdx.x == 0) sf = -1;
+  tile_load_async(sm, gt); tile_load_async(sm + TBD, gt + TBD); tile_load_async(sm + 2 * TBD, gt + 2 * TBD);
+  cp_async_wait_all();
+  __syncthreads();
+  long long t0 = clock64();
+  for (int r = 0; r < reps; r++) {
+    if (which == 0) {          // potrf64 (re-load the SPD tile each rep)
+      tile_load_async(sm, gt); cp_async_wait_all(); __syncthreads();
+      tile_potrf64(sm, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+    } else if (which == 1) {   // trsm64 against the factored tile in sm+TBD
+      tile_load_async(sm, gt + 2 * TBD); cp_async_wait_all(); __syncthreads();
+      tile_trsm64(sm, sm + TBD, sm + 3 * TBD);
+    } else if (which == 2) {   // gemm into global C
+      tile_gemm_nt_global(gt + 3 * TBD, sm, sm + TBD);
+      __syncthreads();
+    } else if (which == 3) {   // load 2 tiles
+      tile_load_async(sm, gt); tile_load_async(sm + TBD, gt + TBD); cp_async_wait_all(); __syncthreads();
+    } else if (which == 4) {   // diag32 only
+      if (threadIdx.x < 32) tile_diag32<0>(sm, 32, threadIdx.x, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+      __syncthreads();
+    } else if (which == 5) {   // rowsolve32 64 rows
+      tile_rowsolve32<0>(sm + 2 * TBD, 0, 64, sm + TBD, sm + 3 * TBD);
+      __syncthreads();
+    } else if (which == 6) {   // gemm into smem C
+      tile_gemm_nt_smem(sm + 2 * TBD, sm, sm + TBD);
+    }
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / reps;
+}
+
+int main() {
+  const int nb = 296;
+  std::vector<double> h((size_t)nb * 4 * TBD);
+  // tile 0: SPD (diagonally dominant), tile 1: its factor is produced by which=0 (we fake: identity-ish lower),
+  for (int b = 0; b < nb; b++) {
+    double* t = h.data() + (size_t)b * 4 * TBD;
+    for (int c = 0; c < 64; c++) for (int r = 0; r < 64; r++) {
+      t[c * 64 + r] = (r == c) ? 70.0 : 0.5 / (1 + r + c);                  // SPD
+      t[TBD + c * 64 + r] = (r == c) ? 2.0 : (r > c ? 0.01 : 0.0);          // lower "L"
+      t[2 * TBD + c * 64 + r] = 0.3 * std::sin(r + 2.0 * c);
+      t[3 * TBD + c * 64 + r] = 0.0;
+    }
+  }
+  double *g, *dinv; long long* out;
+  cudaMalloc(&g, h.size() * 8); cudaMalloc(&dinv, nb * 64 * 8); cudaMalloc(&out, nb * 8);
+  cudaMemcpy(g, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES);
+  const char* names[] = {"potrf64", "trsm64", "gemm_global", "load2tiles", "diag32", "rowsolve32x64", "gemm_smem"};
+  for (int w = 0; w < 7; w++) {
+    for (int grid : {1, 148, 296}) {
+      bench<<<grid, 256, TILE_SMEM_BYTES>>>(w, 20, g, dinv, out);
+      cudaError_t e = cudaDeviceSynchronize();
+      std::vector<long long> o(nb);
+      cudaMemcpy(o.data(), out, (grid < nb ? grid : nb) * 8, cudaMemcpyDeviceToHost);
+      printf("%-14s grid %3d: %8lld cycles/call (%.2f us @1.965GHz)  %s\n", names[w], grid, o[0], o[0] / 1965.0,
+             e == cudaSuccess ? "" : cudaGetErrorString(e));
+    }
+  }
+  return 0;
+}
