@@ -169,6 +169,32 @@ kkt_status hykkt_solve_krylov(kkt_handle h, const double *rbar1, const double *r
                               double *dy, double cg_rtol, int cg_maxit, int max_outer_refine,
                               int krylov);
 
+/*
+ * kkt_solve_unreduced -- Newton direction of the unreduced KKT system K3 (eq. K3) with
+ * Richardson refinement on K3 itself.  Unknowns
+ * d = (dx[n], ds[mi], dy[me], dz[mi], du[n], dv[mi]) with me = m_eq (rows G of J) and
+ * mi = m - m_eq (rows H); X, S, U, V = diag(x, s, u, v).  Solves K3 d = f:
+ *   W dx + G^T dy + H^T dz - du = f1,   dz - dv = f2,   G dx = f3,   H dx + ds = f4,
+ *   U dx + X du = f5,                   V ds + S dv = f6
+ * (f = -F_mu of P:306-315).  The condensed factor of the last kkt_condense/kkt_factor is the
+ * preconditioner: it must be built with Sigma_x = u/x and Sigma_s = v/s (D_x = X^-1 U, D_s =
+ * S^-1 V) -- delta_w, delta_c (and gamma for m_eq > 0, via the HyKKT solve) only
+ * regularise the preconditioner; the iteration converges to the unregularised K3 solution.
+ * Sweep 1 is the direct solve through the condensed system (recovery of P:360-362);
+ * sweeps 2.. are Richardson corrections with a double-double K3 residual.  Per instance the loop
+ * stops when the relative correction ||e||_inf / ||d||_inf <= tol (tol <= 0 -> 1e-14), on a
+ * geometric prediction below tol, or after 1 + max_refine sweeps; kkt_sync_info's refine_iters
+ * reports the corrections applied.  [device] x, u, f1, f5, dx, du [n]; s, v, f2, f4, f6, ds, dz,
+ * dv [mi] (may be NULL if mi = 0); f3, dy [me] (NULL if me = 0); batch-strided; outputs are
+ * overwritten.  Non-blocking for m_eq = 0; for m_eq > 0 each correction is one hykkt_solve.
+ * KKT_ERR_STATE if kkt_condense was given a D override.
+ */
+kkt_status kkt_solve_unreduced(kkt_handle h, const double *x, const double *s, const double *u,
+                               const double *v, const double *f1, const double *f2, const double *f3,
+                               const double *f4, const double *f5, const double *f6, double *dx,
+                               double *ds, double *dy, double *dz, double *du, double *dv,
+                               int max_refine, double tol);
+
 /* Block the host until the handle's stream is idle; report and clear the device status.
  * Any out pointer may be NULL.  status: a kkt_status value; fail_col: original column of
  * the first non-SPD pivot or -1; refine_iters: sweeps run by the last solve (max over the

@@ -152,3 +152,33 @@ def exact_solve(K, b):
         s = A[c][n] - sum(A[c][k] * x[k] for k in range(c + 1, n))
         x[c] = s / A[c][c]
     return x
+
+
+def k3_matrix(W, G, H, x, s, u, v):
+    """Dense unreduced KKT matrix K3 (eq. K3), unknown order (dx, ds, dy, dz, du, dv):
+    rows  [W 0 G^T H^T -I 0; 0 0 0 I 0 -I; G 0 0 0 0 0; H I 0 0 0 0; U 0 0 0 X 0; 0 V 0 0 0 S]."""
+    n, me, mi = W.shape[0], G.shape[0], H.shape[0]
+    N = 2 * n + 3 * mi + me
+    K = np.zeros((N, N))
+    ix, is_, iy = 0, n, n + mi
+    iz, iu, iv = n + mi + me, n + 2 * mi + me, 2 * n + 2 * mi + me
+    K[ix:ix + n, ix:ix + n] = W
+    K[ix:ix + n, iy:iy + me] = G.T
+    K[ix:ix + n, iz:iz + mi] = H.T
+    K[ix:ix + n, iu:iu + n] = -np.eye(n)
+    K[is_:is_ + mi, iz:iz + mi] = np.eye(mi)
+    K[is_:is_ + mi, iv:iv + mi] = -np.eye(mi)
+    K[iy:iy + me, ix:ix + n] = G
+    K[iz:iz + mi, ix:ix + n] = H
+    K[iz:iz + mi, is_:is_ + mi] = np.eye(mi)
+    K[iu:iu + n, ix:ix + n] = np.diag(u)
+    K[iu:iu + n, iu:iu + n] = np.diag(x)
+    K[iv:iv + mi, is_:is_ + mi] = np.diag(v)
+    K[iv:iv + mi, iv:iv + mi] = np.diag(s)
+    return K
+
+
+def k3_split(d, n, me, mi):
+    """(dx, ds, dy, dz, du, dv) blocks of a K3 vector."""
+    o = np.cumsum([0, n, mi, me, mi, n, mi])
+    return tuple(d[o[k]:o[k + 1]] for k in range(6))

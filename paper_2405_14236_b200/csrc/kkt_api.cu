@@ -19,6 +19,7 @@
 #include "resid.cuh"
 #include "trsv.cuh"
 #include "tiles.cuh"
+#include "k3.cuh"
 #include "plan.h"
 #include "tile_plan.h"
 
@@ -76,6 +77,7 @@ struct kkt_plan {
   double *sg = nullptr, *zv = nullptr, *wv = nullptr, *hdx = nullptr, *hr1 = nullptr;
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
   double *cs = nullptr;                                    // CR: s = S r
+  K3Ctx k3{};                                              // unreduced-system refinement (k3.cuh)
   double *g_r1 = nullptr, *g_r2 = nullptr, *g_dx = nullptr, *g_dy = nullptr;  // HyKKT graph I/O
   cudaGraphExec_t hy_exec = nullptr;                       // recorded HyKKT solve
   double hy_rtol = -1, hy_gamma = 0, hy_dw = 0;
@@ -220,6 +222,16 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.opass = c.take<int>(B);
   h->C.cg_runs = c.take<int>(1);
   h->cs = c.take<double>(B * me);
+  {  // K3 refinement scratch (k3.cuh)
+    const size_t mi = m - me;
+    h->k3.r5 = c.take<double>(B * n); h->k3.c1 = c.take<double>(B * n); h->k3.ex = c.take<double>(B * n);
+    h->k3.ey = c.take<double>(B * std::max<size_t>(me, 1)); h->k3.r3 = c.take<double>(B * std::max<size_t>(me, 1));
+    h->k3.b2 = c.take<double>(B * std::max<size_t>(mi, 1)); h->k3.r4 = c.take<double>(B * std::max<size_t>(mi, 1));
+    h->k3.r6 = c.take<double>(B * std::max<size_t>(mi, 1));
+    h->k3.tw = c.take<double2>(B * std::max<size_t>(m, 1));
+    h->k3.done = c.take<int>(B + 1); h->k3.nrm = c.take<unsigned long long>(2 * B);
+    h->k3.prev = c.take<double>(B); h->k3.sweeps = c.take<int>(B);
+  }
   h->g_r1 = c.take<double>(B * n);
   h->g_dx = c.take<double>(B * n);
   h->g_r2 = c.take<double>(B * me);
@@ -1382,6 +1394,74 @@ extern "C" kkt_status hykkt_solve_krylov(kkt_handle h, const double* rbar1, cons
   CUDA_TRY(cudaMemcpyAsync(dy, h->g_dy, mb, cudaMemcpyDeviceToDevice, h->stream));
   h->launches = h->hy_fixed;
   h->hy_pending = true;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_solve_unreduced(kkt_handle h, const double* x, const double* s, const double* u,
+                                          const double* v, const double* f1, const double* f2, const double* f3,
+                                          const double* f4, const double* f5, const double* f6, double* dx,
+                                          double* ds, double* dy, double* dz, double* du, double* dv,
+                                          int max_refine, double tol) {
+  if (!h || !x || !u || !f1 || !f5 || !dx || !du) return KKT_ERR_ARG;
+  if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
+  if (h->Dov) { g_err = "kkt_solve_unreduced needs the Sigma_s form of kkt_condense (no D override)"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  const int me = P.m_eq, mi = P.m - P.m_eq;
+  if (mi > 0 && (!s || !v || !f2 || !f4 || !f6 || !ds || !dz || !dv)) return KKT_ERR_ARG;
+  if (me > 0 && (!f3 || !dy)) return KKT_ERR_ARG;
+  max_refine = std::max(0, max_refine);
+  if (tol <= 0) tol = 1e-14;
+  const size_t B = P.batch;
+  K3Ctx& K = h->k3;
+  K.x = x; K.s = s; K.u = u; K.v = v;
+  K.f1 = f1; K.f2 = f2; K.f3 = f3; K.f4 = f4; K.f5 = f5; K.f6 = f6;
+  K.dx = dx; K.ds = ds; K.dy = dy; K.dz = dz; K.du = du; K.dv = dv;
+  K.dw = h->dw; K.dc = h->dc; K.Ss = h->Ss;
+  cudaStream_t st = h->stream;
+  CUDA_TRY(cudaMemsetAsync(dx, 0, B * P.n * 8, st));
+  CUDA_TRY(cudaMemsetAsync(du, 0, B * P.n * 8, st));
+  if (mi > 0) {
+    CUDA_TRY(cudaMemsetAsync(ds, 0, B * mi * 8, st));
+    CUDA_TRY(cudaMemsetAsync(dz, 0, B * mi * 8, st));
+    CUDA_TRY(cudaMemsetAsync(dv, 0, B * mi * 8, st));
+  }
+  if (me > 0) CUDA_TRY(cudaMemsetAsync(dy, 0, B * me * 8, st));
+  long long launches = 0;
+  k3_init_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, K);
+  LAUNCH_CHECK();
+  launches++;
+  for (int sw = 0; sw <= max_refine; sw++) {
+    if (P.m > 0) {
+      k3_rows_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(h->dp, h->Jv, K);
+      LAUNCH_CHECK();
+      launches++;
+    }
+    k3_cols_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>(h->dp, h->Wv, h->Jv, K);
+    LAUNCH_CHECK();
+    launches++;
+    if (me == 0) {
+      h->launches = 0;
+      TRY(launch_solve(h, K.c1, P.n, K.ex, P.n, K.done));
+      launches += h->launches;
+    } else {
+      TRY(hykkt_solve_krylov(h, K.c1, K.r3, K.ex, K.ey, 1e-12, 0, 2, 0));
+      long long nl = 0;
+      kkt_launch_count(h, &nl);   // (blocking for the HyKKT graph count; K3 on HyKKT is host-synchronous)
+      launches += nl;
+    }
+    k3_update_rows_kernel<<<grid_2d(std::max(P.m, 1), P.batch, h->sms), 256, 0, h->ls>>>(h->dp, h->Jv, K);
+    LAUNCH_CHECK();
+    k3_update_cols_kernel<<<grid_2d(P.n, P.batch, h->sms), 256, 0, h->ls>>>(h->dp, K);
+    LAUNCH_CHECK();
+    k3_decide_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, K, tol, max_refine + 1, h->status);
+    LAUNCH_CHECK();
+    launches += 3;
+  }
+  k3_finish_kernel<<<(P.batch + 127) / 128, 128, 0, h->ls>>>(P.batch, K, h->C.refine_iters);
+  LAUNCH_CHECK();
+  h->launches = launches + 1;
+  h->graph_solve_pending = false;
+  h->hy_pending = false;
   return KKT_OK;
 }
 

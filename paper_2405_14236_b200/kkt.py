@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
-           "kkt_sync_info", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
+           "kkt_sync_info", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
            "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_last_error", "kkt_destroy"]
 
 
@@ -80,6 +80,7 @@ def lib(build_if_missing: bool = True):
             "kkt_step_host": [P, P, P, P, P, P, D, D, D, P, P, I, D],
             "kkt_get_condensed": [P, I, P, P, P],
             "kkt_recover": [P, P, P, P, P, P],
+            "kkt_solve_unreduced": [P] + [P] * 4 + [P] * 6 + [P] * 6 + [I, D],
             "kkt_recover_bounds": [P, P, P, P, P, D, P, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
@@ -181,6 +182,12 @@ def kkt_sync_info(h):
          "kkt_sync_info")
     return dict(status=st.value, status_name=KKT_STATUS.get(st.value, str(st.value)),
                 fail_col=fc.value, refine_iters=it.value, cg_iters=cg.value, bwd_err=be.value)
+
+
+def kkt_solve_unreduced(h, x, s, u, v, f, d, max_refine=10, tol=0.0):
+    """f = (f1..f6), d = (dx, ds, dy, dz, du, dv) device buffers (None where a block is empty)."""
+    _chk(lib().kkt_solve_unreduced(h, _ptr(x), _ptr(s), _ptr(u), _ptr(v), *[_ptr(a) for a in f],
+                                   *[_ptr(a) for a in d], int(max_refine), float(tol)), "kkt_solve_unreduced")
 
 
 def kkt_recover(h, r2, r4, dx, dz, ds):
@@ -301,6 +308,9 @@ class KKTSolver:
             hykkt_solve_krylov(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine, krylov)
         else:
             hykkt_solve(self.h, rbar1, rbar2, dx, dy, cg_rtol, cg_maxit, max_outer_refine)
+
+    def solve_unreduced(self, x, s, u, v, f, d, max_refine=10, tol=0.0):
+        kkt_solve_unreduced(self.h, x, s, u, v, f, d, max_refine, tol)
 
     def recover(self, r2, r4, dx, dz, ds):
         kkt_recover(self.h, r2, r4, dx, dz, ds)

@@ -155,6 +155,43 @@ def bearing(nx=50, ny=50, seed=1000, Xi=1e-8, band=(0.5, 0.8), ecc=0.1, b_len=10
 
 
 # --------------------------------------------------------------------------------------
+# COPS elec (NEXT-3): the dense instance
+# --------------------------------------------------------------------------------------
+def elec(npts=400, seed=7000, Xi=1e-8):
+    """Synthetic COPS elec shape (np electrons on the unit sphere: n = 3 np,
+    m = np): the Hessian of the Coulomb energy couples every pair of points, so W (and K) is
+    fully dense ("some are fully dense (elec)").  LiftedKKT form (m_eq = 0): row i
+    of J is the gradient 2 p_i of the sphere constraint of point i (3 entries), relaxed and
+    active (D = U(0.5,2)/Xi).  The points have no bounds, so Sigma_x is tiny
+    (U(0.5,2)*Xi).  W = A A^T / n + diag(row |.| sum + 1) with A ~ N(0,1) (SPD, R17)."""
+    rng = np.random.default_rng(seed)
+    n, m = 3 * npts, npts
+    A = rng.standard_normal((n, n)) / np.sqrt(n)
+    Wd = A @ A.T
+    Wd += np.diag(np.abs(Wd).sum(1) + 1.0)
+    ii, jj = np.tril_indices(n)
+    Wp, Wc, Wv = _csr_from_coo(n, ii, jj, Wd[ii, jj])
+    pts = rng.standard_normal((npts, 3))
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    Jp = (np.arange(m + 1) * 3).astype(np.int32)
+    Jc = (3 * np.repeat(np.arange(m), 3) + np.tile(np.arange(3), m)).astype(np.int32)
+
+    def draw(rng):
+        P = rng.standard_normal((npts, 3))
+        P /= np.linalg.norm(P, axis=1, keepdims=True)
+        Jv = (2.0 * P).ravel()
+        Sx = rng.uniform(0.5, 2.0, n) * Xi
+        Ss = rng.uniform(0.5, 2.0, m) / Xi
+        return Jv, Wv, Sx, Ss, rng.standard_normal(n), None, None
+
+    Jv, _, Sx, Ss, b, _, _ = draw(rng)
+    inst = KKTInstance("elec-%d" % npts, n, m, 0, Wp, Wc, Wv, Jp, Jc, Jv, Sx, Ss, b=b,
+                       meta=dict(kind="elec", npts=npts, Xi=Xi, seed=seed))
+    inst.meta["_draw"] = draw
+    return inst
+
+
+# --------------------------------------------------------------------------------------
 # ACOPF-shaped (C2..C5)
 # --------------------------------------------------------------------------------------
 def acopf_sizes(nb):
@@ -389,6 +426,7 @@ CONFIGS = {
     "C4": "ACOPF ~78,484 buses, LiftedKKT",
     "C5": "batch of 512 x ACOPF 500 buses (same pattern)",
     "C6": "NEXT-3: COPS bearing 800x800 (n=640,000, bound-only)",
+    "C7": "NEXT-3: COPS elec 800 points, dense (n=2,400, m=800), LiftedKKT",
 }
 
 
@@ -420,4 +458,6 @@ def make_config(name: str, instance: int = 0, gamma: float = 1e7, batch: int | N
                      _pattern_rng_seed=5000, **kw)
     if name == "C6":
         return bearing(800, 800, seed=seed, **kw)
+    if name == "C7":
+        return elec(800, seed=seed, **kw)
     raise KeyError(name)

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     assert decl == set(K.EXPORTS)
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C5", "C3", "C4"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C5", "C3", "C4", "C7"])
 def test_ordering_etree_colcounts_bitexact(cfg):
     inst = make_config(cfg) if cfg != "C5" else make_config("C5", batch=1)
     S = K.KKTSolver.from_instance(inst)

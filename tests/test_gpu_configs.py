@@ -246,3 +246,84 @@ def test_hykkt_is_graph_launched_without_host_sync():
     dx2, dy2, info2, _ = run_hykkt(inst, max_outer=2, solver=S)
     assert np.array_equal(dx, dx2) and np.array_equal(dy, dy2)     # deterministic
     S.close()
+
+
+def _k3_case(n, me, mi, seed, dw=0.0, dc=0.0, gamma=0.0):
+    """Tiny IPM-like K3 system: instance pattern/values plus x, s, u, v > 0 and f blocks."""
+    from synth.generator import tiny_random
+    from oracle import dense
+    inst = tiny_random(n, mi + me, me, seed=seed, Xi=1.0, delta_w=dw, delta_c=dc,
+                       hykkt_gamma=gamma if me else 0.0)
+    rng = np.random.default_rng(seed + 100)
+    x, u = rng.uniform(0.5, 2, n), rng.uniform(0.5, 2, n)
+    s, v = rng.uniform(0.5, 2, mi), rng.uniform(0.5, 2, mi)
+    f = [rng.standard_normal(k) for k in (n, mi, me, mi, n, mi)]
+    J = dense.dense_J(inst)
+    K3 = dense.k3_matrix(dense.dense_W(inst), J[:me], J[me:], x, s, u, v)
+    dref = np.linalg.solve(K3, np.concatenate(f))
+    inst.Sigma_x = u / x
+    inst.Sigma_s = v / s
+    return inst, (x, s, u, v), f, dense.k3_split(dref, n, me, mi)
+
+
+def _run_k3(inst, xsuv, f, max_refine):
+    import torch
+    import paper_2405_14236_b200 as K
+    from kkt_gpu import dev
+    n, me, mi = inst.n, inst.m_eq, inst.m - inst.m_eq
+    S = K.KKTSolver.from_instance(inst).bind(0)
+    g = lambda a: dev(a, "cuda:0") if (a is not None and a.size) else None
+    W, J, Sx, Ss = g(inst.W_vals), g(inst.J_vals), g(inst.Sigma_x), g(inst.Sigma_s)
+    S.condense(W, J, Sx, Ss, None, inst.delta_w, inst.delta_c, inst.gamma)
+    S.factor()
+    d = [torch.zeros(max(k, 1), dtype=torch.float64, device="cuda:0") for k in (n, mi, me, mi, n, mi)]
+    dd = [t if k else None for t, k in zip(d, (n, mi, me, mi, n, mi))]
+    S.solve_unreduced(*[g(a) for a in xsuv], [g(a) for a in f], dd, max_refine)
+    info = S.sync_info()
+    out = [t.cpu().numpy()[:k] for t, k in zip(d, (n, mi, me, mi, n, mi))]
+    S.close()
+    return out, info
+
+
+@pytest.mark.parametrize("me,dw,dc,gamma", [(0, 0.0, 0.0, 0.0), (0, 1e-4, 1e-6, 0.0), (8, 0.0, 0.0, 1e4),
+                                           (8, 1e-5, 0.0, 1e3)])
+def test_unreduced_k3_refinement(me, dw, dc, gamma):
+    """NEXT-1: the direction from kkt_solve_unreduced equals the dense K3 solution
+     block by block -- including with a regularised condensed factor (delta_w, delta_c)
+    as the preconditioner, where only the K3 Richardson sweeps reach the unregularised solution."""
+    inst, xsuv, f, ref = _k3_case(36, me, 20, seed=21 + me, dw=dw, dc=dc, gamma=gamma)
+    out, info = _run_k3(inst, xsuv, f, max_refine=20)
+    assert info["status"] == 0, info
+    scale = max(np.abs(r).max() for r in ref if r.size)
+    for a, r in zip(out, ref):
+        if r.size:
+            assert np.abs(a - r).max() <= 1e-10 * scale, (np.abs(a - r).max() / scale, info)
+    if dw > 0:
+        out0, _ = _run_k3(inst, xsuv, f, max_refine=0)
+        err0 = max(np.abs(a - r).max() for a, r in zip(out0, ref) if r.size) / scale
+        assert err0 > 1e-9 and info["refine_iters"] >= 1, (err0, info)
+
+
+def test_elec_dense_parity():
+    """NEXT-3: COPS elec shape (800 points, fully dense K), a single dense
+    front factorised by the tile-task DMMA kernel, against the oracle."""
+    from kkt_gpu import run_lifted, relerr
+    inst = make_config("C7")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, (relerr(x, R["x"]), info)
+    eta, _ = oracle.backward_error(inst, R["K"], inst.b, x)
+    assert eta <= 1e-10
+    S.close()
+
+
+def test_bearing_800_parity():
+    """NEXT-3: COPS bearing_800 (n = 640,000) against the oracle."""
+    from kkt_gpu import run_lifted, relerr
+    inst = make_config("C6")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, (relerr(x, R["x"]), info)
+    S.close()

@@ -143,3 +143,31 @@ def test_generated_K_is_spd(cfg):
     inst = make_config(cfg) if cfg != "C5" else make_config("C5", batch=1)
     K = _dense_K(*oracle.condense(inst), inst.n)
     assert np.linalg.eigvalsh(K).min() > 0
+
+
+@pytest.mark.parametrize("seed,me", [(11, 0), (12, 4)])
+def test_k3_reduces_to_k2_plus_bound_recovery(seed, me):
+    """NEXT-1 oracle pin: the dense unreduced K3 solved directly equals the K2 solve
+    (delta = 0, D_x = X^-1 U, D_s = S^-1 V) followed by the bound-multiplier recovery
+    du = X^-1 (f5 - U dx), dv = S^-1 (f6 - V ds) (generalised right-hand side)."""
+    from oracle import dense
+    rng = np.random.default_rng(seed)
+    n, mi = 18, 9
+    inst = tiny_random(n, mi + me, me, seed=seed)
+    J = dense.dense_J(inst)
+    G, H = J[:me], J[me:]
+    W = dense.dense_W(inst)
+    x, u = rng.uniform(0.5, 2, n), rng.uniform(0.5, 2, n)
+    s, v = rng.uniform(0.5, 2, mi), rng.uniform(0.5, 2, mi)
+    f = [rng.standard_normal(k) for k in (n, mi, me, mi, n, mi)]
+    K3 = dense.k3_matrix(W, G, H, x, s, u, v)
+    d = np.linalg.solve(K3, np.concatenate(f))
+    dx, ds, dy, dz, du, dv = dense.k3_split(d, n, me, mi)
+    K2 = dense.k2_matrix(W, G, H, u / x, v / s, 0.0, 0.0)
+    b2 = np.concatenate([f[0] + f[4] / x, f[1] + f[5] / s, f[2], f[3]])
+    sol = np.linalg.solve(K2, b2)
+    ex, es = sol[:n], sol[n:n + mi]
+    ey, ez = sol[n + mi:n + mi + me], sol[n + mi + me:]
+    scale = np.abs(d).max()
+    for a, b in ((dx, ex), (ds, es), (dy, ey), (dz, ez), (du, (f[4] - u * ex) / x), (dv, (f[5] - v * es) / s)):
+        assert a.size == 0 or np.abs(a - b).max() <= 1e-10 * scale
