@@ -50,7 +50,8 @@ typedef enum {
 
 typedef struct {
   int ordering;          /* 0 = MD-exact-v1 (default; bit-exact contract R11), 1 = natural  */
-  int factor_kind;       /* 0 = LL^T (default, R5); 1 reserved for pivot-free LDL^T        */
+  int factor_kind;       /* 0 = LL^T (default, R5); 1 = pivot-free LDL^T with inertia (R5b):
+                            every supernode on the CTA / tile paths (no warp class)          */
   int relax_small;       /* amalgamation: merge if combined width <= relax_small (perf only) */
   int relax_big;         /* amalgamation: never merge beyond this width                     */
   double relax_zero_frac;/* amalgamation: max fraction of explicit zeros added               */
@@ -125,7 +126,10 @@ kkt_status kkt_condense(kkt_handle h, const double *W_vals, const double *J_vals
 
 /* kkt_factor -- pivot-free supernodal multifrontal Cholesky P K P^T = L L^T (P:512, P:524,
  * P:560).  A pivot <= 0 or non-finite records KKT_ERR_NOT_SPD and the failing column
- * (original index) in the device status word; the factor is then invalid.  Non-blocking. */
+ * (original index) in the device status word; the factor is then invalid.  With factor_kind = 1
+ * the pivot-free LDL^T (the paper's cuDSS choice) accepts negative pivots, counts
+ * the inertia (kkt_inertia) and fails (KKT_ERR_NONFINITE via kkt_sync_info) only on a
+ * non-finite pivot.  Non-blocking. */
 kkt_status kkt_factor(kkt_handle h);
 
 /*
@@ -194,6 +198,34 @@ kkt_status kkt_solve_unreduced(kkt_handle h, const double *x, const double *s, c
                                const double *f4, const double *f5, const double *f6, double *dx,
                                double *ds, double *dy, double *dz, double *du, double *dv,
                                int max_refine, double tol);
+
+/*
+ * kkt_inertia -- inertia of the last LDL^T factorization (factor_kind = 1; P:424-429 eq.
+ * ipm:inertia: the counts of positive / negative / zero pivots d_j equal those of the eigenvalues
+ * of K by Sylvester's law).  The factor is pivot-free LDL^T in signed-Cholesky form
+ * (K = L~ S L~^T, D = S diag(l~)^2, ldlt.cuh); a pivot with |d_j| <= 1e-14 |K_jj| counts as zero
+ * (R6) and is replaced by sign(d_j) max(1e-14 |K_jj|, 1e-300).  [host] counts[batch][3] =
+ * (positive, negative, zero).  Blocking.  KKT_ERR_STATE for factor_kind 0 or before kkt_factor.
+ */
+kkt_status kkt_inertia(kkt_handle h, int *counts);
+
+/*
+ * kkt_factor_inertia_correct -- condense + factor with the primal regularisation delta_w chosen
+ * by the inertia-correction rule of Wachter & Biegler (2006) that the paper uses (P:373-375,
+ * "delta_w is chosen dynamically using the inertia information"): try delta_w = 0;
+ * else delta_w = dw_first if dw_last = 0, else max(dw_min, k_minus dw_last); while the inertia of
+ * the condensed matrix is not (n, 0, 0) (K SPD), multiply delta_w by k_plus_bar
+ * (dw_last = 0) or k_plus, and fail (KKT_ERR_NOT_SPD) beyond dw_max.  With factor_kind = 1 the
+ * test uses the LDL^T inertia counts, with factor_kind = 0 the Cholesky breakdown (K SPD iff no
+ * pivot <= 0).  [device] value arrays as kkt_condense (one delta_w for the whole batch);
+ * [host] params[7] = {dw_min, dw_first, dw_max, k_minus, k_plus, k_plus_bar, dw_last} or NULL
+ * for {1e-20, 1e-4, 1e40, 1/3, 8, 100, 0}; out: *delta_w_out (the handle is left condensed and
+ * factored with it), *tries_out (factorizations).  Blocking (one host sync per try).
+ */
+kkt_status kkt_factor_inertia_correct(kkt_handle h, const double *W_vals, const double *J_vals,
+                                      const double *Sigma_x, const double *Sigma_s, const double *D,
+                                      double delta_c, double gamma, const double *params,
+                                      double *delta_w_out, int *tries_out);
 
 /* Block the host until the handle's stream is idle; report and clear the device status.
  * Any out pointer may be NULL.  status: a kkt_status value; fail_col: original column of

@@ -60,6 +60,9 @@ def _load():
             lib.oracle_backward_error.argtypes = [C.POINTER(OracleSystem), P, P, P, P, P, P]
             lib.oracle_cg_dense.argtypes = [C.c_int, P, P, P, C.c_double, C.c_int, P]
             lib.oracle_cr_dense.argtypes = [C.c_int, P, P, P, C.c_double, C.c_int, P, P]
+            lib.oracle_ldlt.argtypes = [C.c_int, P, P, P, P, P, P, P, P]
+            lib.oracle_ldlt_solve.argtypes = [C.c_int, P, P, P, P, P, P]
+            lib.oracle_ldlt_solve.restype = None
             lib.oracle_hykkt.argtypes = [C.POINTER(OracleSystem), P, P, P, P, P, P, P, P,
                                          C.c_double, C.c_int, C.c_int, P, P]
             _lib = lib
@@ -189,6 +192,57 @@ def cg_dense(A, b, rtol=1e-12, maxit=1000):
     it = C.c_int(0)
     st = lib.oracle_cg_dense(n, _p(A), _p(_f64(b)), _p(x), float(rtol), int(maxit), C.byref(it))
     return x[:n], st, it.value
+
+
+def ldlt(n, Kp, Ki, Kv, perm, Lp, Li):
+    """Pivot-free LDL^T on the symbolic pattern (unit L below the diagonal slots, d_j in them).
+    Returns (Lx, inertia (pos, neg, zero), first non-finite pivot or -1)."""
+    lib = _load()
+    Lx = np.zeros(max(int(Lp[n]), 1))
+    inert = np.zeros(3, np.int32)
+    fail = lib.oracle_ldlt(n, _p(_i32(Kp)), _p(_i32(Ki)), _p(_f64(Kv)), _p(_i32(perm)), _p(_i32(Lp)),
+                           _p(_i32(Li)), _p(Lx), _p(inert))
+    return Lx, tuple(int(v) for v in inert), fail
+
+
+def ldlt_solve(n, Lp, Li, Lx, perm, b):
+    lib = _load()
+    x = np.zeros(max(n, 1))
+    lib.oracle_ldlt_solve(n, _p(_i32(Lp)), _p(_i32(Li)), _p(_f64(Lx)), _p(_i32(perm)), _p(_f64(b)), _p(x))
+    return x[:n]
+
+
+def inertia_correct(inst, params=None):
+    """Wachter-Biegler primal inertia correction with the oracle LDL^T:
+    the delta_w sequence of kkt_factor_inertia_correct.  Returns (delta_w, tries, inertia)."""
+    import copy
+    dw_min, dw_first, dw_max, k_minus, k_plus, k_plus_bar, dw_last = (
+        params if params is not None else (1e-20, 1e-4, 1e40, 1.0 / 3.0, 8.0, 100.0, 0.0))
+    base = condense(inst)
+    perm = md_order(inst.n, base[0], base[1])
+    _, _, Lp, Li = symbolic(inst.n, base[0], base[1], perm, want_pattern=True)
+
+    def inertia_at(dw):
+        it = copy.copy(inst)
+        it.delta_w = dw
+        K = condense(it)
+        _, inert, fail = ldlt(inst.n, K[0], K[1], K[2], perm, Lp, Li)
+        return inert, fail
+
+    tries = 1
+    inert, fail = inertia_at(0.0)
+    ok = lambda t, f: f < 0 and t == (inst.n, 0, 0)
+    if ok(inert, fail):
+        return 0.0, tries, inert
+    dw = dw_first if dw_last == 0.0 else max(dw_min, k_minus * dw_last)
+    while True:
+        inert, fail = inertia_at(dw)
+        tries += 1
+        if ok(inert, fail):
+            return dw, tries, inert
+        dw = k_plus_bar * dw if dw_last == 0.0 else k_plus * dw
+        if dw > dw_max:
+            return dw, tries, None
 
 
 def cr_dense(A, b, rtol=1e-12, maxit=1000):

@@ -22,6 +22,9 @@
  *   oracle_hykkt         HyKKT steps 1-3 + __float128 outer refinement on the
  *                        saddle system [K G^T; G 0] -> (dx_ref, dy_ref)
  *   oracle_cg            Hestenes-Stiefel CG (stopping rule R10)
+ *   oracle_cr            Hestenes-Stiefel conjugate residuals (same stop rule)
+ *   oracle_ldlt          pivot-free LDL^T of P K P^T with inertia counts (P:424-429,
+ *                        P:1345-1346; zero-pivot rule R6)    + oracle_ldlt_solve
  *
  * Parity pins for each function live in tests/test_oracle_*.py (-m "not gpu").
  */
@@ -362,6 +365,86 @@ int oracle_cholesky(int n, const int *Kp, const int *Ki, const double *Kv, const
   }
   free(iperm); free(Ap); free(fill); free(Ai); free(Ax); free(rp); free(rk); free(rpos); free(x);
   return fail;
+}
+
+/* Pivot-free LDL^T (NEXT-2; P:424-429 inertia, P:1345-1346 the paper's GPU LDL^T) of P K P^T on
+ * the symbolic pattern (Lp, Li): left-looking columns, unit-lower L stored below the diagonal slot,
+ * d_j in the diagonal slot.  d_j = a_jj - sum_k l_jk^2 d_k ; l_ij = (a_ij - sum_k l_ik d_k l_jk) / d_j.
+ * Zero-pivot rule (R6): |d_j| <= 1e-14 |K_jj| counts as zero and d_j is replaced by
+ * sign(d_j) max(1e-14 |K_jj|, 1e-300) (sign(0) = +).  inertia[3] = (positive, negative, zero).
+ * Returns the first non-finite pivot column or -1. */
+int oracle_ldlt(int n, const int *Kp, const int *Ki, const double *Kv, const int *perm,
+                const int *Lp, const int *Li, double *Lx, int *inertia) {
+  int *iperm = malloc(sizeof(int) * (n > 0 ? n : 1));
+  for (int k = 0; k < n; k++) iperm[perm[k]] = k;
+  int *Ap = calloc(n + 1, sizeof(int));
+  for (int j = 0; j < n; j++)
+    for (int p = Kp[j]; p < Kp[j + 1]; p++) {
+      int a = iperm[Ki[p]], b = iperm[j];
+      Ap[(a < b ? a : b) + 1]++;
+    }
+  for (int j = 0; j < n; j++) Ap[j + 1] += Ap[j];
+  int *fill = malloc(sizeof(int) * (n + 1)); memcpy(fill, Ap, sizeof(int) * (n + 1));
+  int *Ai = malloc(sizeof(int) * (Ap[n] + 1)); double *Ax = malloc(sizeof(double) * (Ap[n] + 1));
+  double *Kd = calloc(n > 0 ? n : 1, sizeof(double));   /* K_jj in the permuted order */
+  for (int j = 0; j < n; j++)
+    for (int p = Kp[j]; p < Kp[j + 1]; p++) {
+      int a = iperm[Ki[p]], b = iperm[j];
+      int c = a < b ? a : b, r = a < b ? b : a;
+      Ai[fill[c]] = r; Ax[fill[c]] = Kv[p]; fill[c]++;
+      if (a == b) Kd[a] = Kv[p];
+    }
+  int nnzL = Lp[n];
+  int *rp = calloc(n + 1, sizeof(int));
+  for (int k = 0; k < n; k++)
+    for (int p = Lp[k] + 1; p < Lp[k + 1]; p++) rp[Li[p] + 1]++;
+  for (int i = 0; i < n; i++) rp[i + 1] += rp[i];
+  int *rk = malloc(sizeof(int) * (nnzL + 1)), *rpos = malloc(sizeof(int) * (nnzL + 1));
+  memcpy(fill, rp, sizeof(int) * (n + 1));
+  for (int k = 0; k < n; k++)
+    for (int p = Lp[k] + 1; p < Lp[k + 1]; p++) {
+      int i = Li[p];
+      rk[fill[i]] = k; rpos[fill[i]] = p; fill[i]++;
+    }
+  double *x = calloc(n > 0 ? n : 1, sizeof(double));
+  int fail = -1;
+  inertia[0] = inertia[1] = inertia[2] = 0;
+  for (int j = 0; j < n; j++) {
+    for (int p = Lp[j]; p < Lp[j + 1]; p++) x[Li[p]] = 0.0;
+    for (int p = Ap[j]; p < Ap[j + 1]; p++) x[Ai[p]] += Ax[p];
+    for (int t = rp[j]; t < rp[j + 1]; t++) {                /* columns k with L_jk != 0 */
+      int k = rk[t], p0 = rpos[t];
+      double w = Lx[p0] * Lx[Lp[k]];                          /* l_jk d_k */
+      for (int p = p0; p < Lp[k + 1]; p++) x[Li[p]] -= Lx[p] * w;
+    }
+    double d = x[j];
+    if (!isfinite(d)) { if (fail < 0) fail = j; }
+    double thr = 1e-14 * fabs(Kd[j]);
+    if (!(fabs(d) > thr)) {
+      inertia[2]++;
+      double mag = thr > 1e-300 ? thr : 1e-300;
+      d = (d < 0) ? -mag : mag;
+    } else if (d > 0) inertia[0]++;
+    else inertia[1]++;
+    Lx[Lp[j]] = d;
+    for (int p = Lp[j] + 1; p < Lp[j + 1]; p++) Lx[p] = x[Li[p]] / d;
+  }
+  free(iperm); free(Ap); free(fill); free(Ai); free(Ax); free(Kd); free(rp); free(rk); free(rpos); free(x);
+  return fail;
+}
+
+/* L D L^T x = P b with the factor of oracle_ldlt (fp64) */
+void oracle_ldlt_solve(int n, const int *Lp, const int *Li, const double *Lx, const int *perm,
+                       const double *b, double *x) {
+  double *y = malloc(sizeof(double) * (n > 0 ? n : 1));
+  for (int k = 0; k < n; k++) y[k] = b[perm[k]];
+  for (int j = 0; j < n; j++)
+    for (int p = Lp[j] + 1; p < Lp[j + 1]; p++) y[Li[p]] -= Lx[p] * y[j];
+  for (int j = 0; j < n; j++) y[j] /= Lx[Lp[j]];
+  for (int j = n - 1; j >= 0; j--)
+    for (int p = Lp[j] + 1; p < Lp[j + 1]; p++) y[j] -= Lx[p] * y[Li[p]];
+  for (int k = 0; k < n; k++) x[perm[k]] = y[k];
+  free(y);
 }
 
 /* L y = P b ; L^T z = y ; x = P^T z   (fp64) */

@@ -211,6 +211,7 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
   *code = 2;
   P = Plan();
   P.n = n; P.m = m; P.m_eq = m_eq; P.batch = std::max(1, opt.batch);
+  P.factor_kind = opt.factor_kind;
   P.nnzW = Wp[n];
   P.nnzJ = m ? Jp[m] : 0;
   if (Wp[0] != 0 || (m && Jp[0] != 0)) return "rowptr[0] != 0";
@@ -548,6 +549,7 @@ std::string analyze(int n, int m, int m_eq, const int* Wp, const int* Wc, const 
     // KKT_SCLASS=<doubles> overrides it (tuning hook)
     long long sclass = KKT_SCAP;
     if (const char* e = getenv("KKT_SCLASS")) sclass = std::min<long long>(KKT_SCAP, std::max(0LL, atoll(e)));
+    if (opt.factor_kind == 1) sclass = -1;  // LDL^T: no warp class (every supernode on a signed CTA / tile path)
     for (int s = 0; s < ns; s++) {
       long long r = P.sn_rp[s + 1] - P.sn_rp[s], w = snf[s + 1] - snf[s], R = r - w;
       long long need = r * w + (P.sn_parent[s] >= 0 ? R * (R + 1) / 2 : 0);

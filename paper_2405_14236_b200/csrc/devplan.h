@@ -51,6 +51,9 @@ struct DevPlan {
   long long linv_doubles;
   const int *Wf_p, *Wf_c, *Wf_k, *Jt_p, *Jt_r, *Jt_k, *Gt_end;
   const int *Jrp, *Jci;       // J CSR pattern (caller's, copied at analysis)
+  int ldlt;                   // factor_kind 1: signed Cholesky K = L~ S L~^T (ldlt.cuh)
+  double* Sg;                 // [batch][n] pivot signs s_j (internal numbering), LDL^T only
+  int* inert;                 // [batch][3] (positive, negative, zero) pivot counts, LDL^T only
 };
 
 // Device status words (one per batch instance where noted).

@@ -14,6 +14,7 @@
 //   when it fits, otherwise in global memory (L2) with a 64x64 register-tiled SYRK.
 #pragma once
 #include "dense.cuh"
+#include "ldlt.cuh"
 
 namespace kkt {
 
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(KKT_WPB * 32, MINB) factor_small_kernel(DevPla
 // =====================================================================================
 // Phase 2: one CTA per big supernode (continuation scheduling, see above).
 // =====================================================================================
+template <bool SG>
 __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const double* __restrict__ Kv_all,
                                                              double* Lx_all, double* U_all, double* Dv_all,
                                                              int* cnt_all, int* ctl, int* fail_all,
@@ -225,7 +227,9 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
       double* dv = Dv_all + (long long)b * P.n + I.f0;
       // left-looking 32-column blocks for medium/large fronts in shared memory (one U update,
       // three barriers per block); narrow short fronts keep the 8-column right-looking kernel
-      if (in_smem && (w >= 20 || r >= 128)) front_factor_cta_ll(F, U, r, w, dv, &s_fail);
+      if (SG) front_factor_cta_ldlt(F, U, r, w, dv, &s_fail, P.Sg + (long long)b * P.n + I.f0, Kv, P.Kp, I.f0,
+                                    P.inert + 3 * b);
+      else if (in_smem && (w >= 20 || r >= 128)) front_factor_cta_ll(F, U, r, w, dv, &s_fail);
       else front_factor_cta<8>(F, U, r, w, dv, &s_fail);
       __syncthreads();
       if (tid == 0) trace_stamp(P, 0, s, b, 3);

@@ -78,6 +78,9 @@ struct kkt_plan {
   double *cr = nullptr, *cp = nullptr, *cq = nullptr, *hdy = nullptr, *hr2 = nullptr;
   double *cs = nullptr;                                    // CR: s = S r
   K3Ctx k3{};                                              // unreduced-system refinement (k3.cuh)
+  double* Sg = nullptr;   // LDL^T pivot signs [B][n]
+  int* inert = nullptr;   // LDL^T inertia counts [B][3]
+  bool ldlt = false;
   double *g_r1 = nullptr, *g_r2 = nullptr, *g_dx = nullptr, *g_dy = nullptr;  // HyKKT graph I/O
   cudaGraphExec_t hy_exec = nullptr;                       // recorded HyKKT solve
   double hy_rtol = -1, hy_gamma = 0, hy_dw = 0;
@@ -221,6 +224,8 @@ static void carve_workspace(kkt_plan* h, Carver& c) {
   h->C.oprev = c.take<double>(B);
   h->C.opass = c.take<int>(B);
   h->C.cg_runs = c.take<int>(1);
+  h->Sg = c.take<double>(P.factor_kind == 1 ? B * n : 1);
+  h->inert = c.take<int>(3 * B);
   h->cs = c.take<double>(B * me);
   {  // K3 refinement scratch (k3.cuh)
     const size_t mi = m - me;
@@ -262,7 +267,7 @@ kkt_status kkt_analyze(int n, int m, int m_eq, const int* W_rowptr, const int* W
   kkt_options o;
   kkt_default_options(&o);
   if (opt) o = *opt;
-  if (o.factor_kind != 0) { g_err = "factor_kind 1 (LDL^T) not available"; return KKT_ERR_ARG; }
+  if (o.factor_kind != 0 && o.factor_kind != 1) { g_err = "factor_kind must be 0 (LL^T) or 1 (LDL^T)"; return KKT_ERR_ARG; }
   if (o.batch < 1) { g_err = "batch < 1"; return KKT_ERR_ARG; }
   kkt_plan* h = new (std::nothrow) kkt_plan();
   if (!h) return KKT_ERR_ALLOC;
@@ -272,6 +277,7 @@ kkt_status kkt_analyze(int n, int m, int m_eq, const int* W_rowptr, const int* W
   op.relax_big = o.relax_big;
   op.relax_zero_frac = o.relax_zero_frac;
   op.batch = o.batch;
+  op.factor_kind = o.factor_kind;
   int code = 0;
   std::string err;
   try {
@@ -552,6 +558,7 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
     for (int s_ : P.order_h) maxr_h = std::max(maxr_h, P.sn_rp[s_ + 1] - P.sn_rp[s_]);
     h->huge_solve_cta = maxr_h <= 512;
     if (const char* e = getenv("KKT_HUGE_SOLVE")) h->huge_solve_cta = atoi(e) == 0;
+    if (P.factor_kind == 1) h->huge_solve_cta = true;  // LDL^T: S applied between the CTA-path sweeps
   }
   {  // big-children counts (bottom-up hand-off into CTA parents)
     std::vector<int> nbig(std::max(P.ns, 1), 0);
@@ -591,6 +598,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   h->ws_bytes = need;
   Carver c{(char*)h->ws, 0, false};
   carve_workspace(h, c);
+  h->ldlt = (P.factor_kind == 1);
+  for (DevPlan* dq : {&h->dp, &h->dps}) { dq->ldlt = h->ldlt; dq->Sg = h->Sg; dq->inert = h->inert; }
   CUDA_TRY(cudaMemsetAsync(h->ws, 0, need, h->stream));
   int big = INT_MAX;
   CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
@@ -625,7 +634,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   // occupancy-capped variant, latency-bound ones (C1, C2, C3) the spill-free one (measured)
   h->fsmall_occ = ((long long)P.order_s.size() * P.batch >= 50000) ? 3 : 1;
   if (const char* e = getenv("KKT_FSMALL_OCC")) h->fsmall_occ = atoi(e) == 3 ? 3 : 1;
-  CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
+  CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
+  CUDA_TRY(cudaFuncSetAttribute(factor_big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fbig_smem));
   CUDA_TRY(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
   CUDA_TRY(cudaFuncSetAttribute(bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tsmall_smem));
   CUDA_TRY(cudaFuncSetAttribute(fwd_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->tbig_smem));
@@ -641,7 +651,7 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   const long long ts = (long long)P.order_s.size() * P.batch, tb = (long long)P.order_b.size() * P.batch;
   if (h->fsmall_occ == 3) CUDA_TRY(grid_of(factor_small_kernel<3>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
   else CUDA_TRY(grid_of(factor_small_kernel<1>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
-  CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
+  CUDA_TRY(grid_of(factor_big_kernel<false>, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
   CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem,
                    (long long)(h->huge_solve_cta ? P.up_b.size() : P.up_bf.size()) * P.batch, 1, &h->g_tbig));
@@ -668,7 +678,7 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   }
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
-    CUDA_TRY(grid_of(factor_big_kernel, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
+    CUDA_TRY(grid_of(factor_big_kernel<false>, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
     h->huge_warps = HUGE_WARPS;
     if (const char* e = getenv("KKT_HUGE_WARPS")) h->huge_warps = std::min(8, std::max(1, atoi(e)));
     h->huge_smem = HUGE_SMEM_DOUBLES_PER_WARP * 8 * h->huge_warps;
@@ -687,15 +697,19 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
     }
     h->tiles = !(getenv("KKT_HUGE_OLD") && atoi(getenv("KKT_HUGE_OLD")) > 0);
     if (!P.order_h.empty() && h->tiles) {
-      CUDA_TRY(cudaFuncSetAttribute(tile_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
-      int occ_t = 0;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, tile_factor_kernel, TILE_THREADS, TILE_SMEM_BYTES));
+      CUDA_TRY(cudaFuncSetAttribute(tile_factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
+      CUDA_TRY(cudaFuncSetAttribute(tile_factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
+      int occ_t = 0, occ_t2 = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, tile_factor_kernel<false>, TILE_THREADS, TILE_SMEM_BYTES));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t2, tile_factor_kernel<true>, TILE_THREADS, TILE_SMEM_BYTES));
+      occ_t = std::min(occ_t, occ_t2);
       if (occ_t < 1) { g_err = "tile_factor_kernel does not fit on an SM"; return KKT_ERR_CUDA; }
       h->g_tile = occ_t * h->sms;
       TilePlanHost tph;
       build_tile_plan(P, h->g_tile, tph);
       h->tile_est_us = tph.est_us;
       if (!tph.ok) h->tiles = false;  // fall back to the level kernel (huge.cuh)
+      if (!h->tiles && P.factor_kind == 1) { g_err = "LDL^T needs the tile-task path for the large fronts"; return KKT_ERR_ARG; }
     }
     if (!P.order_h.empty() && h->tiles) {
       TilePlanHost tph;
@@ -820,6 +834,7 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
   const Plan& P = h->P;
   const bool ev = h->ls == h->stream;  // not while recording a graph
   if (ev) CUDA_TRY(cudaEventRecord(h->fev[0], h->ls));
+  if (h->ldlt) CUDA_TRY(cudaMemsetAsync(h->inert, 0, 3 * sizeof(int) * P.batch, h->ls));
   if (!P.order_s.empty()) {
     if (h->fsmall_occ == 3)
       factor_small_kernel<3><<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
@@ -831,7 +846,7 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     h->launches++;
   }
   if (!P.up_bf.empty()) {
-    CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 1) && !P.order_s.empty(), factor_big_kernel, h->g_fbig, KKT_BNT, h->fbig_smem, h->ls,
+    CUDA_TRY(launch_pdl(h->pdl && (h->pdl_mask & 1) && !P.order_s.empty(), h->ldlt ? factor_big_kernel<true> : factor_big_kernel<false>, h->g_fbig, KKT_BNT, h->fbig_smem, h->ls,
                         h->dp, (const double*)h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 1 * KKT_CTL, h->fail,
                         (long long)h->factor_smem_cap));
     h->launches++;
@@ -851,7 +866,8 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
     const double* ub = h->Ub;
     int* fail = h->fail;
     void* args[] = {&dp, &tp, &kv, &lx, &ub, &dv, &fail};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_factor_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
+    CUDA_TRY(cudaLaunchCooperativeKernel(h->ldlt ? (const void*)tile_factor_kernel<true> : (const void*)tile_factor_kernel<false>,
+                                         dim3(h->g_tile), dim3(TILE_THREADS), args,
                                          (size_t)TILE_SMEM_BYTES, h->ls));
     h->launches++;
   } else if (!P.order_h.empty()) {
@@ -912,6 +928,11 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
       void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs};
       CUDA_TRY(cudaLaunchCooperativeKernel((const void*)solve_huge_kernel, dim3(h->g_hsolve), dim3(256), args, 0,
                                            h->ls));
+      h->launches++;
+    }
+    if (h->ldlt) {  // K^-1 = L~^-T S L~^-1: y <- S y before the backward sweep
+      ldlt_sign_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>((long long)P.batch * P.n, h->Y, h->Sg);
+      LAUNCH_CHECK();
       h->launches++;
     }
     if (cta_huge || P.order_b.size() > P.order_h.size()) {
@@ -1488,12 +1509,74 @@ extern "C" kkt_status kkt_sync_info(kkt_handle h, int* status, int* fail_col, in
   CUDA_TRY(cudaMemcpyAsync(h->status, &zero, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(cudaMemcpyAsync(h->fail, &big, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
-  if (fl != INT_MAX && st == 0) st = KKT_ERR_NOT_SPD;
+  if (fl != INT_MAX && st == 0) st = h->ldlt ? KKT_ERR_NONFINITE : KKT_ERR_NOT_SPD;
   if (status) *status = st;
   if (fail_col) *fail_col = (fl != INT_MAX) ? P.perm[fl] : -1;
   if (refine_iters) *refine_iters = *std::max_element(it.begin(), it.end());
   if (cg_iters) *cg_iters = *std::max_element(cg.begin(), cg.end());
   if (bwd_err) *bwd_err = *std::max_element(om.begin(), om.end());
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_inertia(kkt_handle h, int* counts) {
+  if (!h || !counts) return KKT_ERR_ARG;
+  if (!h->ldlt) { g_err = "kkt_inertia needs factor_kind = 1 (LDL^T)"; return KKT_ERR_STATE; }
+  if (!h->factored) { g_err = "kkt_factor first"; return KKT_ERR_STATE; }
+  CUDA_TRY(cudaMemcpyAsync(counts, h->inert, 3 * sizeof(int) * h->P.batch, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_factor_inertia_correct(kkt_handle h, const double* W_vals, const double* J_vals,
+                                                 const double* Sigma_x, const double* Sigma_s, const double* D,
+                                                 double delta_c, double gamma, const double* params,
+                                                 double* delta_w_out, int* tries_out) {
+  if (!h || !delta_w_out) return KKT_ERR_ARG;
+  if (!h->bound) { g_err = "kkt_bind first"; return KKT_ERR_STATE; }
+  // Wachter & Biegler (2006) inertia correction, primal part: defaults of IPOPT
+  double dw_min = 1e-20, dw_first = 1e-4, dw_max = 1e40, k_minus = 1.0 / 3.0, k_plus = 8.0, k_plus_bar = 100.0;
+  double dw_last = 0.0;
+  if (params) {
+    dw_min = params[0]; dw_first = params[1]; dw_max = params[2];
+    k_minus = params[3]; k_plus = params[4]; k_plus_bar = params[5]; dw_last = params[6];
+  }
+  const Plan& P = h->P;
+  std::vector<int> cnt(3 * P.batch);
+  auto correct = [&](bool* ok) -> kkt_status {  // target inertia of the condensed matrix: (n, 0, 0)
+    int st = 0, fc = -1;
+    TRY(kkt_sync_info(h, &st, &fc, nullptr, nullptr, nullptr));
+    if (h->ldlt) {
+      TRY(kkt_inertia(h, cnt.data()));
+      bool good = (st == 0);
+      for (int b = 0; b < P.batch; b++) good = good && cnt[3 * b] == P.n && cnt[3 * b + 1] == 0 && cnt[3 * b + 2] == 0;
+      *ok = good;
+    } else {
+      if (st != 0 && st != KKT_ERR_NOT_SPD) return (kkt_status)st;
+      *ok = (st == 0);   // LL^T: K is SPD iff no pivot failed
+    }
+    return KKT_OK;
+  };
+  int tries = 0;
+  double dw = 0.0;
+  bool ok = false;
+  TRY(kkt_condense(h, W_vals, J_vals, Sigma_x, Sigma_s, D, 0.0, delta_c, gamma));  // IC-1: delta_w = 0
+  TRY(kkt_factor(h));
+  tries++;
+  TRY(correct(&ok));
+  if (!ok) {
+    dw = (dw_last == 0.0) ? dw_first : std::max(dw_min, k_minus * dw_last);       // IC-3
+    for (;;) {
+      TRY(kkt_condense(h, W_vals, J_vals, Sigma_x, Sigma_s, D, dw, delta_c, gamma));  // IC-4
+      TRY(kkt_factor(h));
+      tries++;
+      TRY(correct(&ok));
+      if (ok) break;
+      dw = (dw_last == 0.0) ? k_plus_bar * dw : k_plus * dw;                         // IC-5
+      if (dw > dw_max) { *delta_w_out = dw; if (tries_out) *tries_out = tries; g_err = "inertia correction: delta_w > max"; return KKT_ERR_NOT_SPD; }
+    }
+  }
+  *delta_w_out = dw;
+  if (tries_out) *tries_out = tries;
   return KKT_OK;
 }
 

@@ -76,11 +76,13 @@ struct Plan {
   long long nnzL = 0, nnzL_stored = 0, nprod = 0, update_doubles = 0, uvec_doubles = 0, linv_doubles = 0;
   double flops = 0.0, analyze_ms = 0.0, order_ms = 0.0;
   double flops_huge = 0.0;   // sum over huge supernodes of sum_t (r - t)^2, t < w (stored structure)
+  int factor_kind = 0;       // 0 LL^T, 1 pivot-free LDL^T (signed Cholesky, ldlt.cuh)
   int n_huge = 0;
 };
 
 struct Options {
   int ordering = 0;
+  int factor_kind = 0;   // 1: LDL^T (every supernode on the CTA / tile paths, ldlt.cuh)
   int relax_small = 4;
   int relax_big = 64;
   double relax_zero_frac = 0.05;

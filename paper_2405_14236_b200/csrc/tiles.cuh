@@ -27,6 +27,7 @@
 // column-major) that the triangular solves read.
 #pragma once
 #include "dense.cuh"
+#include "ldlt.cuh"
 
 namespace kkt {
 
@@ -35,7 +36,7 @@ constexpr int TBD = TBS * TBS;     // doubles per tile
 constexpr int TASK_ASM = 0, TASK_POTRF0 = 1, TASK_TRSM = 2, TASK_CRIT = 3, TASK_UPD = 4;
 constexpr int TILE_THREADS = 256;
 // shared memory of tile_factor_kernel: three swizzled tiles + 64 inverse pivots + scratch
-constexpr int TILE_SMEM_BYTES = (3 * TBD + 64 + 32 * 32) * 8 + 64;
+constexpr int TILE_SMEM_BYTES = (3 * TBD + 64 + 32 * 32 + 64) * 8 + 64;  // + 64 pivot signs (LDL^T)
 
 // One huge front (device view).
 struct alignas(16) TFront {
@@ -126,7 +127,8 @@ __device__ __forceinline__ void tile_to_panel(const TFront& F, const double* s, 
 // C (64 x 64, in global memory) -= A B^T with A, B swizzled 64 x 64 tiles in shared memory;
 // warp w owns rows 16 (w >> 1) .. +16, columns 32 (w & 1) .. +32 (2 x 4 DMMA blocks).  The
 // read-modify-write of C is issued before the k-loop so its latency hides under the MMAs.
-__device__ __forceinline__ void tile_gemm_nt_global(double* C, const double* A, const double* B) {
+template <bool SG = false>
+__device__ __forceinline__ void tile_gemm_nt_global(double* C, const double* A, const double* B, const double* ssg = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
   const int rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   double acc[2][4][2], cv[2][4][2];
@@ -144,7 +146,7 @@ __device__ __forceinline__ void tile_gemm_nt_global(double* C, const double* A, 
     const int kk = 4 * ks + lc;
     double a[2], b[4];
 #pragma unroll
-    for (int m = 0; m < 2; m++) a[m] = A[tsw(rb + 8 * m + lr, kk)];
+    for (int m = 0; m < 2; m++) a[m] = SG ? A[tsw(rb + 8 * m + lr, kk)] * ssg[kk] : A[tsw(rb + 8 * m + lr, kk)];
 #pragma unroll
     for (int n = 0; n < 4; n++) b[n] = B[tsw(cb + 8 * n + lr, kk)];
 #pragma unroll
@@ -164,7 +166,8 @@ __device__ __forceinline__ void tile_gemm_nt_global(double* C, const double* A, 
 }
 
 // Same product into a swizzled shared-memory C (the diagonal update inside CRIT).
-__device__ __forceinline__ void tile_gemm_nt_smem(double* C, const double* A, const double* B) {
+template <bool SG = false>
+__device__ __forceinline__ void tile_gemm_nt_smem(double* C, const double* A, const double* B, const double* ssg = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
   const int rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   double acc[2][4][2];
@@ -177,7 +180,7 @@ __device__ __forceinline__ void tile_gemm_nt_smem(double* C, const double* A, co
     const int kk = 4 * ks + lc;
     double a[2], b[4];
 #pragma unroll
-    for (int m = 0; m < 2; m++) a[m] = A[tsw(rb + 8 * m + lr, kk)];
+    for (int m = 0; m < 2; m++) a[m] = SG ? A[tsw(rb + 8 * m + lr, kk)] * ssg[kk] : A[tsw(rb + 8 * m + lr, kk)];
 #pragma unroll
     for (int n = 0; n < 4; n++) b[n] = B[tsw(cb + 8 * n + lr, kk)];
 #pragma unroll
@@ -275,7 +278,9 @@ __device__ __forceinline__ void tile_rowsolve32(double* X, int xrow0, int nrows,
 
 // X(rows, c1:c1+32) -= X(rows, c0:c0+32) L(c1:c1+32, c0:c0+32)^T for rows [xrow0, xrow0+nr), nr in
 // {32, 64}; all threads, DMMA (8 warps: 8-row strips x 32 columns, nr / 8 strips).
-__device__ __forceinline__ void tile_block_update(double* X, int xrow0, int nr, const double* L, int c0, int c1) {
+template <bool SG = false>
+__device__ __forceinline__ void tile_block_update(double* X, int xrow0, int nr, const double* L, int c0, int c1,
+                                                  const double* ssg = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
   const int nstrip = nr >> 3;
   for (int st = warp; st < nstrip; st += 8) {
@@ -286,7 +291,7 @@ __device__ __forceinline__ void tile_block_update(double* X, int xrow0, int nr, 
 #pragma unroll
     for (int ks = 0; ks < 8; ks++) {
       const int kk = c0 + 4 * ks + lc;
-      const double a = X[tsw(rb + lr, kk)];
+      const double a = SG ? X[tsw(rb + lr, kk)] * ssg[kk] : X[tsw(rb + lr, kk)];
 #pragma unroll
       for (int n = 0; n < 4; n++) dmma_nv(acc[n][0], acc[n][1], a, L[tsw(c1 + 8 * n + lr, kk)]);
     }
@@ -299,17 +304,105 @@ __device__ __forceinline__ void tile_block_update(double* X, int xrow0, int nr, 
 
 // L_ik = A_ik L_kk^-T for a whole 64 x 64 tile X (swizzled, in place): 32-column halves with a
 // DMMA update between them.  L: the final diagonal tile (k, k); sinv: its 64 inverse pivots.
-__device__ __forceinline__ void tile_trsm64(double* X, const double* L, const double* sinv) {
+// LDL^T (SG): the unsigned row solve gives Y = A L~^-T; the signed factor is L~_ik = Y S_k.
+template <bool SG = false>
+__device__ __forceinline__ void tile_trsm64(double* X, const double* L, const double* sinv, const double* ssg = nullptr) {
   tile_rowsolve32<0>(X, 0, 64, L, sinv);
   __syncthreads();
   tile_block_update(X, 0, 64, L, 0, 32);
   __syncthreads();
   tile_rowsolve32<32>(X, 0, 64, L, sinv);
   __syncthreads();
+  if (SG) {
+    for (int q = threadIdx.x; q < TBD; q += TILE_THREADS) {
+      const int col = q >> 6, row = q & 63;
+      X[tsw(row, col)] *= ssg[col];
+    }
+    __syncthreads();
+  }
+}
+
+// Signed (LDL^T) Cholesky of a 32 x 32 diagonal block of a swizzled tile (ldlt.cuh rules): one
+// warp, lane = row, not pipelined (the LL^T path keeps the pipelined tile_diag32).
+template <int c0>
+__device__ __forceinline__ void tile_diag32_signed(double* T, int kb, int lane, double* dinv, double* sinv, double* ssg,
+                                                   double* L11s, int* fail_k, double* sg_out, double kjj_lane,
+                                                   int* cnt3) {
+  const int row = c0 + lane;
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; c++)
+    a[c] = (lane < kb && c < kb && c <= lane) ? T[tsw(row, c0 + c)] : (c == lane ? 1.0 : 0.0);
+  double myinv = 0.0, mys = 1.0;
+  unsigned bad = 0;
+  int npos = 0, nneg = 0, nzero = 0;
+#pragma unroll
+  for (int c = 0; c < 32; c++) {
+    const double d = shfl_idx_d(a[c], c);
+    const double kjj = shfl_idx_d(kjj_lane, c);
+    double sgn;
+    bool zero, b_;
+    const double ad = ldlt_pivot(d, kjj, sgn, zero, b_);
+    if (c < kb) {
+      bad |= (b_ ? 1u : 0u) << c;
+      if (zero) nzero++; else if (sgn > 0) npos++; else nneg++;
+    }
+    const double inv = 1.0 / sqrt(ad);
+    if (lane == c) { myinv = inv; mys = sgn; }
+    const double l = (lane > c) ? a[c] * inv * sgn : (lane == c ? ad * inv : 0.0);
+    a[c] = l;
+    L11s[c * 32 + lane] = l;
+    warp_bar();
+    const double ls = l * sgn;
+#pragma unroll
+    for (int cc = c + 1; cc < 32; cc++) a[cc] = fma(-ls, L11s[c * 32 + cc], a[cc]);
+    asm volatile("" ::: "memory");
+  }
+#pragma unroll
+  for (int c = 0; c < 32; c++)
+    if (c < kb) T[tsw(row, c0 + c)] = (lane < kb && c <= lane) ? a[c] : 0.0;
+  if (lane < kb) { sinv[c0 + lane] = myinv; ssg[c0 + lane] = mys; dinv[c0 + lane] = myinv; sg_out[c0 + lane] = mys; }
+  else { sinv[c0 + lane] = 0.0; ssg[c0 + lane] = 1.0; }
+  bad &= (kb < 32) ? ((1u << kb) - 1u) : 0xffffffffu;
+  if (lane == 0) {
+    if (bad && *fail_k < 0) *fail_k = c0 + __ffs(bad) - 1;
+    if (npos) atomicAdd(cnt3, npos);
+    if (nneg) atomicAdd(cnt3 + 1, nneg);
+    if (nzero) atomicAdd(cnt3 + 2, nzero);
+  }
+  warp_bar();
 }
 
 // Cholesky of a 64 x 64 diagonal tile T (swizzled, in place) with kb valid columns:
 // chol(T00) -> T10 L00^-T -> T11 -= L10 L10^T -> chol(T11).  sinv[64] in shared memory.
+// LDL^T variant: signed diagonal blocks, L~10 = Y10 S0 before the signed block update.
+__device__ __forceinline__ void tile_potrf64_signed(double* T, int kb, double* dinv, double* sinv, double* L11s,
+                                                    int* fail_k, double* ssg, double* sg_out, const double* kjj,
+                                                    int* cnt3) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kb0 = min(kb, 32), kb1 = max(kb - 32, 0);
+  if (warp == 0) tile_diag32_signed<0>(T, kb0, lane, dinv, sinv, ssg, L11s, fail_k, sg_out,
+                                       lane < kb0 ? kjj[lane] : 1.0, cnt3);
+  __syncthreads();
+  if (kb1 > 0) {
+    tile_rowsolve32<0>(T, 32, 32, T, sinv);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (int c = 0; c < 32; c++) T[tsw(32 + threadIdx.x, c)] *= ssg[c];
+    }
+    __syncthreads();
+    tile_block_update<true>(T, 32, 32, T, 0, 32, ssg);
+    __syncthreads();
+    if (warp == 0) tile_diag32_signed<32>(T, kb1, lane, dinv, sinv, ssg, L11s, fail_k, sg_out,
+                                          lane < kb1 ? kjj[32 + lane] : 1.0, cnt3);
+  } else if (warp == 0) {
+    for (int c = 0; c < 64; c++) T[tsw(32 + lane, c)] = 0.0;
+    sinv[32 + lane] = 0.0;
+    ssg[32 + lane] = 1.0;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void tile_potrf64(double* T, int kb, double* dinv, double* sinv, double* L11s,
                                              int* fail_k) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -342,6 +435,8 @@ struct TileCtx {
   int* cnt;
   int* fail_all;
   int task;           // ticket of the current task (trace)
+  double* Sg;         // LDL^T: pivot signs of the instance (internal numbering)
+  int* cnt3;          // LDL^T: (positive, negative, zero) pivot counts of the instance
 };
 
 __device__ __forceinline__ double* tile_ptr(const TileCtx& X, const TFront& F, int i, int j) {
@@ -475,18 +570,33 @@ __device__ void task_asm(const TileCtx& X, const TFront& F, int i, int jt, doubl
   publish_cnt(tile_cnt(X, F, i, jt), 1);
 }
 
-// sinv[0..64) <- inverse pivots of panel tile k (global Dv, final once cnt(k, k) == k + 1)
-__device__ __forceinline__ void load_sinv(const TileCtx& X, const TFront& F, int k, double* sinv) {
+// sinv[0..64) <- inverse pivots of panel tile k (global Dv, final once tile (k, k) is); with
+// LDL^T also ssg[0..64) <- the pivot signs
+template <bool SG = false>
+__device__ __forceinline__ void load_sinv(const TileCtx& X, const TFront& F, int k, double* sinv, double* ssg = nullptr) {
   const SnInfo I = X.P->sn[F.s];
   if (threadIdx.x < 64) {
     const int c = k * TBS + threadIdx.x;
-    sinv[threadIdx.x] = (threadIdx.x < tsize(F, k)) ? __ldcg(X.Dv + I.f0 + c) : 0.0;
+    const bool v = threadIdx.x < tsize(F, k);
+    sinv[threadIdx.x] = v ? __ldcg(X.Dv + I.f0 + c) : 0.0;
+    if (SG) ssg[threadIdx.x] = v ? __ldcg(X.Sg + I.f0 + c) : 1.0;
+  }
+}
+// LDL^T: K_jj of the columns of panel tile k (zero-pivot threshold, ldlt.cuh)
+__device__ __forceinline__ void load_kjj(const TileCtx& X, const TFront& F, int k, double* kjj) {
+  const SnInfo I = X.P->sn[F.s];
+  if (threadIdx.x < 64) {
+    const int c = I.f0 + k * TBS + threadIdx.x;
+    kjj[threadIdx.x] = (threadIdx.x < tsize(F, k)) ? __ldg(X.Kv + __ldg(X.P->Kp + c)) : 1.0;
   }
 }
 
+template <bool SG>
 __device__ void task_potrf0(const TileCtx& X, const TFront& F, double* sm) {
-  double *T0 = sm, *sinv = sm + 3 * TBD, *L11s = sinv + 64;
+  double *T0 = sm, *sinv = sm + 3 * TBD, *L11s = sinv + 64, *ssg = L11s + 1024;
   __shared__ int s_fail;
+  __shared__ double s_kjj[64];
+  if (SG) load_kjj(X, F, 0, s_kjj);
   wait_cnt(tile_cnt(X, F, 0, 0), 1);
   if (threadIdx.x == 0) s_fail = -1;
   tile_load_async(T0, tile_ptr(X, F, 0, 0));
@@ -494,33 +604,38 @@ __device__ void task_potrf0(const TileCtx& X, const TFront& F, double* sm) {
   cp_async_wait_all();
   __syncthreads();
   const SnInfo I = X.P->sn[F.s];
-  tile_potrf64(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail);
+  if (SG) tile_potrf64_signed(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail, ssg, X.Sg + I.f0, s_kjj, X.cnt3);
+  else tile_potrf64(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail);
   tile_store(tile_ptr(X, F, 0, 0), T0);
   tile_to_panel(F, T0, X.Lx + I.Lp, 0, 0);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + s_fail);
   publish_cnt(tile_cnt(X, F, 0, 0), 2);
 }
 
+template <bool SG>
 __device__ void task_trsm(const TileCtx& X, const TFront& F, int i, int k, double* sm) {
-  double *Lk = sm, *A = sm + TBD, *sinv = sm + 3 * TBD;
+  double *Lk = sm, *A = sm + TBD, *sinv = sm + 3 * TBD, *ssg = sinv + 64 + 1024;
   wait_cnt(tile_cnt(X, F, k, k), k + 2);
   tile_load_async(Lk, tile_ptr(X, F, k, k));
   wait_cnt(tile_cnt(X, F, i, k), k + 1);
   tile_load_async(A, tile_ptr(X, F, i, k));
-  load_sinv(X, F, k, sinv);
+  load_sinv<SG>(X, F, k, sinv, ssg);
   stamp_ready(X);
   cp_async_wait_all();
   __syncthreads();
-  tile_trsm64(A, Lk, sinv);
+  tile_trsm64<SG>(A, Lk, sinv, ssg);
   tile_store(tile_ptr(X, F, i, k), A);
   const SnInfo I = X.P->sn[F.s];
   tile_to_panel(F, A, X.Lx + I.Lp, i, k);
   publish_cnt(tile_cnt(X, F, i, k), k + 2);
 }
 
+template <bool SG>
 __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) {
-  double *Lk = sm, *A1 = sm + TBD, *A2 = sm + 2 * TBD, *sinv = sm + 3 * TBD, *L11s = sinv + 64;
+  double *Lk = sm, *A1 = sm + TBD, *A2 = sm + 2 * TBD, *sinv = sm + 3 * TBD, *L11s = sinv + 64, *ssg = L11s + 1024;
   __shared__ int s_fail;
+  __shared__ double s_kjj[64];
+  if (SG) load_kjj(X, F, k + 1, s_kjj);
   const SnInfo I = X.P->sn[F.s];
   if (threadIdx.x == 0) s_fail = -1;
   wait_cnt(tile_cnt(X, F, k, k), k + 2);
@@ -529,26 +644,29 @@ __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) 
   tile_load_async(A1, tile_ptr(X, F, k + 1, k));
   wait_cnt(tile_cnt(X, F, k + 1, k + 1), k + 1);
   tile_load_async(A2, tile_ptr(X, F, k + 1, k + 1));
-  load_sinv(X, F, k, sinv);
+  load_sinv<SG>(X, F, k, sinv, ssg);
   stamp_ready(X);
   cp_async_wait_all();
   __syncthreads();
   // TRSM(k+1, k), published at once (the other updates of step k may start)
-  tile_trsm64(A1, Lk, sinv);
+  tile_trsm64<SG>(A1, Lk, sinv, ssg);
   tile_store(tile_ptr(X, F, k + 1, k), A1);
   tile_to_panel(F, A1, X.Lx + I.Lp, k + 1, k);
   publish_cnt(tile_cnt(X, F, k + 1, k), k + 2);
   // A2 -= L1 L1^T, Cholesky of A2
-  tile_gemm_nt_smem(A2, A1, A1);
-  tile_potrf64(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail);
+  tile_gemm_nt_smem<SG>(A2, A1, A1, ssg);
+  if (SG) tile_potrf64_signed(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail, ssg,
+                              X.Sg + I.f0 + (k + 1) * TBS, s_kjj, X.cnt3);
+  else tile_potrf64(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail);
   tile_store(tile_ptr(X, F, k + 1, k + 1), A2);
   tile_to_panel(F, A2, X.Lx + I.Lp, k + 1, k + 1);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + (k + 1) * TBS + s_fail);
   publish_cnt(tile_cnt(X, F, k + 1, k + 1), k + 3);
 }
 
+template <bool SG>
 __device__ void task_upd(const TileCtx& X, const TFront& F, int i, int j, int k, double* sm) {
-  double *A = sm, *B = sm + TBD;
+  double *A = sm, *B = sm + TBD, *sinv = sm + 3 * TBD, *ssg = sinv + 64 + 1024;
   wait_cnt(tile_cnt(X, F, i, k), k + 2);
   tile_load_async(A, tile_ptr(X, F, i, k));
   if (j != i) {
@@ -557,12 +675,14 @@ __device__ void task_upd(const TileCtx& X, const TFront& F, int i, int j, int k,
   }
   wait_cnt(tile_cnt(X, F, i, j), k + 1);
   stamp_ready(X);
+  if (SG) load_sinv<true>(X, F, k, sinv, ssg);
   cp_async_wait_all();
   __syncthreads();
-  tile_gemm_nt_global(tile_ptr(X, F, i, j), A, j != i ? B : A);
+  tile_gemm_nt_global<SG>(tile_ptr(X, F, i, j), A, j != i ? B : A, ssg);
   publish_cnt(tile_cnt(X, F, i, j), k + 2);
 }
 
+template <bool SG>
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_factor_kernel(DevPlan P, TilePlan T, const double* __restrict__ Kv_all,
                                                                     double* Lx_all, const double* U_all, double* Dv_all,
                                                                     int* fail_all) {
@@ -593,14 +713,16 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_factor_kernel(DevPlan P,
     X.cnt = T.cnt + (long long)b * T.ncnt;
     X.fail_all = fail_all;
     X.task = t;
+    X.Sg = SG ? P.Sg + (long long)b * P.n : nullptr;
+    X.cnt3 = SG ? P.inert + 3 * b : nullptr;
     const TFront F = T.fr[tk.y];
     const int i = tk.z & 0xffff, j = tk.z >> 16, k = tk.w;
     switch (type) {
       case TASK_ASM: task_asm(X, F, i, j, tsm); break;
-      case TASK_POTRF0: task_potrf0(X, F, tsm); break;
-      case TASK_TRSM: task_trsm(X, F, i, k, tsm); break;
-      case TASK_CRIT: task_crit(X, F, k, tsm); break;
-      default: task_upd(X, F, i, j, k, tsm); break;
+      case TASK_POTRF0: task_potrf0<SG>(X, F, tsm); break;
+      case TASK_TRSM: task_trsm<SG>(X, F, i, k, tsm); break;
+      case TASK_CRIT: task_crit<SG>(X, F, k, tsm); break;
+      default: task_upd<SG>(X, F, i, j, k, tsm); break;
     }
     if (T.trace) {
       __syncthreads();

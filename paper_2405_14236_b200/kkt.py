@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
-           "kkt_sync_info", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
+           "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
            "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_last_error", "kkt_destroy"]
 
 
@@ -80,6 +80,8 @@ def lib(build_if_missing: bool = True):
             "kkt_step_host": [P, P, P, P, P, P, D, D, D, P, P, I, D],
             "kkt_get_condensed": [P, I, P, P, P],
             "kkt_recover": [P, P, P, P, P, P],
+            "kkt_inertia": [P, P],
+            "kkt_factor_inertia_correct": [P, P, P, P, P, P, D, D, P, C.POINTER(D), C.POINTER(I)],
             "kkt_solve_unreduced": [P] + [P] * 4 + [P] * 6 + [P] * 6 + [I, D],
             "kkt_recover_bounds": [P, P, P, P, P, D, P, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
@@ -190,6 +192,23 @@ def kkt_solve_unreduced(h, x, s, u, v, f, d, max_refine=10, tol=0.0):
                                    *[_ptr(a) for a in d], int(max_refine), float(tol)), "kkt_solve_unreduced")
 
 
+def kkt_inertia(h, batch=1):
+    c = np.zeros(3 * batch, np.int32)
+    _chk(lib().kkt_inertia(h, c.ctypes.data), "kkt_inertia")
+    return c.reshape(batch, 3)
+
+
+def kkt_factor_inertia_correct(h, W_vals, J_vals, Sigma_x, Sigma_s, D=None, delta_c=0.0, gamma=0.0,
+                               params=None):
+    """Returns (delta_w, tries); params = [dw_min, dw_first, dw_max, k_minus, k_plus, k_plus_bar, dw_last]."""
+    dw, tr = C.c_double(0.0), C.c_int(0)
+    pa = None if params is None else np.ascontiguousarray(params, dtype=np.float64)
+    _chk(lib().kkt_factor_inertia_correct(h, _ptr(W_vals), _ptr(J_vals), _ptr(Sigma_x), _ptr(Sigma_s), _ptr(D),
+                                          float(delta_c), float(gamma), None if pa is None else pa.ctypes.data,
+                                          C.byref(dw), C.byref(tr)), "kkt_factor_inertia_correct")
+    return dw.value, tr.value
+
+
 def kkt_recover(h, r2, r4, dx, dz, ds):
     _chk(lib().kkt_recover(h, _ptr(r2), _ptr(r4), _ptr(dx), _ptr(dz), _ptr(ds)), "kkt_recover")
 
@@ -265,9 +284,9 @@ class KKTSolver:
     """One handle: analysis on construction; `bind()` attaches a CUDA device + torch stream."""
 
     def __init__(self, n, m, m_eq, W_rowptr, W_colind, J_rowptr, J_colind, batch=1, ordering=0,
-                 relax_small=4, relax_big=64, relax_zero_frac=0.05):
+                 relax_small=4, relax_big=64, relax_zero_frac=0.05, factor_kind=0):
         o = kkt_default_options()
-        o.batch, o.ordering = int(batch), int(ordering)
+        o.batch, o.ordering, o.factor_kind = int(batch), int(ordering), int(factor_kind)
         o.relax_small, o.relax_big, o.relax_zero_frac = relax_small, relax_big, relax_zero_frac
         self.n, self.m, self.m_eq, self.batch = n, m, m_eq, batch
         self.h, self.info = kkt_analyze(n, m, m_eq, W_rowptr, W_colind, J_rowptr, J_colind, o)
@@ -311,6 +330,13 @@ class KKTSolver:
 
     def solve_unreduced(self, x, s, u, v, f, d, max_refine=10, tol=0.0):
         kkt_solve_unreduced(self.h, x, s, u, v, f, d, max_refine, tol)
+
+    def inertia(self):
+        return kkt_inertia(self.h, self.batch)
+
+    def factor_inertia_correct(self, W_vals, J_vals, Sigma_x, Sigma_s, D=None, delta_c=0.0, gamma=0.0, params=None):
+        self._vals = (W_vals, J_vals, Sigma_x, Sigma_s, D)
+        return kkt_factor_inertia_correct(self.h, W_vals, J_vals, Sigma_x, Sigma_s, D, delta_c, gamma, params)
 
     def recover(self, r2, r4, dx, dz, ds):
         kkt_recover(self.h, r2, r4, dx, dz, ds)

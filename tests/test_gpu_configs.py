@@ -327,3 +327,98 @@ def test_bearing_800_parity():
     assert info["status"] == 0, info
     assert relerr(x, R["x"]) <= 1e-8, (relerr(x, R["x"]), info)
     S.close()
+
+
+def _ldlt_solver(inst, **kw):
+    import paper_2405_14236_b200 as K
+    return K.KKTSolver.from_instance(inst, factor_kind=1, **kw).bind(0)
+
+
+@pytest.mark.parametrize("case,hcap", [("tiny", None), ("C5i", None), ("C2", None), ("C2s", "1500"), ("C7", None)])
+def test_ldlt_spd_parity(case, hcap, monkeypatch):
+    """NEXT-2: factor_kind = 1 (pivot-free LDL^T, signed-Cholesky form) on SPD systems: inertia
+    (n, 0, 0) and the refined solution matches the oracle; "C2s"+KKT_HCAP runs the signed tile
+    kernel, C7 (dense elec) one signed dense front."""
+    from kkt_gpu import run_lifted, relerr
+    from synth.generator import tiny_random
+    if hcap:
+        monkeypatch.setenv("KKT_HCAP", hcap)
+    inst = {"tiny": lambda: tiny_random(40, 30, 0, seed=5, Xi=1e-6, delta_w=1e-4, delta_c=1e-3),
+            "C5i": lambda: make_config("C5", batch=1)}.get(case, lambda: make_config(case))()
+    R = oracle.reference_solve(inst)
+    S = _ldlt_solver(inst)
+    x, info, S = run_lifted(inst, max_refine=10, solver=S)
+    assert info["status"] == 0, info
+    assert tuple(S.inertia()[0]) == (inst.n, 0, 0)
+    assert relerr(x, R["x"]) <= 1e-8, (relerr(x, R["x"]), info)
+    S.close()
+
+
+def _indefinite(case, seed):
+    from synth.generator import tiny_random
+    if case == "tiny":
+        return tiny_random(40, 16, 0, seed=seed, Xi=1e-2, w_psd=False)
+    inst = make_config("C5", batch=1, Xi=1e-2)      # W - 8 I: a few dozen negative eigenvalues
+    inst.W_vals = inst.W_vals.copy()
+    diag = inst.W_rowptr[1:] - 1
+    inst.W_vals[diag] -= 8.0
+    return inst
+
+
+@pytest.mark.parametrize("case,seed,hcap", [("tiny", 301, None), ("tiny", 302, None), ("C5i", 0, None),
+                                            ("C5i", 0, "600")])
+def test_ldlt_indefinite_inertia_and_solve(case, seed, hcap, monkeypatch):
+    """NEXT-2 on indefinite K: the device inertia equals the oracle LDL^T inertia (and the dense
+    eigenvalue counts for the tiny cases), and the refined solve matches a dense solve."""
+    from kkt_gpu import run_lifted, relerr
+    if hcap:
+        monkeypatch.setenv("KKT_HCAP", hcap)
+    inst = _indefinite(case, seed)
+    Kp, Ki, Kv = oracle.condense(inst)
+    perm = oracle.md_order(inst.n, Kp, Ki)
+    _, _, Lp, Li = oracle.symbolic(inst.n, Kp, Ki, perm, want_pattern=True)
+    Lx, inert, fail = oracle.ldlt(inst.n, Kp, Ki, Kv, perm, Lp, Li)
+    assert fail < 0 and inert[1] > 0
+    S = _ldlt_solver(inst)
+    x, info, S = run_lifted(inst, max_refine=10, solver=S)
+    assert info["status"] == 0, info
+    assert tuple(S.inertia()[0]) == inert
+    n = inst.n
+    if n <= 100:
+        A = np.zeros((n, n))
+        for j in range(n):
+            for p in range(Kp[j], Kp[j + 1]):
+                A[Ki[p], j] = Kv[p]; A[j, Ki[p]] = Kv[p]
+        ev = np.linalg.eigvalsh(A)
+        assert inert == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
+        xr = np.linalg.solve(A, inst.b)
+    else:
+        xr = oracle.ldlt_solve(n, Lp, Li, Lx, perm, inst.b)
+    assert relerr(x, xr) <= 1e-8, (relerr(x, xr), info)
+    S.close()
+
+
+@pytest.mark.parametrize("factor_kind", [1, 0])
+def test_inertia_correction_matches_oracle(factor_kind):
+    """The delta_w loop (Wachter-Biegler) on the device takes the same
+    decisions as the oracle loop (LDL^T inertia counts; for LL^T the Cholesky breakdown), ends
+    with the same delta_w, and the factor it leaves solves the shifted system."""
+    import torch
+    import paper_2405_14236_b200 as K
+    from kkt_gpu import dev, relerr
+    inst = _indefinite("tiny", 303)
+    dw_ref, tries_ref, inert = oracle.inertia_correct(inst)
+    assert inert == (inst.n, 0, 0) and tries_ref >= 2
+    S = K.KKTSolver.from_instance(inst, factor_kind=factor_kind).bind(0)
+    W, J, Sx, Ss, b = [dev(a, "cuda:0") for a in (inst.W_vals, inst.J_vals, inst.Sigma_x, inst.Sigma_s, inst.b)]
+    dw, tries = S.factor_inertia_correct(W, J, Sx, Ss, None, inst.delta_c, inst.gamma)
+    assert dw == dw_ref and tries == tries_ref, (dw, tries, dw_ref, tries_ref)
+    x = torch.zeros_like(b)
+    S.solve(b, x, 10, 0.0)
+    info = S.sync_info()
+    import copy
+    shifted = copy.copy(inst)
+    shifted.delta_w = dw
+    R = oracle.reference_solve(shifted)
+    assert info["status"] == 0 and relerr(x.cpu().numpy(), R["x"]) <= 1e-8
+    S.close()

@@ -164,3 +164,84 @@ def test_plain_fp64_solve_is_not_enough_in_stress_regime():
     x0 = oracle.trisolve(inst.n, R["Lp"], R["Li"], R["Lx"], R["perm"], inst.b)
     err = np.abs(x0 - R["x"]).max() / np.abs(R["x"]).max()
     assert err > 1e-11
+
+
+def _dense_K(inst):
+    Kp, Ki, Kv = oracle.condense(inst)
+    n = inst.n
+    A = np.zeros((n, n))
+    for j in range(n):
+        for p in range(Kp[j], Kp[j + 1]):
+            A[Ki[p], j] = Kv[p]; A[j, Ki[p]] = Kv[p]
+    return (Kp, Ki, Kv), A
+
+
+def _ldlt_of(inst):
+    K, A = _dense_K(inst)
+    perm = oracle.md_order(inst.n, K[0], K[1])
+    _, _, Lp, Li = oracle.symbolic(inst.n, K[0], K[1], perm, want_pattern=True)
+    Lx, inert, fail = oracle.ldlt(inst.n, K[0], K[1], K[2], perm, Lp, Li)
+    return K, A, perm, Lp, Li, Lx, inert, fail
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ldlt_inertia_equals_eigenvalue_counts(seed):
+    """NEXT-2 pin (Sylvester): the pivot-free LDL^T's (positive, negative, zero)
+    pivot counts equal the signs of the eigenvalues of K (numpy eigvalsh) on indefinite inputs
+    (W with an indefinite diagonal), and L D L^T reproduces P K P^T."""
+    inst = tiny_random(24, 10, 0, seed=200 + seed, Xi=1e-2, w_psd=False)
+    K, A, perm, Lp, Li, Lx, inert, fail = _ldlt_of(inst)
+    assert fail < 0
+    ev = np.linalg.eigvalsh(A)
+    assert np.min(np.abs(ev)) > 1e-8 * np.max(np.abs(ev))      # nonsingular test matrix
+    assert inert == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
+    n = inst.n
+    L = np.eye(n); d = np.zeros(n)
+    for j in range(n):
+        d[j] = Lx[Lp[j]]
+        for p in range(Lp[j] + 1, Lp[j + 1]):
+            L[Li[p], j] = Lx[p]
+    PA = A[np.ix_(perm, perm)]
+    assert np.abs(L @ np.diag(d) @ L.T - PA).max() <= 1e-12 * np.abs(A).max()
+    x = oracle.ldlt_solve(n, Lp, Li, Lx, perm, inst.b)
+    assert np.abs(A @ x - inst.b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + np.abs(inst.b).max())
+
+
+def test_ldlt_textbook_and_spd_cases():
+    """diag(-1, 2, -3) -> inertia (1, 2, 0); an SPD K gives d_j = (Cholesky l_jj)^2 and (n, 0, 0);
+    an exactly singular K (zero row) counts one zero pivot (R6)."""
+    from synth.generator import KKTInstance
+    def diag_inst(dv):
+        n = len(dv)
+        return KKTInstance("d", n, 0, 0, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                           np.array(dv, float), np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0),
+                           np.zeros(n), np.zeros(0), b=np.ones(n))
+    _, _, _, _, _, _, inert, _ = _ldlt_of(diag_inst([-1.0, 2.0, -3.0]))
+    assert inert == (1, 2, 0)
+    _, _, _, _, _, _, inert, _ = _ldlt_of(diag_inst([4.0, 0.0, 1.0]))
+    assert inert == (2, 0, 1)
+    inst = make_config("C5", batch=1, Xi=1e-2)     # well-conditioned: pivots agree to rounding
+    K, A, perm, Lp, Li, Lx, inert, fail = _ldlt_of(inst)
+    assert inert == (inst.n, 0, 0) and fail < 0
+    Lc, f2 = oracle.cholesky(inst.n, K[0], K[1], K[2], perm, Lp, Li)
+    d = np.array([Lx[Lp[j]] for j in range(inst.n)])
+    lc = np.array([Lc[Lp[j]] for j in range(inst.n)])
+    assert np.all(np.abs(d - lc * lc) <= 1e-11 * d)
+
+
+def test_inertia_correction_rule():
+    """Wachter-Biegler primal correction in the oracle: an SPD K keeps
+    delta_w = 0; an indefinite W is shifted until the LDL^T inertia is (n, 0, 0), with the
+    delta_w sequence 1e-4 x 100^k of the rule -- and the accepted shift exceeds -lambda_min."""
+    inst = tiny_random(30, 12, 0, seed=9, Xi=1e-2)
+    dw, tries, inert = oracle.inertia_correct(inst)
+    assert dw == 0.0 and tries == 1 and inert == (30, 0, 0)
+    bad = tiny_random(30, 12, 0, seed=9, Xi=1e-2, w_psd=False)
+    dw, tries, inert = oracle.inertia_correct(bad)
+    assert inert == (30, 0, 0) and tries >= 2
+    assert dw == 1e-4 * 100.0 ** (tries - 2)
+    _, A = _dense_K(bad)
+    lam = np.linalg.eigvalsh(A).min()
+    assert lam < 0 and dw > -lam
+    _, A2 = _dense_K(bad)
+    assert np.linalg.eigvalsh(A2 + (dw / 100.0) * np.eye(30)).min() < 0 or tries == 2
