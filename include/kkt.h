@@ -301,6 +301,9 @@ int kkt_debug_steps(kkt_handle h, long long *out, int n);
  * trace[n][4] (globaltimer ns at ticket, dependencies met, end; SM id) when KKT_TRACE=1 was set
  * at kkt_bind; *est_us = the bind-time list-schedule estimate of the makespan.  Blocking. */
 int kkt_tile_trace(kkt_handle h, long long *trace, int *tasks, int n, double *est_us);
+/* Same for the tile-task solve through the large fronts (last solve launch; task types: gather,
+ * forward update, forward chain step, backward update, backward chain step). */
+int kkt_tile_solve_trace(kkt_handle h, long long *trace, int *tasks, int n, double *est_us);
 
 /* Last error message (static storage, thread-local). */
 const char *kkt_last_error(void);

@@ -19,6 +19,7 @@
 #include "resid.cuh"
 #include "trsv.cuh"
 #include "tiles.cuh"
+#include "tsolve.cuh"
 #include "k3.cuh"
 #include "plan.h"
 #include "tile_plan.h"
@@ -81,6 +82,7 @@ struct kkt_plan {
   double* Sg = nullptr;   // LDL^T pivot signs [B][n]
   int* inert = nullptr;   // LDL^T inertia counts [B][3]
   bool ldlt = false;
+  bool resid_warp = false;   // residual columns by warps (some column has > 96 terms)
   double *g_r1 = nullptr, *g_r2 = nullptr, *g_dx = nullptr, *g_dy = nullptr;  // HyKKT graph I/O
   cudaGraphExec_t hy_exec = nullptr;                       // recorded HyKKT solve
   double hy_rtol = -1, hy_gamma = 0, hy_dw = 0;
@@ -139,6 +141,13 @@ struct kkt_plan {
   int g_tile = 1;
   double tile_est_us = 0.0;
   long long* tile_trace = nullptr;  // KKT_TRACE: per-task stamps of the tile kernel
+  // tile-task solves through the huge fronts (tsolve.cuh); KKT_TSOLVE=0: level kernel (hsolve.cuh)
+  bool tsolve = false;
+  TSolvePlan tsp{};
+  void* ts_mem = nullptr;
+  size_t ts_cnt_bytes = 0;
+  double ts_est_us = 0.0;
+  long long* ts_trace = nullptr;
   bool fev_valid = false;
 };
 
@@ -424,7 +433,7 @@ static void release_device(kkt_plan* h) {
   if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
   h->pinned_flags = nullptr;
   fr(h->trace_buf); fr(h->dbg_buf); fr(h->huge_mem); fr(h->hsolve_mem);
-  fr(h->tile_mem); fr(h->tile_pool); fr(h->tile_trace);
+  fr(h->tile_mem); fr(h->tile_pool); fr(h->tile_trace); fr(h->ts_mem); fr(h->ts_trace);
   if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
   h->solve_exec = nullptr;
   if (h->hy_exec) cudaGraphExecDestroy(h->hy_exec);
@@ -599,6 +608,13 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   Carver c{(char*)h->ws, 0, false};
   carve_workspace(h, c);
   h->ldlt = (P.factor_kind == 1);
+  {
+    int maxc = 0;
+    for (int i = 0; i < P.n; i++)
+      maxc = std::max(maxc, (P.Wf_p[i + 1] - P.Wf_p[i]) + (P.Jt_p[i + 1] - P.Jt_p[i]));
+    h->resid_warp = maxc > 96;
+    if (const char* e = getenv("KKT_RESID_WARP")) h->resid_warp = atoi(e) > 0;
+  }
   for (DevPlan* dq : {&h->dp, &h->dps}) { dq->ldlt = h->ldlt; dq->Sg = h->Sg; dq->inert = h->inert; }
   CUDA_TRY(cudaMemsetAsync(h->ws, 0, need, h->stream));
   int big = INT_MAX;
@@ -723,7 +739,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       const size_t hb = align_up(tph.hidx.size() * sizeof(int));
       const size_t chb = align_up(tph.tch.size() * sizeof(int)), cub = align_up(tph.tcut.size() * sizeof(int));
       const size_t kpb = align_up(tph.tkptr.size() * sizeof(int)), kib = align_up(tph.tkidx.size() * sizeof(int));
-      CUDA_TRY(cudaMalloc(&h->tile_mem, fb + tkb + hb + chb + cub + kpb + kib));
+      const size_t ibb = align_up(tph.ibase.size() * sizeof(long long));
+      CUDA_TRY(cudaMalloc(&h->tile_mem, fb + tkb + hb + chb + cub + kpb + kib + ibb));
       char* base = (char*)h->tile_mem;
       CUDA_TRY(cudaMemcpy(base, tph.fr.data(), tph.fr.size() * sizeof(TFrontHost), cudaMemcpyHostToDevice));
       CUDA_TRY(cudaMemcpy(base + fb, tasks.data(), tasks.size() * sizeof(TTask), cudaMemcpyHostToDevice));
@@ -733,9 +750,11 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       char* kb_ = base + fb + tkb + hb + chb + cub;
       CUDA_TRY(cudaMemcpy(kb_, tph.tkptr.data(), tph.tkptr.size() * sizeof(int), cudaMemcpyHostToDevice));
       CUDA_TRY(cudaMemcpy(kb_ + kpb, tph.tkidx.data(), tph.tkidx.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(kb_ + kpb + kib, tph.ibase.data(), tph.ibase.size() * sizeof(long long), cudaMemcpyHostToDevice));
       const size_t poolb = align_up(B * (size_t)tph.pool_doubles * sizeof(double));
+      const size_t invb = align_up(B * (size_t)tph.inv_doubles * sizeof(double));
       h->tile_cnt_bytes = align_up((B * (size_t)tph.ncnt + 1) * sizeof(int));
-      CUDA_TRY(cudaMalloc(&h->tile_pool, poolb + h->tile_cnt_bytes));
+      CUDA_TRY(cudaMalloc(&h->tile_pool, poolb + invb + h->tile_cnt_bytes));
       TilePlan& T = h->tp;
       T.fr = (const TFront*)base;
       T.tasks = (const int4*)(base + fb);
@@ -749,8 +768,45 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       T.ncnt = tph.ncnt;
       T.pool_doubles = tph.pool_doubles;
       T.pool = (double*)h->tile_pool;
-      T.cnt = (int*)((char*)h->tile_pool + poolb);
+      T.inv = (double*)((char*)h->tile_pool + poolb);
+      T.inv_doubles = tph.inv_doubles;
+      T.ibase = (const long long*)(kb_ + kpb + kib);
+      T.cnt = (int*)((char*)h->tile_pool + poolb + invb);
       T.trace = nullptr;
+      h->tsolve = !h->huge_solve_cta && !(getenv("KKT_TSOLVE") && atoi(getenv("KKT_TSOLVE")) == 0);
+      if (h->tsolve) {
+        TSolvePlanHost tsh;
+        build_tile_solve_plan(P, tph, h->g_tile, tsh);
+        h->ts_est_us = tsh.est_us;
+        std::vector<TTask> st;
+        st.reserve(tsh.tasks.size() * B);
+        for (const TTask& t : tsh.tasks)
+          for (size_t b = 0; b < B; b++) st.push_back(TTask{t.x | (int)(b << 4), t.y, t.z, t.w});
+        const size_t sb = align_up(st.size() * sizeof(TTask)), cbb = align_up(tsh.cbase2.size() * sizeof(int));
+        const size_t pbb = align_up(tsh.pbase.size() * sizeof(long long));
+        const size_t partb = align_up(B * (size_t)tsh.part_doubles * sizeof(double));
+        h->ts_cnt_bytes = align_up((B * (size_t)tsh.ncnt + 1) * sizeof(int));
+        CUDA_TRY(cudaMalloc(&h->ts_mem, sb + cbb + pbb + partb + h->ts_cnt_bytes));
+        char* tb_ = (char*)h->ts_mem;
+        CUDA_TRY(cudaMemcpy(tb_, st.data(), st.size() * sizeof(TTask), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(tb_ + sb, tsh.cbase2.data(), tsh.cbase2.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(tb_ + sb + cbb, tsh.pbase.data(), tsh.pbase.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        h->tsp.pbase = (const long long*)(tb_ + sb + cbb);
+        h->tsp.part = (double*)(tb_ + sb + cbb + pbb);
+        h->tsp.part_doubles = tsh.part_doubles;
+        h->tsp.tasks = (const int4*)tb_;
+        h->tsp.ntask = (int)st.size();
+        h->tsp.ncnt = tsh.ncnt;
+        h->tsp.cbase2 = (const int*)(tb_ + sb);
+        h->tsp.cnt = (int*)(tb_ + sb + cbb + pbb + partb);
+        h->tsp.trace = nullptr;
+        CUDA_TRY(cudaFuncSetAttribute(tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
+      }
+      if (h->tsolve && getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
+        CUDA_TRY(cudaMalloc(&h->ts_trace, (size_t)h->tsp.ntask * 4 * sizeof(long long)));
+        CUDA_TRY(cudaMemset(h->ts_trace, 0, (size_t)h->tsp.ntask * 4 * sizeof(long long)));
+        h->tsp.trace = h->ts_trace;
+      }
       if (getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
         CUDA_TRY(cudaMalloc(&h->tile_trace, (size_t)T.ntask * 4 * sizeof(long long)));
         CUDA_TRY(cudaMemset(h->tile_trace, 0, (size_t)T.ntask * 4 * sizeof(long long)));
@@ -918,7 +974,20 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
                           h->ctl + 3 * KKT_CTL, done, h->pcap, (const double*)(h->use_linv ? h->Li : nullptr)));
       h->launches++;
     }
-    if (!P.order_h.empty() && !cta_huge) {
+    if (!P.order_h.empty() && !cta_huge && h->tsolve) {
+      CUDA_TRY(cudaMemsetAsync(h->tsp.cnt, 0, h->ts_cnt_bytes, h->ls));
+      DevPlan dp = h->dp;
+      TilePlan tp = h->tp;
+      TSolvePlan sp = h->tsp;
+      const double *dv = h->Dv, *rh = rhs;
+      double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
+      long long rs_ = rs, xs_ = xs;
+      const int* dn = done;
+      void* args[] = {&dp, &tp, &sp, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn};
+      CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_solve_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
+                                           (size_t)TILE_SMEM_BYTES, h->ls));
+      h->launches++;
+    } else if (!P.order_h.empty() && !cta_huge) {
       DevPlan dp = h->dp;
       const double *lx = h->Lx, *dv = h->Dv, *rh = rhs;
       double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
@@ -963,6 +1032,14 @@ static kkt_status launch_resid(kkt_plan* h, const double* x, const double* rhs, 
         h->dp, h->Jv, h->Dh, h->Dl, x, P.n, mode, dy, rb2, h->res2, h->T, h->A, done);
     LAUNCH_CHECK();
     h->launches++;
+  }
+  if (h->resid_warp) {  // long columns (dense W): one warp per column
+    dim3 g = grid_2d(((long long)P.n + 7) / 8 * 256, P.batch, h->sms);
+    resid_cols_warp_kernel<<<g, 256, 0, h->ls>>>(
+        h->dp, h->Wv, h->Jv, h->Sx, h->dw, x, P.n, rhs, P.n, h->T, h->A, res, omega, done);
+    LAUNCH_CHECK();
+    h->launches++;
+    return KKT_OK;
   }
   resid_cols_kernel<<<grid_2d(P.n, P.batch, h->sms), 256, 0, h->ls>>>(
       h->dp, h->Wv, h->Jv, h->Sx, h->dw, x, P.n, rhs, P.n, h->T, h->A, res, omega, done);
@@ -1741,6 +1818,21 @@ extern "C" int kkt_tile_trace(kkt_handle h, long long* trace, int* tasks, int n,
   if (trace && n > 0) {
     if (!h->tile_trace) return -1;
     if (cudaMemcpy(trace, h->tile_trace, (size_t)n * 32, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  }
+  return nt;
+}
+
+// tracing aid: the same for the tile-task solve of the last solve launch (which = 1)
+extern "C" int kkt_tile_solve_trace(kkt_handle h, long long* trace, int* tasks, int n, double* est_us) {
+  if (!h || !h->tsolve || !h->ts_mem) return -1;
+  if (est_us) *est_us = h->ts_est_us;
+  const int nt = h->tsp.ntask;
+  n = std::min(n, nt);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return -2;
+  if (tasks && n > 0 && cudaMemcpy(tasks, h->tsp.tasks, (size_t)n * 16, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  if (trace && n > 0) {
+    if (!h->ts_trace) return -1;
+    if (cudaMemcpy(trace, h->ts_trace, (size_t)n * 32, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
   }
   return nt;
 }

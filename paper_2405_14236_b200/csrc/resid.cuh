@@ -90,4 +90,60 @@ __global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, cons
   if (omega) block_max_atomic(omega + b, ommax);
 }
 
+// Variant for long columns (dense W, e.g. COPS elec): one WARP per column.  Lanes accumulate a
+// strided subset of the column's W and J^T terms in double-double, then a fixed xor-butterfly
+// (dd_add) combines them: the summation order is fixed, so results stay deterministic.
+// grid (gx, batch); blockDim = 256 (8 columns per block).
+__global__ void resid_cols_warp_kernel(DevPlan P, const double* __restrict__ Wv, const double* __restrict__ Jv,
+                                       const double* __restrict__ Sx, double dw, const double* __restrict__ x,
+                                       long long xs, const double* __restrict__ rhs, long long rs,
+                                       const double2* __restrict__ T, const double* __restrict__ A,
+                                       double* res, unsigned long long* omega, const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (done && (done[P.batch] == 0 || done[b])) return;  // block-uniform exits
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const double* W = Wv + (long long)b * P.nnzW;
+  const double* J = Jv + (long long)b * P.nnzJ;
+  const double* xb = x + (long long)b * xs;
+  const double2* Tb = T + (long long)b * P.m;
+  const double* Ab = A + (long long)b * P.m;
+  double ommax = 0.0;
+  for (int i = blockIdx.x * nwb + wib; i < P.n; i += gridDim.x * nwb) {
+    const long long idx = (long long)b * P.n + i;
+    dd y = {0.0, 0.0};
+    double den = 0.0;
+    for (int p = P.Wf_p[i] + lane; p < P.Wf_p[i + 1]; p += 32) {
+      const double wv = W[P.Wf_k[p]], xv = xb[P.Wf_c[p]];
+      y = dd_add(y, two_prod(wv, xv));
+      den = fma(fabs(wv), fabs(xv), den);
+    }
+    for (int p = P.Jt_p[i] + lane; p < P.Jt_p[i + 1]; p += 32) {
+      const int r = P.Jt_r[p];
+      const double jv = J[P.Jt_k[p]];
+      const double2 t = Tb[r];
+      y = dd_add(y, dd_mul_d(dd{t.x, t.y}, jv));
+      den = fma(fabs(jv), Ab[r], den);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const dd oth = {__shfl_xor_sync(0xffffffffu, y.hi, o), __shfl_xor_sync(0xffffffffu, y.lo, o)};
+      // both partners compute the same sum: order the operands by lane so the result is identical
+      y = (lane & o) ? dd_add(oth, y) : dd_add(y, oth);
+      den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    const double xi = xb[i];
+    const dd s2 = two_sum(Sx[idx], dw);
+    y = dd_add(dd_mul_d(s2, xi), y);
+    den = fma(fabs(s2.hi), fabs(xi), den);
+    const double bi = rhs[(long long)b * rs + i];
+    const dd rr = dd_add(dd{bi, 0.0}, dd{-y.hi, -y.lo});
+    const double rv = rr.hi + rr.lo;
+    if (lane == 0) res[idx] = rv;
+    den += fabs(bi);
+    const double om = (den > 0.0) ? fabs(rv) / den : (rv != 0.0 ? INFINITY : 0.0);
+    ommax = (isnan(om) || isnan(ommax)) ? NAN : fmax(ommax, om);
+  }
+  if (omega) block_max_atomic(omega + b, ommax);
+}
+
 }  // namespace kkt

@@ -20,6 +20,7 @@ namespace kkt {
 
 namespace {
 constexpr int TB = 64;
+constexpr int TS_G = 0, TS_U = 1, TS_C = 2, TS_BU_ = 3, TS_BC_ = 4, TS_UF = 5;  // tsolve.cuh task types
 
 struct Task {
   int type, f, i, j, k;
@@ -28,6 +29,64 @@ struct Task {
 
 int tl(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
 }  // namespace
+
+// List-scheduling simulation: bottom-level priorities, earliest free worker; returns the
+// simulated makespan and the start order (a topological order of the DAG).
+template <class TaskT>
+static double list_schedule(const std::vector<TaskT>& tasks, const std::vector<std::vector<int>>& pred,
+                            int workers, std::vector<int>& order) {
+  const int N = (int)tasks.size();
+  std::vector<std::vector<int>> succ(N);
+  for (int t = 0; t < N; t++)
+    for (int p : pred[t]) succ[p].push_back(t);
+  std::vector<double> blev(N, 0.0);
+  for (int t = N - 1; t >= 0; t--) {
+    double m = 0.0;
+    for (int q : succ[t]) m = std::max(m, blev[q]);
+    blev[t] = tasks[t].dur + m;
+  }
+  std::vector<int> npred(N);
+  std::vector<double> ready_at(N, 0.0), fin(N, 0.0);
+  for (int t = 0; t < N; t++) npred[t] = (int)pred[t].size();
+  using PQ = std::pair<double, int>;
+  auto cmp_prio = [&](int a, int b) { return blev[a] != blev[b] ? blev[a] < blev[b] : a > b; };
+  std::priority_queue<int, std::vector<int>, decltype(cmp_prio)> avail(cmp_prio);
+  std::priority_queue<PQ, std::vector<PQ>, std::greater<PQ>> pending, running;
+  for (int t = 0; t < N; t++)
+    if (npred[t] == 0) pending.push({0.0, t});
+  int free_w = std::max(1, workers);
+  double now = 0.0;
+  order.clear();
+  order.reserve(N);
+  while ((int)order.size() < N) {
+    while (!pending.empty() && pending.top().first <= now) { avail.push(pending.top().second); pending.pop(); }
+    if (free_w > 0 && !avail.empty()) {
+      const int t = avail.top();
+      avail.pop();
+      fin[t] = now + tasks[t].dur;
+      running.push({fin[t], t});
+      order.push_back(t);
+      free_w--;
+      continue;
+    }
+    double nxt = 1e300;
+    if (!running.empty()) nxt = running.top().first;
+    if (free_w > 0 && !pending.empty()) nxt = std::min(nxt, pending.top().first);
+    now = std::max(now, nxt);
+    while (!running.empty() && running.top().first <= now) {
+      const int t = running.top().second;
+      running.pop();
+      free_w++;
+      for (int q : succ[t]) {
+        ready_at[q] = std::max(ready_at[q], fin[t]);
+        if (--npred[q] == 0) pending.push({ready_at[q], q});
+      }
+    }
+  }
+  double mk = 0.0;
+  for (int t = 0; t < N; t++) mk = std::max(mk, fin[t]);
+  return mk;
+}
 
 void build_tile_plan(const Plan& P, int workers, TilePlanHost& out) {
   out = TilePlanHost();
@@ -94,6 +153,12 @@ void build_tile_plan(const Plan& P, int workers, TilePlanHost& out) {
   }
   out.pool_doubles = std::max<long long>(tb, 1);
   out.ncnt = std::max(cb, 1);
+  {
+    long long ib = 0;
+    for (auto& F : out.fr) { out.ibase.push_back(ib); ib += (long long)F.nbp * TB * TB; }
+    out.inv_doubles = std::max<long long>(ib, 1);
+    if (out.ibase.empty()) out.ibase.push_back(0);
+  }
   if (out.fr.empty()) return;
 
   // ---- tasks with predecessor lists (generation order is topological) ----
@@ -136,6 +201,7 @@ void build_tile_plan(const Plan& P, int workers, TilePlanHost& out) {
     const std::vector<int> p_asm;                        // (per-tile assembly dependencies)
     int diag_prod = add(1, f, 0, 0, 0, d_potrf, {last_upd[tl(0, 0, nt)]});  // POTRF0
     last_upd[tl(0, 0, nt)] = diag_prod;
+    add(5, f, 0, 0, 0, d_trsm, {diag_prod});                                  // INV(0)
     for (int k = 0; k < nbp; k++) {
       const bool crit = (k + 1 < nbp);
       std::fill(lprod.begin(), lprod.end(), -1);
@@ -170,71 +236,116 @@ void build_tile_plan(const Plan& P, int workers, TilePlanHost& out) {
             final_u[f][tl(i, j, nt) - tl(nbp, nbp, nt)] = id;
           }
         }
-      if (crit) { last_upd[tl(k + 1, k + 1, nt)] = crit_id; diag_prod = crit_id; }
-    }
-  }
-  const int N = (int)tasks.size();
-  // ---- bottom levels ----
-  std::vector<std::vector<int>> succ(N);
-  for (int t = 0; t < N; t++)
-    for (int p : pred[t]) succ[p].push_back(t);
-  std::vector<double> blev(N, 0.0);
-  for (int t = N - 1; t >= 0; t--) {
-    double m = 0.0;
-    for (int q : succ[t]) m = std::max(m, blev[q]);
-    blev[t] = tasks[t].dur + m;
-  }
-  // ---- list-scheduling simulation ----
-  std::vector<int> npred(N);
-  std::vector<double> ready_at(N, 0.0), fin(N, 0.0), start(N, 0.0);
-  for (int t = 0; t < N; t++) npred[t] = (int)pred[t].size();
-  using PQ = std::pair<double, int>;
-  auto cmp_prio = [&](int a, int b) { return blev[a] != blev[b] ? blev[a] < blev[b] : a > b; };
-  std::priority_queue<int, std::vector<int>, decltype(cmp_prio)> avail(cmp_prio);
-  std::priority_queue<PQ, std::vector<PQ>, std::greater<PQ>> pending;  // (ready time, task)
-  std::priority_queue<PQ, std::vector<PQ>, std::greater<PQ>> running;  // (finish time, task)
-  for (int t = 0; t < N; t++)
-    if (npred[t] == 0) pending.push({0.0, t});
-  int free_w = std::max(1, workers);
-  double now = 0.0;
-  std::vector<int> order;
-  order.reserve(N);
-  while ((int)order.size() < N) {
-    while (!pending.empty() && pending.top().first <= now) { avail.push(pending.top().second); pending.pop(); }
-    if (free_w > 0 && !avail.empty()) {
-      const int t = avail.top();
-      avail.pop();
-      start[t] = now;
-      fin[t] = now + tasks[t].dur;
-      running.push({fin[t], t});
-      order.push_back(t);
-      free_w--;
-      continue;
-    }
-    // advance time to the next event
-    double nxt = 1e300;
-    if (!running.empty()) nxt = running.top().first;
-    if (free_w > 0 && !pending.empty()) nxt = std::min(nxt, pending.top().first);
-    now = std::max(now, nxt);
-    while (!running.empty() && running.top().first <= now) {
-      const int t = running.top().second;
-      running.pop();
-      free_w++;
-      for (int q : succ[t]) {
-        ready_at[q] = std::max(ready_at[q], fin[t]);
-        if (--npred[q] == 0) pending.push({ready_at[q], q});
+      if (crit) {
+        last_upd[tl(k + 1, k + 1, nt)] = crit_id;
+        diag_prod = crit_id;
+        add(5, f, k + 1, k + 1, k + 1, d_trsm, {crit_id});                    // INV(k + 1)
       }
     }
   }
-  out.est_us = 0.0;
-  for (int t = 0; t < N; t++) out.est_us = std::max(out.est_us, fin[t]);
+  std::vector<int> order;
+  out.est_us = list_schedule(tasks, pred, workers, order);
+  const int N = (int)tasks.size();
   out.tasks.resize(N);
   for (int q = 0; q < N; q++) {
     const Task& T = tasks[order[q]];
     out.tasks[q] = TTask{T.type, T.f, T.i | (T.j << 16), T.k};
   }
-  out.ntask_by_type.assign(5, 0);
+  out.ntask_by_type.assign(6, 0);
   for (const Task& T : tasks) out.ntask_by_type[T.type]++;
+}
+
+}  // namespace kkt
+
+namespace kkt {
+
+void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, TSolvePlanHost& out) {
+  out = TSolvePlanHost();
+  const int nf = (int)tp.fr.size();
+  out.cbase2.resize(std::max(nf, 1));
+  out.pbase.resize(std::max(nf, 1));
+  int cb = 0;
+  long long pb = 0;
+  for (int f = 0; f < nf; f++) {
+    const TFrontHost& F = tp.fr[f];
+    out.cbase2[f] = cb;
+    cb += 2 * F.nt + 3 * F.nbp + 2;
+    out.pbase[f] = pb;
+    pb += ((long long)F.nt * F.nbp + (long long)F.nbp * (F.nbp + 1)) * TB;
+  }
+  out.ncnt = std::max(cb, 1);
+  out.part_doubles = std::max<long long>(pb, 1);
+  if (nf == 0) return;
+  struct STask { int type, f, i, k; double dur; };
+  std::vector<STask> tasks;
+  std::vector<std::vector<int>> pred;
+  auto add = [&](int type, int f, int i, int k, double dur, std::vector<int> p) {
+    tasks.push_back({type, f, i, k, dur});
+    pred.push_back(std::move(p));
+    return (int)tasks.size() - 1;
+  };
+  const double d_g = 2.0, d_u = 1.5, d_c = 2.5;
+  std::vector<std::vector<int>> ufinal(nf);
+  std::vector<std::vector<int>> fc(nf);
+  // ---- forward, fronts in postorder ----
+  for (int f = 0; f < nf; f++) {
+    const TFrontHost& F = tp.fr[f];
+    const int nt = F.nt, nbp = F.nbp;
+    std::vector<int> chp;
+    for (int q = 0; q < F.nch; q++) {
+      const int hc = tp.hidx[tp.tch[2 * (F.ch0 + q)]];
+      if (hc >= 0) chp.insert(chp.end(), ufinal[hc].begin(), ufinal[hc].end());
+    }
+    std::vector<int> g(nt);
+    for (int t = 0; t < nt; t++) g[t] = add(TS_G, f, t, 0, d_g, chp);
+    std::vector<std::vector<int>> prod(nt);     // producers of the partials P[t][.]
+    fc[f].assign(nbp, -1);
+    for (int k = 0; k < nbp; k++) {
+      std::vector<int> p = {g[k]};
+      p.insert(p.end(), prod[k].begin(), prod[k].end());
+      const int c = add(TS_C, f, k + 1, k, d_c, p);
+      fc[f][k] = c;
+      if (k + 1 < nt) prod[k + 1].push_back(c);
+      for (int i = k + 2; i < nt; i++) prod[i].push_back(add(TS_U, f, i, k, d_u, {c}));
+    }
+    for (int t = nbp; t < nt; t++) {
+      std::vector<int> p = {g[t]};
+      p.insert(p.end(), prod[t].begin(), prod[t].end());
+      ufinal[f].push_back(add(TS_UF, f, t, 0, d_g, p));
+    }
+  }
+  // ---- backward, fronts top-down (reverse postorder) ----
+  std::vector<int> xlast(nf, -1);
+  for (int f = nf - 1; f >= 0; f--) {
+    const TFrontHost& F = tp.fr[f];
+    const int nt = F.nt, nbp = F.nbp;
+    const int par = P.sn_parent[F.s];
+    const int hp = par >= 0 ? tp.hidx[par] : -1;
+    std::vector<std::vector<int>> q(nbp);       // producers of Q[k][.]
+    if (nt > nbp)
+      for (int k = 0; k < nbp; k++) {
+        std::vector<int> p;
+        if (hp >= 0) p.push_back(xlast[hp]);
+        q[k].push_back(add(TS_BU_, f, nt - 1, k, d_u * (nt - nbp), p));
+      }
+    int xprev = -1;
+    for (int k = nbp - 1; k >= 0; k--) {
+      std::vector<int> p = {fc[f][k]};
+      p.insert(p.end(), q[k].begin(), q[k].end());
+      if (xprev >= 0) p.push_back(xprev);
+      const int x = add(TS_BC_, f, k + 1, k, d_c, p);
+      xprev = x;
+      for (int j = k - 2; j >= 0; j--) q[j].push_back(add(TS_BU_, f, k, j, d_u, {x}));
+    }
+    xlast[f] = xprev;
+  }
+  std::vector<int> order;
+  out.est_us = list_schedule(tasks, pred, workers, order);
+  out.tasks.resize(tasks.size());
+  for (size_t qq = 0; qq < order.size(); qq++) {
+    const STask& T = tasks[order[qq]];
+    out.tasks[qq] = TTask{T.type, T.f, T.i, T.k};
+  }
 }
 
 }  // namespace kkt

@@ -33,7 +33,7 @@ namespace kkt {
 
 constexpr int TBS = 64;            // tile edge
 constexpr int TBD = TBS * TBS;     // doubles per tile
-constexpr int TASK_ASM = 0, TASK_POTRF0 = 1, TASK_TRSM = 2, TASK_CRIT = 3, TASK_UPD = 4;
+constexpr int TASK_ASM = 0, TASK_POTRF0 = 1, TASK_TRSM = 2, TASK_CRIT = 3, TASK_UPD = 4, TASK_INV = 5;
 constexpr int TILE_THREADS = 256;
 // shared memory of tile_factor_kernel: three swizzled tiles + 64 inverse pivots + scratch
 constexpr int TILE_SMEM_BYTES = (3 * TBD + 64 + 32 * 32 + 64) * 8 + 64;  // + 64 pivot signs (LDL^T)
@@ -61,6 +61,9 @@ struct TilePlan {
   double* pool;        // [batch][pool_doubles]
   int* cnt;            // [batch][ncnt] (zeroed before the launch) ; cnt[batch * ncnt] = ticket
   long long* trace;    // optional [ntask][4]: start, dependencies met, end (globaltimer ns), SM id
+  double* inv;         // [batch][inv_doubles]: (L_kk^-1)^T of every diagonal panel tile (solves)
+  long long inv_doubles;
+  const long long* ibase;  // [nf] offset of a front's nbp inverse tiles
 };
 
 __device__ __forceinline__ int tlin(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
@@ -435,6 +438,7 @@ struct TileCtx {
   int* cnt;
   int* fail_all;
   int task;           // ticket of the current task (trace)
+  double* inv;        // instance's inverse-diagonal-tile pool
   double* Sg;         // LDL^T: pivot signs of the instance (internal numbering)
   int* cnt3;          // LDL^T: (positive, negative, zero) pivot counts of the instance
 };
@@ -682,6 +686,25 @@ __device__ void task_upd(const TileCtx& X, const TFront& F, int i, int j, int k,
   publish_cnt(tile_cnt(X, F, i, j), k + 2);
 }
 
+// INV(f, k): (L_kk^-1)^T of the final diagonal tile for the triangular solves (tsolve.cuh):
+// the row solve of the identity, X = I L_kk^-T (tile_trsm64), off the factorisation's critical path
+__device__ void task_inv(const TileCtx& X, const TFront& F, int fidx, int k, double* sm) {
+  double *Lk = sm, *A = sm + TBD, *sinv = sm + 3 * TBD;
+  wait_cnt(tile_cnt(X, F, k, k), k + 2);
+  tile_load_async(Lk, tile_ptr(X, F, k, k));
+  load_sinv<false>(X, F, k, sinv);
+  for (int q = threadIdx.x; q < TBD; q += TILE_THREADS) {
+    const int col = q >> 6, row = q & 63;
+    A[tsw(row, col)] = (row == col) ? 1.0 : 0.0;
+  }
+  stamp_ready(X);
+  cp_async_wait_all();
+  __syncthreads();
+  tile_trsm64<false>(A, Lk, sinv);
+  tile_store(X.inv + X.T->ibase[fidx] + (long long)k * TBD, A);
+  __syncthreads();
+}
+
 template <bool SG>
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_factor_kernel(DevPlan P, TilePlan T, const double* __restrict__ Kv_all,
                                                                     double* Lx_all, const double* U_all, double* Dv_all,
@@ -713,6 +736,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_factor_kernel(DevPlan P,
     X.cnt = T.cnt + (long long)b * T.ncnt;
     X.fail_all = fail_all;
     X.task = t;
+    X.inv = T.inv + (long long)b * T.inv_doubles;
     X.Sg = SG ? P.Sg + (long long)b * P.n : nullptr;
     X.cnt3 = SG ? P.inert + 3 * b : nullptr;
     const TFront F = T.fr[tk.y];
@@ -722,6 +746,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_factor_kernel(DevPlan P,
       case TASK_POTRF0: task_potrf0<SG>(X, F, tsm); break;
       case TASK_TRSM: task_trsm<SG>(X, F, i, k, tsm); break;
       case TASK_CRIT: task_crit<SG>(X, F, k, tsm); break;
+      case TASK_INV: task_inv(X, F, tk.y, k, tsm); break;
       default: task_upd<SG>(X, F, i, j, k, tsm); break;
     }
     if (T.trace) {

@@ -1,0 +1,425 @@
+// tsolve.cuh -- triangular solves through the large fronts (the huge class of tiles.cuh) as a task
+// DAG over the 64 x 64 L tiles of the tile pool, on a persistent CTA grid (SURVEY
+// §8(a) a3).  Replaces the level-synchronous whole-GPU wavefront (hsolve.cuh) for these fronts.
+//
+// Front f (rows in blocks of 64 restarting at w, as the factorisation): forward y1 = L11^-1 v1,
+// u = v2 - L21 y1; backward x1 = L11^-T (y1 - L21^T x2).  Row block t of the front keeps its
+// working vector in the solve's own buffers: panel blocks in Y (internal numbering, y then z),
+// update blocks in the front's u vector (uv + uvp, read by the parent's gather).
+//
+// Forward tasks:  FG(f, t)   gather v_t = [P b]_t + sum over children (fixed order) of their u
+//                            entries landing in block t
+//                 FU(f,i,k)  partial P[i][k] = L_ik y_k (i >= k + 2) into its own slot: the
+//                            producers of one block run in any order, in parallel
+//                 FC(f, k)   chain step: r_k = v_k - sum_j P[k][j] (j ascending), y_k = L_kk^-1 r_k
+//                            with the inverse diagonal tile, publish; then P[k+1][k] itself
+//                 UF(f, t)   update block t >= nbp: u_t = v_t - sum_k P[t][k] (the parent reads it)
+// Backward tasks: BU(f,k,i)  partial Q[k][.] = L_ik^T x_i: all update rows in one task (after the
+//                            parent's backward), panel rows i >= k + 2 one each (after x_i)
+//                 BC(f, k)   chain step (k = nbp-1..0): z_k = y_k - Q[k][U] - sum_i Q[k][i]
+//                            (i descending) - L_{k+1,k}^T x_{k+1}, x_k = L_kk^-T z_k, write x
+// Counters per instance are zeroed before the launch; every task waits only on tasks earlier in
+// the list-schedule order (tile_plan.cpp), all workers resident: deadlock-free.  Every sum has a
+// fixed order (no floating-point atomics): deterministic, bitwise identical run to run.
+#pragma once
+#include "tiles.cuh"
+
+namespace kkt {
+
+constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF = 5;
+
+struct TSolvePlan {
+  const int4* tasks;   // x = type | (instance << 4), y = front, z = i, w = k
+  int ntask;
+  int ncnt;            // counters per instance
+  int* cnt;            // [batch][ncnt] + ticket at [batch * ncnt]
+  // per front f (counter layout from cbase2[f]): gf[nt] (block gathered), pc[nt] (forward
+  // partials present), yf[nbp] (y_k final), ufin (u blocks final), qc[nbp] (backward partials
+  // present), xf[nbp] (x_k final), xdone (x blocks final)
+  const int* cbase2;   // [nf]
+  long long* trace;    // optional [ntask][4]
+  double* part;        // [batch][part_doubles] partial products (one 64-slot per producer)
+  long long part_doubles;
+  const long long* pbase;  // [nf]: forward slots P[t][k] (nt x nbp x 64), then backward Q[k][s]
+                           // (nbp x (nbp + 1) x 64; s = source panel block i, or nbp = update rows)
+};
+
+__device__ __forceinline__ int* ts_gf(const TSolvePlan& S, int* cnt, const TFront& F, int f, int t) { return cnt + S.cbase2[f] + t; }
+__device__ __forceinline__ int* ts_pc(const TSolvePlan& S, int* cnt, const TFront& F, int f, int t) { return cnt + S.cbase2[f] + F.nt + t; }
+__device__ __forceinline__ int* ts_yf(const TSolvePlan& S, int* cnt, const TFront& F, int f, int k) { return cnt + S.cbase2[f] + 2 * F.nt + k; }
+__device__ __forceinline__ int* ts_ufin(const TSolvePlan& S, int* cnt, const TFront& F, int f) { return cnt + S.cbase2[f] + 2 * F.nt + F.nbp; }
+__device__ __forceinline__ int* ts_qc(const TSolvePlan& S, int* cnt, const TFront& F, int f, int k) { return cnt + S.cbase2[f] + 2 * F.nt + F.nbp + 1 + k; }
+__device__ __forceinline__ int* ts_xf(const TSolvePlan& S, int* cnt, const TFront& F, int f, int k) { return cnt + S.cbase2[f] + 2 * F.nt + 2 * F.nbp + 1 + k; }
+__device__ __forceinline__ int* ts_xdone(const TSolvePlan& S, int* cnt, const TFront& F, int f) { return cnt + S.cbase2[f] + 2 * F.nt + 3 * F.nbp + 1; }
+
+// working vector of row block t of front f: Y (panel) or the front's u vector
+__device__ __forceinline__ double* ts_vec(const TFront& F, const SnInfo& I, double* Y, double* uvb, int t) {
+  return t < F.nbp ? Y + I.f0 + t * TBS : uvb + I.uvp + (t - F.nbp) * TBS;
+}
+
+struct TSCtx {
+  const DevPlan* P;
+  const TilePlan* T;
+  const TSolvePlan* S;
+  const double* pool;
+  const double* inv;   // the instance's inverse diagonal tiles (L_kk^-1)^T
+  const double* Dv;
+  const double* rhs;
+  double* Y;
+  double* uvb;
+  double* Xp;
+  double* xout;
+  int* cnt;
+  double* part;        // the instance's partial-product slots
+};
+
+__device__ __forceinline__ double* ts_pslot(const TSCtx& X, const TFront& F, int f, int t, int k) {
+  return X.part + X.S->pbase[f] + ((long long)t * F.nbp + k) * TBS;
+}
+__device__ __forceinline__ double* ts_qslot(const TSCtx& X, const TFront& F, int f, int k, int src) {
+  return X.part + X.S->pbase[f] + (long long)F.nt * F.nbp * TBS + ((long long)k * (F.nbp + 1) + src) * TBS;
+}
+
+__device__ __forceinline__ void ts_wait(const int* c, int target) {
+  if (threadIdx.x == 0) {
+    while (ld_volatile(c) < target) { __nanosleep(32); }
+    fence_acq_rel();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void ts_publish(int* c, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0) { __threadfence(); st_release(c, v); }
+}
+__device__ __forceinline__ void ts_publish_add(int* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) { __threadfence(); red_release_add(c, 1); }
+}
+
+// r (64, shared) -= A (swizzled tile) x (64, shared): 4 threads per row, 16 columns each
+__device__ __forceinline__ void ts_gemv_n(double* r, const double* A, const double* x) {
+  const int row = threadIdx.x >> 2, q = threadIdx.x & 3;
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    const int col = q * 16 + c;
+    acc = fma(A[tsw(row, col)], x[col], acc);
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  __syncthreads();
+  if (q == 0) r[row] -= acc;
+  __syncthreads();
+}
+// z (64, shared) -= A^T x: 4 threads per column, 16 rows each
+__device__ __forceinline__ void ts_gemv_t(double* z, const double* A, const double* x) {
+  const int col = threadIdx.x >> 2, q = threadIdx.x & 3;
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    const int row = q * 16 + c;
+    acc = fma(A[tsw(row, col)], x[row], acc);
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  __syncthreads();
+  if (q == 0) z[col] -= acc;
+  __syncthreads();
+}
+// y = L^-1 r for a 64 x 64 lower-triangular swizzled tile with inverse pivots di (shared): warp 0,
+// lane = row, two 32-row halves (substitution) with a 32 x 32 product between them
+__device__ __forceinline__ void ts_lsolve(double* v, const double* L, const double* di, int nb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int row = 32 * h + lane;
+      double a = v[row];
+      if (h == 1) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < 32; c++) acc = fma(L[tsw(row, c)], v[c], acc);
+        a -= acc;
+      }
+      const double dr = di[row];
+#pragma unroll
+      for (int c = 0; c < 32; c++) {
+        const double yc = __shfl_sync(0xffffffffu, a * dr, c);
+        if (lane == c) a = yc;
+        else if (lane > c) a = fma(-L[tsw(row, 32 * h + c)], yc, a);
+      }
+      v[row] = (row < nb) ? a : 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+// x = L^-T z (same tile), warp 0, lane = column, halves 1 then 0
+__device__ __forceinline__ void ts_ltsolve(double* v, const double* L, const double* di, int nb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+#pragma unroll
+    for (int h = 1; h >= 0; h--) {
+      const int col = 32 * h + lane;
+      double a = v[col];
+      if (h == 0) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int r = 32; r < 64; r++) acc = fma(L[tsw(r, col)], v[r], acc);
+        a -= acc;
+      }
+      const double dc = di[col];
+#pragma unroll
+      for (int k = 31; k >= 0; k--) {
+        const double xk = __shfl_sync(0xffffffffu, a * dc, k);
+        if (lane == k) a = xk;
+        else if (lane < k) a = fma(-L[tsw(32 * h + k, col)], xk, a);
+      }
+      v[col] = (col < nb) ? a : 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ const double* ts_tile(const TSCtx& X, const TFront& F, int i, int j) {
+  return X.pool + F.tbase + (long long)tlin(i, j, F.nt) * TBD;
+}
+
+// FG(f, t): gather of row block t (children in fixed order) -> the block's working vector; gf = 1
+__device__ void ts_gather(const TSCtx& X, const TFront& F, int f, int t, double* sv) {
+  const DevPlan& P = *X.P;
+  const SnInfo I = P.sn[F.s];
+  const int r0 = trow0(F, t), nr = tsize(F, t);
+  if (threadIdx.x < F.nch) {  // huge children: their u blocks must be final
+    const int2 cr = X.T->tch[F.ch0 + threadIdx.x];
+    const int hc = __ldg(X.T->hidx + cr.x);
+    if (hc >= 0) {
+      const TFront C = X.T->fr[hc];
+      const int* u = ts_ufin(*X.S, X.cnt, C, hc);
+      while (ld_volatile(u) < C.nt - C.nbp) { __nanosleep(32); }
+      fence_acq_rel();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < TBS)
+    sv[threadIdx.x] = (t < F.nbp && threadIdx.x < nr) ? __ldg(X.rhs + __ldg(P.perm + I.f0 + r0 + threadIdx.x)) : 0.0;
+  for (int q = 0; q < F.nch; q++) {
+    const int2 cr = X.T->tch[F.ch0 + q];
+    const int* cut = X.T->tcut + cr.y;
+    const int a = __ldg(cut + t), b = __ldg(cut + t + 1);
+    __syncthreads();
+    if (b > a) {
+      const SnInfo C = P.sn[cr.x];
+      const int* rel = P.sn_rel + C.rp0 + C.w;
+      const double* u = X.uvb + C.uvp;
+      for (int e = a + threadIdx.x; e < b; e += TILE_THREADS) sv[__ldg(rel + e) - r0] += __ldcg(u + e);
+    }
+  }
+  __syncthreads();
+  double* v = ts_vec(F, I, X.Y, X.uvb, t);
+  if (threadIdx.x < nr) v[threadIdx.x] = sv[threadIdx.x];
+  ts_publish(ts_gf(*X.S, X.cnt, F, f, t), 1);
+}
+
+// r (64, shared) = v_t - sum_{k < nk} P[t][k] in fixed order (k ascending)
+__device__ __forceinline__ void ts_sum_partials(const TSCtx& X, const TFront& F, int f, int t, int nk, const double* v,
+                                                double* r) {
+  if (threadIdx.x < TBS) {
+    double a = v[threadIdx.x];
+    for (int k = 0; k < nk; k++) a -= __ldcg(ts_pslot(X, F, f, t, k) + threadIdx.x);
+    r[threadIdx.x] = a;
+  }
+  __syncthreads();
+}
+
+// FU(f, i, k): partial P[i][k] = L_ik y_k (no ordering among the producers of one block)
+__device__ void ts_fupdate(const TSCtx& X, const TFront& F, int f, int i, int k, double* sm) {
+  const SnInfo I = X.P->sn[F.s];
+  double *A = sm, *yv = sm + 3 * TBD, *pv = yv + 64;
+  tile_load_async(A, ts_tile(X, F, i, k));
+  ts_wait(ts_yf(*X.S, X.cnt, F, f, k), 1);
+  const int nk = tsize(F, k);
+  if (threadIdx.x < TBS) { yv[threadIdx.x] = threadIdx.x < nk ? __ldcg(X.Y + I.f0 + k * TBS + threadIdx.x) : 0.0; pv[threadIdx.x] = 0.0; }
+  cp_async_wait_all();
+  __syncthreads();
+  ts_gemv_n(pv, A, yv);                                   // pv = -L_ik y_k
+  if (threadIdx.x < TBS) ts_pslot(X, F, f, i, k)[threadIdx.x] = -pv[threadIdx.x];
+  ts_publish_add(ts_pc(*X.S, X.cnt, F, f, i));
+}
+
+// FC(f, k): chain step -- r_k = v_k - sum_j P[k][j], y_k = L_kk^-1 r_k (inverse tile), publish;
+// then the partial P[k+1][k] = L_{k+1,k} y_k for the next block
+__device__ void ts_fchain(const TSCtx& X, const TFront& F, int f, int k, double* sm) {
+  const SnInfo I = X.P->sn[F.s];
+  double *Xi = sm, *Lo = sm + TBD, *r = sm + 3 * TBD, *w = r + 64, *v = w + 64;
+  tile_load_async(Xi, X.inv + X.T->ibase[f] + (long long)k * TBD);   // (L_kk^-1)^T
+  if (k + 1 < F.nt) tile_load_async(Lo, ts_tile(X, F, k + 1, k));
+  const int nk = tsize(F, k);
+  ts_wait(ts_gf(*X.S, X.cnt, F, f, k), 1);
+  ts_wait(ts_pc(*X.S, X.cnt, F, f, k), k);
+  double* y = X.Y + I.f0 + k * TBS;
+  if (threadIdx.x < TBS) { w[threadIdx.x] = threadIdx.x < nk ? __ldcg(y + threadIdx.x) : 0.0; v[threadIdx.x] = 0.0; }
+  __syncthreads();
+  ts_sum_partials(X, F, f, k, k, w, r);
+  cp_async_wait_all();
+  __syncthreads();
+  ts_gemv_t(v, Xi, r);                              // v = -(L_kk^-1 r): y = -v
+  if (threadIdx.x < TBS) { v[threadIdx.x] = -v[threadIdx.x]; w[threadIdx.x] = 0.0; }
+  __syncthreads();
+  if (threadIdx.x < nk) y[threadIdx.x] = v[threadIdx.x];
+  ts_publish(ts_yf(*X.S, X.cnt, F, f, k), 1);
+  if (k + 1 < F.nt) {
+    ts_gemv_n(w, Lo, v);                            // w = -L_{k+1,k} y_k
+    if (threadIdx.x < TBS) ts_pslot(X, F, f, k + 1, k)[threadIdx.x] = -w[threadIdx.x];
+    ts_publish_add(ts_pc(*X.S, X.cnt, F, f, k + 1));
+  }
+}
+
+// UF(f, t), t >= nbp: u_t = v_t - sum_k P[t][k] (k ascending) -> the front's u vector; ufin++
+__device__ void ts_ufinal(const TSCtx& X, const TFront& F, int f, int t, double* sm) {
+  const SnInfo I = X.P->sn[F.s];
+  double *v = sm + 3 * TBD, *r = v + 64;
+  ts_wait(ts_gf(*X.S, X.cnt, F, f, t), 1);
+  ts_wait(ts_pc(*X.S, X.cnt, F, f, t), F.nbp);
+  double* u = ts_vec(F, I, X.Y, X.uvb, t);
+  const int nr = tsize(F, t);
+  if (threadIdx.x < TBS) v[threadIdx.x] = threadIdx.x < nr ? __ldcg(u + threadIdx.x) : 0.0;
+  __syncthreads();
+  ts_sum_partials(X, F, f, t, F.nbp, v, r);
+  if (threadIdx.x < nr) u[threadIdx.x] = r[threadIdx.x];
+  ts_publish_add(ts_ufin(*X.S, X.cnt, F, f));
+}
+
+// backward: x of row r of front f's update rows (ancestor columns, final after the parent)
+__device__ __forceinline__ double ts_xanc(const TSCtx& X, const SnInfo& I, const TFront& F, int row) {
+  return __ldcg(X.Xp + __ldg(X.P->sn_rows + I.rp0 + row));
+}
+
+// BU(f, k, i): backward partial Q[k][s] = L_ik^T x_i.  i >= nbp: one task for all update rows
+// (i descending nt-1..nbp, tiles double-buffered; slot s = nbp) once the parent's backward is
+// done; i < nbp: one panel row block (after x_i; slot s = i)
+__device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i, double* sm) {
+  const SnInfo I = X.P->sn[F.s];
+  double *A0 = sm, *A1 = sm + TBD, *xv = sm + 3 * TBD, *zv = xv + 64;
+  const bool urows = (i >= F.nbp);
+  const int i_hi = urows ? F.nt - 1 : i, i_lo = urows ? F.nbp : i;
+  tile_load_async(A0, ts_tile(X, F, i_hi, k));
+  if (urows) {
+    if (I.par >= 0) {
+      const int hp = __ldg(X.T->hidx + I.par);
+      const TFront Pf = X.T->fr[hp];
+      ts_wait(ts_xdone(*X.S, X.cnt, Pf, hp), Pf.nbp);
+    }
+  } else {
+    ts_wait(ts_xf(*X.S, X.cnt, F, f, i), 1);
+  }
+  if (threadIdx.x < TBS) zv[threadIdx.x] = 0.0;
+  for (int ii = i_hi; ii >= i_lo; ii--) {
+    double* cur = ((i_hi - ii) & 1) ? A1 : A0;
+    double* nxt = ((i_hi - ii) & 1) ? A0 : A1;
+    const int nr = tsize(F, ii), r0 = trow0(F, ii);
+    if (threadIdx.x < TBS) {
+      const int q = threadIdx.x;
+      xv[q] = q < nr ? (urows ? ts_xanc(X, I, F, r0 + q) : __ldcg(X.Xp + I.f0 + r0 + q)) : 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (ii > i_lo) tile_load_async(nxt, ts_tile(X, F, ii - 1, k));  // next tile in flight
+    ts_gemv_t(zv, cur, xv);                                          // zv -= L^T x
+  }
+  if (threadIdx.x < TBS) ts_qslot(X, F, f, k, urows ? F.nbp : i)[threadIdx.x] = -zv[threadIdx.x];
+  ts_publish_add(ts_qc(*X.S, X.cnt, F, f, k));
+}
+
+// BC(f, k): chain step -- z_k = y_k - Q[k][U] - sum_{i = nbp-1 .. k+2} Q[k][i] - L_{k+1,k}^T x_{k+1}
+// (that fixed order), x_k = L_kk^-T z_k (inverse tile), written to Xp and xout
+__device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double* sm) {
+  const DevPlan& P = *X.P;
+  const SnInfo I = P.sn[F.s];
+  double *Xi = sm, *Lo = sm + TBD, *v = sm + 3 * TBD, *xn = v + 64, *o = xn + 64;
+  tile_load_async(Xi, X.inv + X.T->ibase[f] + (long long)k * TBD);   // (L_kk^-1)^T
+  const int own = (k + 1 < F.nbp) ? 1 : 0;
+  if (own) tile_load_async(Lo, ts_tile(X, F, k + 1, k));
+  const int nk = tsize(F, k);
+  const int hasu = F.nt > F.nbp ? 1 : 0;
+  const int npanel = max(F.nbp - k - 2, 0);
+  ts_wait(ts_yf(*X.S, X.cnt, F, f, k), 1);
+  if (own) {
+    ts_wait(ts_xf(*X.S, X.cnt, F, f, k + 1), 1);
+    if (threadIdx.x < TBS)
+      xn[threadIdx.x] = threadIdx.x < tsize(F, k + 1) ? __ldcg(X.Xp + I.f0 + (k + 1) * TBS + threadIdx.x) : 0.0;
+  }
+  ts_wait(ts_qc(*X.S, X.cnt, F, f, k), hasu + npanel);
+  if (threadIdx.x < TBS) {
+    double a = threadIdx.x < nk ? __ldcg(X.Y + I.f0 + k * TBS + threadIdx.x) : 0.0;
+    if (hasu) a -= __ldcg(ts_qslot(X, F, f, k, F.nbp) + threadIdx.x);
+    for (int i = F.nbp - 1; i >= k + 2; i--) a -= __ldcg(ts_qslot(X, F, f, k, i) + threadIdx.x);
+    v[threadIdx.x] = a;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (own) ts_gemv_t(v, Lo, xn);
+  if (threadIdx.x < TBS) o[threadIdx.x] = 0.0;
+  __syncthreads();
+  ts_gemv_n(o, Xi, v);                              // o = -(L_kk^-T z)
+  if (threadIdx.x < TBS) v[threadIdx.x] = -o[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < nk) {
+    const int c = I.f0 + k * TBS + threadIdx.x;
+    X.Xp[c] = v[threadIdx.x];
+    X.xout[__ldg(P.perm + c)] = v[threadIdx.x];
+  }
+  ts_publish(ts_xf(*X.S, X.cnt, F, f, k), 1);
+  ts_publish_add(ts_xdone(*X.S, X.cnt, F, f));
+}
+
+__global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, TilePlan T, TSolvePlan S,
+                                                                   const double* __restrict__ Dv_all,
+                                                                   const double* __restrict__ rhs, long long rs,
+                                                                   double* Y_all, double* uv_all, double* Xp_all,
+                                                                   double* xout, long long xs,
+                                                                   const int* __restrict__ done) {
+  extern __shared__ __align__(16) double tsm[];
+  __shared__ int s_task;
+  if (done && done[P.batch] == 0) return;  // every instance has finished refining (grid-uniform)
+  int* ticket = S.cnt + (long long)P.batch * S.ncnt;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_task = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int t = s_task;
+    if (t >= S.ntask) break;
+    const int4 tk = S.tasks[t];
+    const int type = tk.x & 15, b = tk.x >> 4;
+    if (done && done[b]) continue;   // finished instance: all its tasks skip (no dependents run)
+    if (S.trace && threadIdx.x == 0) S.trace[4LL * t] = gtimer();
+    TSCtx X;
+    X.P = &P; X.T = &T; X.S = &S;
+    X.pool = T.pool + (long long)b * T.pool_doubles;
+    X.inv = T.inv + (long long)b * T.inv_doubles;
+    X.Dv = Dv_all + (long long)b * P.n;
+    X.rhs = rhs + (long long)b * rs;
+    X.Y = Y_all + (long long)b * P.n;
+    X.uvb = uv_all + (long long)b * P.uvec_doubles;
+    X.Xp = Xp_all + (long long)b * P.n;
+    X.xout = xout + (long long)b * xs;
+    X.cnt = S.cnt + (long long)b * S.ncnt;
+    X.part = S.part + (long long)b * S.part_doubles;
+    const TFront F = T.fr[tk.y];
+    switch (type) {
+      case TS_GATHER: ts_gather(X, F, tk.y, tk.z, tsm); break;
+      case TS_FU: ts_fupdate(X, F, tk.y, tk.z, tk.w, tsm); break;
+      case TS_FC: ts_fchain(X, F, tk.y, tk.w, tsm); break;
+      case TS_BU: ts_bupdate(X, F, tk.y, tk.w, tk.z, tsm); break;
+      case TS_UF: ts_ufinal(X, F, tk.y, tk.z, tsm); break;
+      default: ts_bchain(X, F, tk.y, tk.w, tsm); break;
+    }
+    if (S.trace) {
+      __syncthreads();
+      if (threadIdx.x == 0) S.trace[4LL * t + 2] = gtimer();
+    }
+  }
+}
+
+}  // namespace kkt

@@ -22,7 +22,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
            "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
-           "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_last_error", "kkt_destroy"]
+           "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_tile_solve_trace", "kkt_last_error", "kkt_destroy"]
 
 
 class KKTError(RuntimeError):
@@ -90,6 +90,7 @@ def lib(build_if_missing: bool = True):
             "kkt_factor_phase_ms": [P, P],
             "kkt_debug_steps": [P, P, I],
             "kkt_tile_trace": [P, P, P, I, P],
+            "kkt_tile_solve_trace": [P, P, P, I, P],
             "kkt_destroy": [P],
         }
         for name, args in sig.items():
@@ -261,15 +262,17 @@ def kkt_factor_phase_ms(h):
     return float(ms[0]), float(ms[1])
 
 
-def kkt_tile_trace(h, want_trace=True):
-    """(tasks [N, 4] int32, trace [N, 4] int64 or None, estimated makespan us) of the tile kernel."""
+def kkt_tile_trace(h, want_trace=True, solve=False):
+    """(tasks [N, 4] int32, trace [N, 4] int64 or None, estimated makespan us) of the tile kernel
+    (solve=True: of the tile-task solve)."""
+    fn = lib().kkt_tile_solve_trace if solve else lib().kkt_tile_trace
     est = C.c_double(0.0)
-    n = lib().kkt_tile_trace(h, None, None, 0, C.byref(est))
+    n = fn(h, None, None, 0, C.byref(est))
     if n < 0:
         raise KKTError(8, "kkt_tile_trace")
     tasks = np.zeros((max(n, 1), 4), np.int32)
     tr = np.zeros((max(n, 1), 4), np.int64) if want_trace else None
-    rc = lib().kkt_tile_trace(h, tr.ctypes.data if want_trace else None, tasks.ctypes.data, n, C.byref(est))
+    rc = fn(h, tr.ctypes.data if want_trace else None, tasks.ctypes.data, n, C.byref(est))
     if rc < 0:
         raise KKTError(8, "kkt_tile_trace")
     return tasks[:n], (tr[:n] if want_trace else None), est.value

@@ -422,3 +422,18 @@ def test_inertia_correction_matches_oracle(factor_kind):
     R = oracle.reference_solve(shifted)
     assert info["status"] == 0 and relerr(x.cpu().numpy(), R["x"]) <= 1e-8
     S.close()
+
+
+def test_warp_residual_variant(monkeypatch):
+    """The warp-per-column double-double residual (chosen for long columns, e.g. dense elec)
+    forced on C2s: oracle parity and deterministic (bitwise equal on a repeat)."""
+    from kkt_gpu import run_lifted, relerr
+    monkeypatch.setenv("KKT_RESID_WARP", "1")
+    inst = make_config("C2s")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-12, relerr(x, R["x"])
+    x2, _, _ = run_lifted(inst, max_refine=10, solver=S)
+    assert np.array_equal(x, x2)
+    S.close()

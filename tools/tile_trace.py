@@ -13,22 +13,27 @@ from paper_2405_14236_b200 import kkt as KK
 from synth.generator import make_config
 
 cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "C4"
+SOLVE = "--solve" in sys.argv
 inst = make_config(cfg)
 S = K.KKTSolver.from_instance(inst).bind(0)
 d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda:0")
 W, J, Sx, Ss = d(inst.W_vals), d(inst.J_vals), d(inst.Sigma_x), d(inst.Sigma_s)
+b = d(inst.b)
+xs = torch.zeros_like(b)
 for _ in range(3):
     S.condense(W, J, Sx, Ss, None, inst.delta_w, inst.delta_c, inst.gamma)
     S.factor()
+    if SOLVE:
+        S.solve(b, xs, 0, 0.0)
 torch.cuda.synchronize()
 print("factor phase ms (small+big, large):", S.factor_phase_ms())
-tasks, tr, est = KK.kkt_tile_trace(S.h)
+tasks, tr, est = KK.kkt_tile_trace(S.h, solve=SOLVE)
 tr = tr.astype(np.float64)
 t0 = tr[:, 0].min()
 st, rd, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
 rd = np.where(tr[:, 1] > 0, rd, st)      # no wait recorded -> ready at start
 typ = tasks[:, 0] & 15
-names = ["ASM", "POTRF0", "TRSM", "CRIT", "UPD"]
+names = ["FG", "FU", "FC", "BU", "BC"] if SOLVE else ["ASM", "POTRF0", "TRSM", "CRIT", "UPD"]
 span = en.max()
 print(f"tasks {len(tasks)}  span {span:.1f} us  (list-schedule estimate {est:.1f} us)")
 busy = (en - st).sum()
