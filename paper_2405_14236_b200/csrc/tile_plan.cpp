@@ -271,7 +271,7 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
     out.cbase2[f] = cb;
     cb += 2 * F.nt + 3 * F.nbp + 2;
     out.pbase[f] = pb;
-    pb += ((long long)F.nt * F.nbp + (long long)F.nbp * (F.nbp + 1)) * TB;
+    pb += ((long long)F.nt * F.nbp + (long long)F.nbp * F.nt) * TB;
   }
   out.ncnt = std::max(cb, 1);
   out.part_doubles = std::max<long long>(pb, 1);
@@ -285,19 +285,24 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
     return (int)tasks.size() - 1;
   };
   const double d_g = 2.0, d_u = 1.5, d_c = 2.5;
-  std::vector<std::vector<int>> ufinal(nf);
+  std::vector<std::vector<std::vector<int>>> ublk(nf);   // per U block: its gather + partial producers
   std::vector<std::vector<int>> fc(nf);
   // ---- forward, fronts in postorder ----
   for (int f = 0; f < nf; f++) {
     const TFrontHost& F = tp.fr[f];
     const int nt = F.nt, nbp = F.nbp;
-    std::vector<int> chp;
-    for (int q = 0; q < F.nch; q++) {
-      const int hc = tp.hidx[tp.tch[2 * (F.ch0 + q)]];
-      if (hc >= 0) chp.insert(chp.end(), ufinal[hc].begin(), ufinal[hc].end());
-    }
     std::vector<int> g(nt);
-    for (int t = 0; t < nt; t++) g[t] = add(TS_G, f, t, 0, d_g, chp);
+    for (int t = 0; t < nt; t++) {   // the gather waits for the child blocks feeding parent block t
+      std::vector<int> chp;
+      for (int q = 0; q < F.nch; q++) {
+        const int hc = tp.hidx[tp.tch[2 * (F.ch0 + q)]];
+        const int* cut = &tp.tcut[tp.tch[2 * (F.ch0 + q) + 1]];
+        if (hc < 0 || cut[t + 1] <= cut[t]) continue;
+        for (int tc = cut[t] >> 6; tc <= (cut[t + 1] - 1) >> 6; tc++)
+          chp.insert(chp.end(), ublk[hc][tc].begin(), ublk[hc][tc].end());
+      }
+      g[t] = add(TS_G, f, t, 0, d_g, chp);
+    }
     std::vector<std::vector<int>> prod(nt);     // producers of the partials P[t][.]
     fc[f].assign(nbp, -1);
     for (int k = 0; k < nbp; k++) {
@@ -311,7 +316,7 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
     for (int t = nbp; t < nt; t++) {
       std::vector<int> p = {g[t]};
       p.insert(p.end(), prod[t].begin(), prod[t].end());
-      ufinal[f].push_back(add(TS_UF, f, t, 0, d_g, p));
+      ublk[f].push_back(p);
     }
   }
   // ---- backward, fronts top-down (reverse postorder) ----
@@ -322,11 +327,12 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
     const int par = P.sn_parent[F.s];
     const int hp = par >= 0 ? tp.hidx[par] : -1;
     std::vector<std::vector<int>> q(nbp);       // producers of Q[k][.]
-    if (nt > nbp)
-      for (int k = 0; k < nbp; k++) {
+    const int UCH = 2;   // tsolve.cuh TS_UCHUNK
+    for (int k = 0; k < nbp; k++)       // update rows in chunks of UCH tiles, parallel
+      for (int c0 = nbp; c0 < nt; c0 += UCH) {
         std::vector<int> p;
         if (hp >= 0) p.push_back(xlast[hp]);
-        q[k].push_back(add(TS_BU_, f, nt - 1, k, d_u * (nt - nbp), p));
+        q[k].push_back(add(TS_BU_, f, c0, k, d_u * std::min(UCH, nt - c0), p));
       }
     int xprev = -1;
     for (int k = nbp - 1; k >= 0; k--) {

@@ -13,11 +13,13 @@
 //                            producers of one block run in any order, in parallel
 //                 FC(f, k)   chain step: r_k = v_k - sum_j P[k][j] (j ascending), y_k = L_kk^-1 r_k
 //                            with the inverse diagonal tile, publish; then P[k+1][k] itself
-//                 UF(f, t)   update block t >= nbp: u_t = v_t - sum_k P[t][k] (the parent reads it)
-// Backward tasks: BU(f,k,i)  partial Q[k][.] = L_ik^T x_i: all update rows in one task (after the
-//                            parent's backward), panel rows i >= k + 2 one each (after x_i)
-//                 BC(f, k)   chain step (k = nbp-1..0): z_k = y_k - Q[k][U] - sum_i Q[k][i]
-//                            (i descending) - L_{k+1,k}^T x_{k+1}, x_k = L_kk^-T z_k, write x
+//                 (the update blocks t >= nbp are finalised by the parent's gathers:
+//                 u_t = v_t - sum_k P[t][k], k ascending)
+// Backward tasks: BU(f,k,i)  partial Q[k][.] = L_ik^T x_i: update rows in chunks of TS_UCHUNK tiles
+//                            (after the parent's backward), panel rows i >= k + 2 one each
+//                 BC(f, k)   chain step (k = nbp-1..0): z_k = y_k - sum over update chunks (last
+//                            first) - sum_i Q[k][i] (i descending) - L_{k+1,k}^T x_{k+1},
+//                            x_k = L_kk^-T z_k, write x
 // Counters per instance are zeroed before the launch; every task waits only on tasks earlier in
 // the list-schedule order (tile_plan.cpp), all workers resident: deadlock-free.  Every sum has a
 // fixed order (no floating-point atomics): deterministic, bitwise identical run to run.
@@ -27,6 +29,7 @@
 namespace kkt {
 
 constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF = 5;
+constexpr int TS_UCHUNK = 2;   // update-row tiles per backward task (parallel chunks, one slot each)
 
 struct TSolvePlan {
   const int4* tasks;   // x = type | (instance << 4), y = front, z = i, w = k
@@ -41,7 +44,7 @@ struct TSolvePlan {
   double* part;        // [batch][part_doubles] partial products (one 64-slot per producer)
   long long part_doubles;
   const long long* pbase;  // [nf]: forward slots P[t][k] (nt x nbp x 64), then backward Q[k][s]
-                           // (nbp x (nbp + 1) x 64; s = source panel block i, or nbp = update rows)
+                           // (nbp x nt x 64; s = source panel block i, or nbp + c = update-row chunk c)
 };
 
 __device__ __forceinline__ int* ts_gf(const TSolvePlan& S, int* cnt, const TFront& F, int f, int t) { return cnt + S.cbase2[f] + t; }
@@ -71,13 +74,18 @@ struct TSCtx {
   double* xout;
   int* cnt;
   double* part;        // the instance's partial-product slots
+  int task;            // ticket (trace)
 };
+// trace: all waits of the current task are over (slot 1)
+__device__ __forceinline__ void ts_ready(const TSCtx& X) {
+  if (X.S->trace && threadIdx.x == 0) X.S->trace[4LL * X.task + 1] = gtimer();
+}
 
 __device__ __forceinline__ double* ts_pslot(const TSCtx& X, const TFront& F, int f, int t, int k) {
   return X.part + X.S->pbase[f] + ((long long)t * F.nbp + k) * TBS;
 }
 __device__ __forceinline__ double* ts_qslot(const TSCtx& X, const TFront& F, int f, int k, int src) {
-  return X.part + X.S->pbase[f] + (long long)F.nt * F.nbp * TBS + ((long long)k * (F.nbp + 1) + src) * TBS;
+  return X.part + X.S->pbase[f] + (long long)F.nt * F.nbp * TBS + ((long long)k * F.nt + src) * TBS;
 }
 
 __device__ __forceinline__ void ts_wait(const int* c, int target) {
@@ -186,22 +194,31 @@ __device__ __forceinline__ const double* ts_tile(const TSCtx& X, const TFront& F
   return X.pool + F.tbase + (long long)tlin(i, j, F.nt) * TBD;
 }
 
-// FG(f, t): gather of row block t (children in fixed order) -> the block's working vector; gf = 1
+// FG(f, t): gather of row block t (children in fixed order) -> the block's working vector; gf = 1.
+// A huge child's update entries are finalised here: u_e = v_e - sum_k P_child[t_c][k] (k ascending)
+// once the child's blocks t_c covering them have all their partial products (no separate task).
 __device__ void ts_gather(const TSCtx& X, const TFront& F, int f, int t, double* sv) {
   const DevPlan& P = *X.P;
   const SnInfo I = P.sn[F.s];
   const int r0 = trow0(F, t), nr = tsize(F, t);
-  if (threadIdx.x < F.nch) {  // huge children: their u blocks must be final
+  if (threadIdx.x < F.nch) {  // huge children: the blocks feeding this one must be complete
     const int2 cr = X.T->tch[F.ch0 + threadIdx.x];
     const int hc = __ldg(X.T->hidx + cr.x);
-    if (hc >= 0) {
+    const int* cut = X.T->tcut + cr.y;
+    const int a = __ldg(cut + t), b = __ldg(cut + t + 1);
+    if (hc >= 0 && b > a) {
       const TFront C = X.T->fr[hc];
-      const int* u = ts_ufin(*X.S, X.cnt, C, hc);
-      while (ld_volatile(u) < C.nt - C.nbp) { __nanosleep(32); }
+      for (int tc = C.nbp + (a >> 6); tc <= C.nbp + ((b - 1) >> 6); tc++) {
+        const int* g = ts_gf(*X.S, X.cnt, C, hc, tc);
+        const int* pc = ts_pc(*X.S, X.cnt, C, hc, tc);
+        while (ld_volatile(g) < 1) { __nanosleep(32); }
+        while (ld_volatile(pc) < C.nbp) { __nanosleep(32); }
+      }
       fence_acq_rel();
     }
   }
   __syncthreads();
+  ts_ready(X);
   if (threadIdx.x < TBS)
     sv[threadIdx.x] = (t < F.nbp && threadIdx.x < nr) ? __ldg(X.rhs + __ldg(P.perm + I.f0 + r0 + threadIdx.x)) : 0.0;
   for (int q = 0; q < F.nch; q++) {
@@ -213,7 +230,19 @@ __device__ void ts_gather(const TSCtx& X, const TFront& F, int f, int t, double*
       const SnInfo C = P.sn[cr.x];
       const int* rel = P.sn_rel + C.rp0 + C.w;
       const double* u = X.uvb + C.uvp;
-      for (int e = a + threadIdx.x; e < b; e += TILE_THREADS) sv[__ldg(rel + e) - r0] += __ldcg(u + e);
+      const int hc = __ldg(X.T->hidx + cr.x);
+      if (hc >= 0) {
+        const TFront Cf = X.T->fr[hc];
+        for (int e = a + threadIdx.x; e < b; e += TILE_THREADS) {
+          double val = __ldcg(u + e);
+          const double* p0 = X.part + X.S->pbase[hc] + ((long long)(Cf.nbp + (e >> 6)) * Cf.nbp) * TBS + (e & 63);
+#pragma unroll 8
+          for (int k = 0; k < Cf.nbp; k++) val -= __ldcg(p0 + (long long)k * TBS);
+          sv[__ldg(rel + e) - r0] += val;
+        }
+      } else {
+        for (int e = a + threadIdx.x; e < b; e += TILE_THREADS) sv[__ldg(rel + e) - r0] += __ldcg(u + e);
+      }
     }
   }
   __syncthreads();
@@ -227,7 +256,9 @@ __device__ __forceinline__ void ts_sum_partials(const TSCtx& X, const TFront& F,
                                                 double* r) {
   if (threadIdx.x < TBS) {
     double a = v[threadIdx.x];
-    for (int k = 0; k < nk; k++) a -= __ldcg(ts_pslot(X, F, f, t, k) + threadIdx.x);
+    const double* p0 = ts_pslot(X, F, f, t, 0) + threadIdx.x;
+#pragma unroll 8
+    for (int k = 0; k < nk; k++) a -= __ldcg(p0 + (long long)k * TBS);   // loads in flight, fixed order
     r[threadIdx.x] = a;
   }
   __syncthreads();
@@ -239,6 +270,7 @@ __device__ void ts_fupdate(const TSCtx& X, const TFront& F, int f, int i, int k,
   double *A = sm, *yv = sm + 3 * TBD, *pv = yv + 64;
   tile_load_async(A, ts_tile(X, F, i, k));
   ts_wait(ts_yf(*X.S, X.cnt, F, f, k), 1);
+  ts_ready(X);
   const int nk = tsize(F, k);
   if (threadIdx.x < TBS) { yv[threadIdx.x] = threadIdx.x < nk ? __ldcg(X.Y + I.f0 + k * TBS + threadIdx.x) : 0.0; pv[threadIdx.x] = 0.0; }
   cp_async_wait_all();
@@ -258,6 +290,7 @@ __device__ void ts_fchain(const TSCtx& X, const TFront& F, int f, int k, double*
   const int nk = tsize(F, k);
   ts_wait(ts_gf(*X.S, X.cnt, F, f, k), 1);
   ts_wait(ts_pc(*X.S, X.cnt, F, f, k), k);
+  ts_ready(X);
   double* y = X.Y + I.f0 + k * TBS;
   if (threadIdx.x < TBS) { w[threadIdx.x] = threadIdx.x < nk ? __ldcg(y + threadIdx.x) : 0.0; v[threadIdx.x] = 0.0; }
   __syncthreads();
@@ -282,6 +315,7 @@ __device__ void ts_ufinal(const TSCtx& X, const TFront& F, int f, int t, double*
   double *v = sm + 3 * TBD, *r = v + 64;
   ts_wait(ts_gf(*X.S, X.cnt, F, f, t), 1);
   ts_wait(ts_pc(*X.S, X.cnt, F, f, t), F.nbp);
+  ts_ready(X);
   double* u = ts_vec(F, I, X.Y, X.uvb, t);
   const int nr = tsize(F, t);
   if (threadIdx.x < TBS) v[threadIdx.x] = threadIdx.x < nr ? __ldcg(u + threadIdx.x) : 0.0;
@@ -303,7 +337,9 @@ __device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i,
   const SnInfo I = X.P->sn[F.s];
   double *A0 = sm, *A1 = sm + TBD, *xv = sm + 3 * TBD, *zv = xv + 64;
   const bool urows = (i >= F.nbp);
-  const int i_hi = urows ? F.nt - 1 : i, i_lo = urows ? F.nbp : i;
+  const int chunk = urows ? (i - F.nbp) / TS_UCHUNK : 0;
+  const int i_lo = urows ? F.nbp + chunk * TS_UCHUNK : i;
+  const int i_hi = urows ? min(F.nt - 1, i_lo + TS_UCHUNK - 1) : i;
   tile_load_async(A0, ts_tile(X, F, i_hi, k));
   if (urows) {
     if (I.par >= 0) {
@@ -314,6 +350,7 @@ __device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i,
   } else {
     ts_wait(ts_xf(*X.S, X.cnt, F, f, i), 1);
   }
+  ts_ready(X);
   if (threadIdx.x < TBS) zv[threadIdx.x] = 0.0;
   for (int ii = i_hi; ii >= i_lo; ii--) {
     double* cur = ((i_hi - ii) & 1) ? A1 : A0;
@@ -328,7 +365,7 @@ __device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i,
     if (ii > i_lo) tile_load_async(nxt, ts_tile(X, F, ii - 1, k));  // next tile in flight
     ts_gemv_t(zv, cur, xv);                                          // zv -= L^T x
   }
-  if (threadIdx.x < TBS) ts_qslot(X, F, f, k, urows ? F.nbp : i)[threadIdx.x] = -zv[threadIdx.x];
+  if (threadIdx.x < TBS) ts_qslot(X, F, f, k, urows ? F.nbp + chunk : i)[threadIdx.x] = -zv[threadIdx.x];
   ts_publish_add(ts_qc(*X.S, X.cnt, F, f, k));
 }
 
@@ -342,7 +379,7 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
   const int own = (k + 1 < F.nbp) ? 1 : 0;
   if (own) tile_load_async(Lo, ts_tile(X, F, k + 1, k));
   const int nk = tsize(F, k);
-  const int hasu = F.nt > F.nbp ? 1 : 0;
+  const int nchunk = (F.nt - F.nbp + TS_UCHUNK - 1) / TS_UCHUNK;
   const int npanel = max(F.nbp - k - 2, 0);
   ts_wait(ts_yf(*X.S, X.cnt, F, f, k), 1);
   if (own) {
@@ -350,11 +387,15 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
     if (threadIdx.x < TBS)
       xn[threadIdx.x] = threadIdx.x < tsize(F, k + 1) ? __ldcg(X.Xp + I.f0 + (k + 1) * TBS + threadIdx.x) : 0.0;
   }
-  ts_wait(ts_qc(*X.S, X.cnt, F, f, k), hasu + npanel);
+  ts_wait(ts_qc(*X.S, X.cnt, F, f, k), nchunk + npanel);
+  ts_ready(X);
   if (threadIdx.x < TBS) {
     double a = threadIdx.x < nk ? __ldcg(X.Y + I.f0 + k * TBS + threadIdx.x) : 0.0;
-    if (hasu) a -= __ldcg(ts_qslot(X, F, f, k, F.nbp) + threadIdx.x);
-    for (int i = F.nbp - 1; i >= k + 2; i--) a -= __ldcg(ts_qslot(X, F, f, k, i) + threadIdx.x);
+    const double* q0 = ts_qslot(X, F, f, k, 0) + threadIdx.x;
+#pragma unroll 8
+    for (int c = nchunk - 1; c >= 0; c--) a -= __ldcg(q0 + (long long)(F.nbp + c) * TBS);
+#pragma unroll 8
+    for (int i = F.nbp - 1; i >= k + 2; i--) a -= __ldcg(q0 + (long long)i * TBS);
     v[threadIdx.x] = a;
   }
   cp_async_wait_all();
@@ -406,6 +447,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, 
     X.xout = xout + (long long)b * xs;
     X.cnt = S.cnt + (long long)b * S.ncnt;
     X.part = S.part + (long long)b * S.part_doubles;
+    X.task = t;
     const TFront F = T.fr[tk.y];
     switch (type) {
       case TS_GATHER: ts_gather(X, F, tk.y, tk.z, tsm); break;
