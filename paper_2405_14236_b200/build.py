@@ -23,6 +23,16 @@ def deps():
         [os.path.join(ROOT, "include", "kkt.h")]
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """Tuning experiments: the same sources with extra -D flags into another in-tree .so."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + ["-D" + d for d in defines] + sources() + ["-o", out]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO):
         t = os.path.getmtime(SO)

@@ -122,6 +122,37 @@ __device__ __forceinline__ void copy_g2s(T* dst, const T* src, int n, int tid, i
 // producer data written earlier in the same launch by another CTA: bypass L1
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
+// ------------------------------------------------------------------ TMA bulk copies (1-D)
+// cp.async.bulk global -> shared with an mbarrier transaction count: one thread issues the
+// copies of a whole staging set, every thread waits on the barrier's phase.  Addresses and
+// sizes must be 16-byte multiples (the callers round ranges outwards; every global array has
+// >= 16 bytes of slack after its end, kkt_api.cu: vbytes / Carver).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+// generic-proxy accesses of shared memory before this point are ordered before later
+// async-proxy (TMA) writes to it (buffer reuse across tasks)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* a, double v) {
   // non-negative doubles order like their bit patterns; NaN maps above +inf
   unsigned long long b = isnan(v) ? 0x7ff8000000000000ULL : __double_as_longlong(v);
@@ -211,7 +242,7 @@ __device__ __forceinline__ int next_task(int* ctl, int* s_task) {
 //   ctl[8] = all tasks done.  The last worker to exit resets it for the next launch.
 #define KKT_CTL 16
 __device__ __forceinline__ void reset_ctl(int* ctl) {
-  ctl[0] = 0; ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[8] = 0;
+  ctl[0] = 0; ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[4] = 0; ctl[5] = 0; ctl[6] = 0; ctl[8] = 0;
   __threadfence();
 }
 __device__ __forceinline__ void persistent_exit(int* ctl) {

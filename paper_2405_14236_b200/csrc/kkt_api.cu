@@ -18,6 +18,8 @@
 #include "hsolve.cuh"
 #include "resid.cuh"
 #include "trsv.cuh"
+#include "sblock.cuh"
+#include "fblock.cuh"
 #include "tiles.cuh"
 #include "tsolve.cuh"
 #include "k3.cuh"
@@ -148,6 +150,17 @@ struct kkt_plan {
   size_t ts_cnt_bytes = 0;
   double ts_est_us = 0.0;
   long long* ts_trace = nullptr;
+  // subtree-block solves of the small supernodes (sblock.cuh); KKT_SBLOCK=0: per-node kernels
+  bool sblock = false;
+  SBPlan sbp{};
+  void* sb_mem = nullptr;
+  void* sb_mem2 = nullptr;
+  // subtree-block factorisation of the small supernodes (fblock.cuh); KKT_FBLOCK=0: per-node kernel
+  bool fblock = false;
+  FBPlan fbp{};
+  void* fb_mem = nullptr;
+  int fb_smem = 0, g_ffblk = 1;
+  int sb_smem = 0, g_fblk = 1, g_bblk = 1;
   bool fev_valid = false;
 };
 
@@ -160,7 +173,7 @@ struct Carver {
   template <class T>
   T* take(size_t count) {
     size_t o = off;
-    off = align_up(off + count * sizeof(T));
+    off = align_up(off + count * sizeof(T) + 16);  // >= 16 bytes of slack (TMA ranges round out)
     return dry ? nullptr : reinterpret_cast<T*>(base + o);
   }
 };
@@ -352,7 +365,7 @@ static void rebuild_J_csr(const Plan& P, std::vector<int>& Jrp, std::vector<int>
 }
 
 template <class T>
-static size_t vbytes(const std::vector<T>& v) { return align_up(v.size() * sizeof(T) + 1); }
+static size_t vbytes(const std::vector<T>& v) { return align_up(v.size() * sizeof(T) + 16); }  // TMA slack
 
 // Level schedule of the huge fronts for a cooperative grid of G CTAs (see HugeSched in
 // huge.cuh): one allocation holding the entries, their barrier counters, the level pointers and
@@ -433,7 +446,9 @@ static void release_device(kkt_plan* h) {
   if (h->pinned_flags) cudaFreeHost(h->pinned_flags);
   h->pinned_flags = nullptr;
   fr(h->trace_buf); fr(h->dbg_buf); fr(h->huge_mem); fr(h->hsolve_mem);
-  fr(h->tile_mem); fr(h->tile_pool); fr(h->tile_trace); fr(h->ts_mem); fr(h->ts_trace);
+  fr(h->tile_mem); fr(h->tile_pool); fr(h->tile_trace); fr(h->ts_mem); fr(h->ts_trace); fr(h->sb_mem); fr(h->sb_mem2); fr(h->fb_mem);
+  h->fblock = false;
+  h->sblock = false;
   if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
   h->solve_exec = nullptr;
   if (h->hy_exec) cudaGraphExecDestroy(h->hy_exec);
@@ -692,6 +707,118 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       CUDA_TRY(grid_of(linv_kernel, KKT_BNT, h->linv_smem, (long long)P.order_b.size() * P.batch, 1, &h->g_linv));
     }
   }
+  // subtree blocks of the small supernodes for the factorisation (fblock.cuh)
+  h->fblock = !P.order_s.empty() && getenv("KKT_FBLOCK") && atoi(getenv("KKT_FBLOCK")) > 0;  // opt-in (slower so far)
+  if (h->fblock) {
+    const int cap = getenv("KKT_FB_CAP") ? std::max(KKT_SCAP, atoi(getenv("KKT_FB_CAP"))) : 6144;
+    FBlockHost H;
+    build_fblocks(P, cap, H);
+    if (H.blk.empty()) {
+      h->fblock = false;
+    } else {
+      const size_t b1 = align_up(H.blk.size() * sizeof(FBlk) + 16), b2 = vbytes(H.meta), b3 = vbytes(H.up_init);
+      CUDA_TRY(cudaMalloc(&h->fb_mem, b1 + b2 + b3));
+      char* fb = (char*)h->fb_mem;
+      CUDA_TRY(cudaMemcpy(fb, H.blk.data(), H.blk.size() * sizeof(FBlk), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(fb + b1, H.meta.data(), H.meta.size() * sizeof(int), cudaMemcpyHostToDevice));
+      if (!H.up_init.empty())
+        CUDA_TRY(cudaMemcpy(fb + b1 + b2, H.up_init.data(), H.up_init.size() * sizeof(int), cudaMemcpyHostToDevice));
+      FBPlan& F = h->fbp;
+      F.blk = (const FBlk*)fb;
+      F.nblk = (int)H.blk.size();
+      F.meta = (const int*)(fb + b1);
+      F.up_init = (const int*)(fb + b1 + b2);
+      F.n_up_init = (int)H.up_init.size();
+      F.smem_doubles = std::max(H.max_smem, KKT_SCAP);
+      h->fb_smem = F.smem_doubles * 8;
+      CUDA_TRY(cudaFuncSetAttribute(factor_block_kernel<FB_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->fb_smem));
+      CUDA_TRY(grid_of(factor_block_kernel<FB_MINB>, FB_NT, h->fb_smem, (long long)(F.nblk + F.n_up_init) * P.batch, 1, &h->g_ffblk));
+    }
+  }
+  // subtree blocks of the small supernodes (sblock.cuh): the solves' small phase
+  h->sblock = !P.order_s.empty() && !(getenv("KKT_SBLOCK") && atoi(getenv("KKT_SBLOCK")) == 0);
+  if (h->sblock) {
+    const int cap = getenv("KKT_SB_CAP") ? std::max(1024, atoi(getenv("KKT_SB_CAP"))) : 6144;
+    SBlockHost H;
+    build_sblocks(P, cap, H);
+    if (H.blk.empty()) {
+      h->sblock = false;
+    } else {
+      const size_t b1 = align_up(H.blk.size() * sizeof(SBlk) + 16), b2 = vbytes(H.blk_of),
+                   b3 = vbytes(H.meta), b4 = vbytes(H.lrow);
+      CUDA_TRY(cudaMalloc(&h->sb_mem, b1 + b2 + b3 + b4));
+      char* sb = (char*)h->sb_mem;
+      CUDA_TRY(cudaMemcpy(sb, H.blk.data(), H.blk.size() * sizeof(SBlk), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sb + b1, H.blk_of.data(), H.blk_of.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sb + b1 + b2, H.meta.data(), H.meta.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sb + b1 + b2 + b3, H.lrow.data(), H.lrow.size() * sizeof(int), cudaMemcpyHostToDevice));
+      SBPlan& S = h->sbp;
+      S.blk = (const SBlk*)sb;
+      S.nblk = (int)H.blk.size();
+      S.blk_of = (const int*)(sb + b1);
+      S.meta = (const int*)(sb + b1 + b2);
+      S.lrow = (const int*)(sb + b1 + b2 + b3);
+      // whole-tree schedules for the solve-side plan view: supernodes in the tree kernels are
+      // every non-huge one, or all of them when the view solves the huge fronts as CTA nodes.
+      // Estimated task durations (us, measured on C4 traces): block 8, single small supernode
+      // 4 + 0.3 w, big supernode 6 + r w / 1200.
+      const bool vcta = h->huge_solve_cta;
+      const int ns = P.ns;
+      auto intree = [&](int s_) { return s_ >= 0 && (!P.sn[s_].huge || vcta); };
+      std::vector<double> dur(ns, 0.0), up(ns, 0.0), start(ns, 0.0);
+      for (int s_ = 0; s_ < ns; s_++) {
+        const SnInfo& I = P.sn[s_];
+        dur[s_] = I.big ? 6.0 + (double)I.r * I.w / 1200.0 : (H.blk_of[s_] >= 0 ? 8.0 : 4.0 + 0.3 * I.w);
+      }
+      for (int s_ = ns - 1; s_ >= 0; s_--) {  // parents first (postorder)
+        const int par = P.sn_parent[s_];
+        const bool pin = intree(par) && H.blk_of[s_] != -2;
+        up[s_] = dur[s_] + (pin ? up[par] : 0.0);              // forward: path to the top
+        start[s_] = pin ? start[par] + dur[par] : 0.0;        // backward: estimated start
+      }
+      std::vector<int> ford;
+      std::vector<double> fpri;
+      for (size_t q = 0; q < H.blk.size(); q++) { ford.push_back((int)q); fpri.push_back(up[H.blk[q].s_hi]); }
+      std::vector<int2> bord;
+      for (int s_ = 0; s_ < ns; s_++) {
+        if (!intree(s_) || H.blk_of[s_] == -2) continue;
+        if (P.sn[s_].big && P.sn_cp[s_ + 1] == P.sn_cp[s_]) { ford.push_back(-s_ - 1); fpri.push_back(up[s_]); }
+        const int par = P.sn_parent[s_];
+        bord.push_back(make_int2(s_, intree(par) ? par : -1));
+      }
+      std::vector<int> fidx(ford.size());
+      for (size_t q = 0; q < fidx.size(); q++) fidx[q] = (int)q;
+      std::stable_sort(fidx.begin(), fidx.end(), [&](int a_, int b_) { return fpri[a_] > fpri[b_]; });
+      std::vector<int> fsorted(ford.size());
+      for (size_t q = 0; q < fidx.size(); q++) fsorted[q] = ford[fidx[q]];
+      std::stable_sort(bord.begin(), bord.end(), [&](const int2& a_, const int2& b_) {
+        return start[a_.x] != start[b_.x] ? start[a_.x] < start[b_.x] : up[a_.x] > up[b_.x];
+      });
+      const size_t b5 = vbytes(fsorted), b6 = align_up(bord.size() * sizeof(int2) + 16);
+      CUDA_TRY(cudaMalloc(&h->sb_mem2, b5 + b6));
+      CUDA_TRY(cudaMemcpy(h->sb_mem2, fsorted.data(), fsorted.size() * sizeof(int), cudaMemcpyHostToDevice));
+      if (!bord.empty()) CUDA_TRY(cudaMemcpy((char*)h->sb_mem2 + b5, bord.data(), bord.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      S.fwd_order = (const int*)h->sb_mem2;
+      S.n_fwd = (int)fsorted.size();
+      S.bwd_order = (const int2*)((char*)h->sb_mem2 + b5);
+      S.n_bwd = (int)bord.size();
+      S.smem_doubles = std::max({H.max_smem, h->dp.max_rw_small + P.max_r_small + 2, P.max_front + 8 * 32 + 2});
+      h->sb_smem = S.smem_doubles * 8;
+      // every big supernode of the tree needs its L11^-1: the blocked substitution's registers
+      // would cost the small phase its occupancy, so such plans keep the per-node kernels
+      bool blk = !h->use_linv;
+      for (int s_ = 0; s_ < P.ns; s_++)
+        if (P.sn[s_].big && (!P.sn[s_].huge || vcta) && P.sn_Lip[s_] < 0) blk = true;
+      if (blk) h->sblock = false;
+      auto fk = tree_fwd_kernel<false>;
+      auto bk = tree_bwd_kernel<false>;
+      CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sb_smem));
+      CUDA_TRY(cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sb_smem));
+      CUDA_TRY(grid_of(fk, SB_NT, h->sb_smem, (long long)S.n_fwd * P.batch, 1, &h->g_fblk));
+      CUDA_TRY(grid_of(bk, SB_NT, h->sb_smem, (long long)S.n_bwd * P.batch, 1, &h->g_bblk));
+    }
+  }
+
   {
     const long long ubf = (long long)P.up_bf.size() * P.batch;
     CUDA_TRY(grid_of(factor_big_kernel<false>, KKT_BNT, h->fbig_smem, ubf, 1, &h->g_fbig));
@@ -891,7 +1018,12 @@ extern "C" kkt_status kkt_factor(kkt_handle h) {
   const bool ev = h->ls == h->stream;  // not while recording a graph
   if (ev) CUDA_TRY(cudaEventRecord(h->fev[0], h->ls));
   if (h->ldlt) CUDA_TRY(cudaMemsetAsync(h->inert, 0, 3 * sizeof(int) * P.batch, h->ls));
-  if (!P.order_s.empty()) {
+  if (!P.order_s.empty() && h->fblock) {
+    factor_block_kernel<FB_MINB><<<h->g_ffblk, FB_NT, h->fb_smem, h->ls>>>(
+        h->dp, h->fbp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0 * KKT_CTL, h->fail);
+    LAUNCH_CHECK();
+    h->launches++;
+  } else if (!P.order_s.empty()) {
     if (h->fsmall_occ == 3)
       factor_small_kernel<3><<<h->g_fsmall, KKT_WPB * 32, h->fsmall_smem, h->ls>>>(
         h->dp, h->Kv, h->Lx, h->Ub, h->Dv, h->facnt, h->ctl + 0 * KKT_CTL, h->fail);
@@ -955,12 +1087,59 @@ extern "C" kkt_status kkt_factor_phase_ms(kkt_handle h, double* ms) {
   return KKT_OK;
 }
 
+// forward + backward through the huge fronts (tile-task solve or the level kernel); nothing
+// when the solve-side plan view treats them as CTA supernodes
+static kkt_status launch_huge_solve(kkt_plan* h, const double* rhs, long long rs, double* xout,
+                                    long long xs, const int* done) {
+  const Plan& P = h->P;
+  const bool cta_huge = h->huge_solve_cta;
+  if (!P.order_h.empty() && !cta_huge && h->tsolve) {
+    CUDA_TRY(cudaMemsetAsync(h->tsp.cnt, 0, h->ts_cnt_bytes, h->ls));
+    DevPlan dp = h->dp;
+    TilePlan tp = h->tp;
+    TSolvePlan sp = h->tsp;
+    const double *dv = h->Dv, *rh = rhs;
+    double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
+    long long rs_ = rs, xs_ = xs;
+    const int* dn = done;
+    void* args[] = {&dp, &tp, &sp, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_solve_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
+                                         (size_t)TILE_SMEM_BYTES, h->ls));
+    h->launches++;
+  } else if (!P.order_h.empty() && !cta_huge) {
+    DevPlan dp = h->dp;
+    const double *lx = h->Lx, *dv = h->Dv, *rh = rhs;
+    double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
+    long long rs_ = rs, xs_ = xs;
+    const int* dn = done;
+    HugeSched hs = h->hsched_s;
+    void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)solve_huge_kernel, dim3(h->g_hsolve), dim3(256), args, 0,
+                                         h->ls));
+    h->launches++;
+  }
+  return KKT_OK;
+}
+
 // forward + backward solve of all batch instances: xout = K^-1 rhs
 static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, double* xout,
                                long long xs, const int* done) {
   const Plan& P = h->P;
   const DevPlan& dq = h->huge_solve_cta ? h->dps : h->dp;  // solve-side plan view
   const bool cta_huge = h->huge_solve_cta;
+  if (h->sblock) {  // whole-tree kernels around the huge fronts' tile solve
+    const double* li = h->use_linv ? h->Li : nullptr;
+    tree_fwd_kernel<false><<<h->g_fblk, SB_NT, h->sb_smem, h->ls>>>(
+        dq, h->sbp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done, li);
+    LAUNCH_CHECK();
+    h->launches++;
+    TRY(launch_huge_solve(h, rhs, rs, xout, xs, done));
+    tree_bwd_kernel<false><<<h->g_bblk, SB_NT, h->sb_smem, h->ls>>>(
+        dq, h->sbp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->bflag, h->ctl + 5 * KKT_CTL, done, li);
+    LAUNCH_CHECK();
+    h->launches++;
+    return KKT_OK;
+  }
   if (!P.order_s.empty()) {
     fwd_small_kernel<<<h->g_tsmall, KKT_WPB * 32, h->tsmall_smem, h->ls>>>(
         dq, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done);
@@ -974,31 +1153,7 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
                           h->ctl + 3 * KKT_CTL, done, h->pcap, (const double*)(h->use_linv ? h->Li : nullptr)));
       h->launches++;
     }
-    if (!P.order_h.empty() && !cta_huge && h->tsolve) {
-      CUDA_TRY(cudaMemsetAsync(h->tsp.cnt, 0, h->ts_cnt_bytes, h->ls));
-      DevPlan dp = h->dp;
-      TilePlan tp = h->tp;
-      TSolvePlan sp = h->tsp;
-      const double *dv = h->Dv, *rh = rhs;
-      double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
-      long long rs_ = rs, xs_ = xs;
-      const int* dn = done;
-      void* args[] = {&dp, &tp, &sp, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn};
-      CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_solve_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
-                                           (size_t)TILE_SMEM_BYTES, h->ls));
-      h->launches++;
-    } else if (!P.order_h.empty() && !cta_huge) {
-      DevPlan dp = h->dp;
-      const double *lx = h->Lx, *dv = h->Dv, *rh = rhs;
-      double *y = h->Y, *uv = h->uv, *xp = h->Xp, *xo = xout;
-      long long rs_ = rs, xs_ = xs;
-      const int* dn = done;
-      HugeSched hs = h->hsched_s;
-      void* args[] = {&dp, &lx, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn, &hs};
-      CUDA_TRY(cudaLaunchCooperativeKernel((const void*)solve_huge_kernel, dim3(h->g_hsolve), dim3(256), args, 0,
-                                           h->ls));
-      h->launches++;
-    }
+    TRY(launch_huge_solve(h, rhs, rs, xout, xs, done));
     if (h->ldlt) {  // K^-1 = L~^-T S L~^-1: y <- S y before the backward sweep
       ldlt_sign_kernel<<<grid_for((long long)P.batch * P.n, 256, h->sms), 256, 0, h->ls>>>((long long)P.batch * P.n, h->Y, h->Sg);
       LAUNCH_CHECK();
@@ -1016,8 +1171,8 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
     // overlapped with bwd_big only when bwd_big is the kernel right before it
     const bool after_big = (cta_huge ? !P.order_b.empty() : P.order_b.size() > P.order_h.size()) && (h->pdl_mask & 4);
     CUDA_TRY(launch_pdl(h->pdl && after_big, bwd_small_kernel, h->g_bsmall, KKT_WPB * 32, h->tsmall_smem, h->ls,
-                        dq, (const double*)h->Lx, (const double*)h->Dv, (const double*)h->Y, h->Xp, xout, xs,
-                        h->TQs, h->ctl + 5 * KKT_CTL, done, h->bflag, (int)(h->pdl && after_big)));
+                          dq, (const double*)h->Lx, (const double*)h->Dv, (const double*)h->Y, h->Xp, xout, xs,
+                          h->TQs, h->ctl + 5 * KKT_CTL, done, h->bflag, (int)(h->pdl && after_big)));
     h->launches++;
   }
   return KKT_OK;

@@ -49,7 +49,8 @@ class KKTAnalysisInfo(C.Structure):
 
 
 def so_path() -> str:
-    return _build.SO
+    # KKT_LIB: an alternative in-tree build of the same library (tuning experiments, tools/)
+    return os.environ.get("KKT_LIB", _build.SO)
 
 
 def lib(build_if_missing: bool = True):

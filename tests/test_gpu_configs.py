@@ -437,3 +437,40 @@ def test_warp_residual_variant(monkeypatch):
     x2, _, _ = run_lifted(inst, max_refine=10, solver=S)
     assert np.array_equal(x, x2)
     S.close()
+
+
+SBLOCK_CASES = [("C2", {}), ("C2", {"KKT_SB_CAP": "1024", "KKT_FB_CAP": "2048"}), ("C1", {}), ("C5b8", {}),
+                ("C5b8", {"KKT_SB_CAP": "1500", "KKT_FB_CAP": "3000"}), ("C2s", {"KKT_NO_PDL": "1"}),
+                ("C3L", {})]
+
+
+@pytest.mark.parametrize("switch", ["KKT_SBLOCK", "KKT_FBLOCK"])
+@pytest.mark.parametrize("case,env", SBLOCK_CASES)
+def test_subtree_block_kernels_bitwise(case, env, switch, monkeypatch):
+    """Small supernodes by subtree blocks -- the whole-tree solve kernels (sblock.cuh: TMA-staged
+    subtrees, big supernodes and single small ones continued in the same grid) and the block
+    factorisation (fblock.cuh) -- against the per-node kernels (switch = 0): same sums in the
+    same order -> bitwise the same x, and the oracle's solution.  A small budget (KKT_SB_CAP /
+    KKT_FB_CAP) leaves many supernodes outside the blocks (continuation chains, single-supernode
+    backward tasks, childless single leaves of the factorisation)."""
+    from kkt_gpu import run_lifted, relerr
+    if case == "C5b8":
+        inst = make_config("C5", batch=8)
+    elif case == "C3L":  # the C3 pattern as LiftedKKT: huge fronts solved by the tile path
+        inst = acopf(10000, 3000, name="acopf10000-lifted")
+    else:
+        inst = make_config(case)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv(switch, "0")
+    x0, info0, S0 = run_lifted(inst, max_refine=10)
+    S0.close()
+    monkeypatch.setenv(switch, "1")
+    x, info, S = run_lifted(inst, max_refine=10)
+    S.close()
+    assert info["status"] == 0, info
+    assert info["refine_iters"] == info0["refine_iters"]
+    assert np.array_equal(x, x0), float(np.abs(x - x0).max())
+    if case in ("C2", "C1"):
+        R = oracle.reference_solve(inst)
+        assert relerr(x, R["x"]) <= 1e-8
