@@ -417,7 +417,7 @@ def run_ours(args, rank, world):
         ach = B * work["factor_flops_large"] / (fl_ms[1] * 1e-3) / 1e12
         roofs["factor_large"] = {
             "bound": "tensor", "achieved": ach, "peak": fp64["dmma_tflops"], "unit": "TFLOP/s",
-            "traffic": None, "kernel": "factor_huge_kernel (large supernodes)",
+            "traffic": None, "kernel": "tile_factor_kernel (large supernodes: 64x64 tile DAG, DMMA)",
             "work": f"B x {work['factor_flops_large']:.4g} flops (sum over large supernodes of "
                     "sum_t (r - t)^2)",
             "threshold": "front > 25600 doubles (beyond one CTA's shared memory) and ancestors; "

@@ -160,7 +160,7 @@ struct kkt_plan {
   FBPlan fbp{};
   void* fb_mem = nullptr;
   int fb_smem = 0, g_ffblk = 1;
-  int sb_smem = 0, g_fblk = 1, g_bblk = 1;
+  int sb_smem = 0, g_fblk = 1, g_bblk = 1, sb_nt = 256;
   bool fev_valid = false;
 };
 
@@ -580,7 +580,10 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
     // C4/C6 831/1239 -> whole GPU).  KKT_HUGE_SOLVE=1 forces the whole-GPU kernel, =0 the CTA one.
     int maxr_h = 0;
     for (int s_ : P.order_h) maxr_h = std::max(maxr_h, P.sn_rp[s_ + 1] - P.sn_rp[s_]);
-    h->huge_solve_cta = maxr_h <= 512;
+    // with the per-node solve kernels (KKT_SBLOCK=0) huge fronts up to 512 rows solve faster as CTA
+    // supernodes; with the whole-tree kernels the tile solve wins everywhere (C3: 20.4 -> 15.2 ms)
+    const bool no_sblock = getenv("KKT_SBLOCK") && atoi(getenv("KKT_SBLOCK")) == 0;
+    h->huge_solve_cta = no_sblock && maxr_h <= 512;
     if (const char* e = getenv("KKT_HUGE_SOLVE")) h->huge_solve_cta = atoi(e) == 0;
     if (P.factor_kind == 1) h->huge_solve_cta = true;  // LDL^T: S applied between the CTA-path sweeps
   }
@@ -738,9 +741,13 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   // subtree blocks of the small supernodes (sblock.cuh): the solves' small phase
   h->sblock = !P.order_s.empty() && !(getenv("KKT_SBLOCK") && atoi(getenv("KKT_SBLOCK")) == 0);
   if (h->sblock) {
-    const int cap = getenv("KKT_SB_CAP") ? std::max(1024, atoi(getenv("KKT_SB_CAP"))) : 6144;
+    // CTA size: 256 threads for latency-bound trees, 128 (6 CTAs per SM, smaller blocks) when
+    // the small phase is throughput-bound (>= 50k small supernode tasks: C4, C5, C6; measured)
+    h->sb_nt = ((long long)P.order_s.size() * P.batch >= 50000) ? 128 : 256;
+    if (const char* e = getenv("KKT_SB_NT")) h->sb_nt = atoi(e) == 128 ? 128 : 256;
+    const int cap = getenv("KKT_SB_CAP") ? std::max(1024, atoi(getenv("KKT_SB_CAP"))) : (h->sb_nt == 128 ? 4096 : 6144);
     SBlockHost H;
-    build_sblocks(P, cap, H);
+    build_sblocks(P, cap, h->sb_nt / 32, H);
     if (H.blk.empty()) {
       h->sblock = false;
     } else {
@@ -810,12 +817,12 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       for (int s_ = 0; s_ < P.ns; s_++)
         if (P.sn[s_].big && (!P.sn[s_].huge || vcta) && P.sn_Lip[s_] < 0) blk = true;
       if (blk) h->sblock = false;
-      auto fk = tree_fwd_kernel<false>;
-      auto bk = tree_bwd_kernel<false>;
+      auto fk = h->sb_nt == 128 ? tree_fwd_kernel<false, 128> : tree_fwd_kernel<false, 256>;
+      auto bk = h->sb_nt == 128 ? tree_bwd_kernel<false, 128> : tree_bwd_kernel<false, 256>;
       CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sb_smem));
       CUDA_TRY(cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sb_smem));
-      CUDA_TRY(grid_of(fk, SB_NT, h->sb_smem, (long long)S.n_fwd * P.batch, 1, &h->g_fblk));
-      CUDA_TRY(grid_of(bk, SB_NT, h->sb_smem, (long long)S.n_bwd * P.batch, 1, &h->g_bblk));
+      CUDA_TRY(grid_of(fk, h->sb_nt, h->sb_smem, (long long)S.n_fwd * P.batch, 1, &h->g_fblk));
+      CUDA_TRY(grid_of(bk, h->sb_nt, h->sb_smem, (long long)S.n_bwd * P.batch, 1, &h->g_bblk));
     }
   }
 
@@ -1129,12 +1136,12 @@ static kkt_status launch_solve(kkt_plan* h, const double* rhs, long long rs, dou
   const bool cta_huge = h->huge_solve_cta;
   if (h->sblock) {  // whole-tree kernels around the huge fronts' tile solve
     const double* li = h->use_linv ? h->Li : nullptr;
-    tree_fwd_kernel<false><<<h->g_fblk, SB_NT, h->sb_smem, h->ls>>>(
+    (h->sb_nt == 128 ? tree_fwd_kernel<false, 128> : tree_fwd_kernel<false, 256>)<<<h->g_fblk, h->sb_nt, h->sb_smem, h->ls>>>(
         dq, h->sbp, h->Lx, h->Dv, rhs, rs, h->Y, h->uv, h->fcnt, h->ctl + 2 * KKT_CTL, done, li);
     LAUNCH_CHECK();
     h->launches++;
     TRY(launch_huge_solve(h, rhs, rs, xout, xs, done));
-    tree_bwd_kernel<false><<<h->g_bblk, SB_NT, h->sb_smem, h->ls>>>(
+    (h->sb_nt == 128 ? tree_bwd_kernel<false, 128> : tree_bwd_kernel<false, 256>)<<<h->g_bblk, h->sb_nt, h->sb_smem, h->ls>>>(
         dq, h->sbp, h->Lx, h->Dv, h->Y, h->Xp, xout, xs, h->bflag, h->ctl + 5 * KKT_CTL, done, li);
     LAUNCH_CHECK();
     h->launches++;

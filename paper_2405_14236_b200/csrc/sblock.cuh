@@ -32,9 +32,8 @@ __device__ __forceinline__ void bwd_sweep_sm(const double* Lp, int r, int w, con
   else bwd_sweep_warp<2>(Lp, r, w, dv, xa, lane);
 }
 
-#ifndef SB_MINB
-#define SB_MINB 3   // resident CTAs per SM the register allocation must allow (spill-free at 85 registers)
-#endif
+// resident CTAs per SM the register allocation must allow: 24 warps per SM at <= 85 registers
+template <int NT> constexpr int sb_minb() { return 768 / NT; }
 
 struct SBPlan {
   const SBlk* blk;
@@ -72,12 +71,13 @@ __device__ __forceinline__ SBRange sb_range(const T* src, long long n) {
 // ---------------------------------------------------------------- forward, one block
 // Stage the block's ranges (TMA), gather b, run the levels leaves first; on return the root's
 // v (= [y; u]) is in shared memory at the returned pointer.
+template <int NT>
 __device__ __forceinline__ const double* fwd_block(const DevPlan& P, const SBPlan& B, const SBlk& K, int b,
                                                    const double* Lb, const double* Dv, const double* bb,
                                                    double* Y, double* sm, uint64_t* bar, uint32_t& phase,
                                                    int* qc, int tid, int lane, int warp) {
   const int nn = K.s_hi - K.s_lo + 1;
-  const SBLayout O = sb_layout(nn, K.nlev, K.nL, K.ncol, K.nr, K.nch, K.Rroot);
+  const SBLayout O = sb_layout(nn, K.nlev, K.nL, K.ncol, K.nr, K.nch, K.Rroot, NT / 32);
   const SBRange rL = sb_range(Lb + K.L0, K.nL), rD = sb_range(Dv + K.F0, K.ncol),
                 rS = sb_range(P.sn + K.s_lo, nn), rR = sb_range(P.sn_rel + K.RP0, K.nr),
                 rC = sb_range(P.sn_ch + K.CP0, K.nch), rM = sb_range(B.meta + K.m0, K.nlev + 1 + nn);
@@ -93,7 +93,7 @@ __device__ __forceinline__ const double* fwd_block(const DevPlan& P, const SBPla
   }
   // right-hand side of the block's columns (generic loads, overlapping the bulk copies)
   double* bcol = sm + O.bcol;
-  for (int c = tid; c < K.ncol; c += SB_NT) bcol[c] = bb[__ldg(P.perm + K.F0 + c)];
+  for (int c = tid; c < K.ncol; c += NT) bcol[c] = bb[__ldg(P.perm + K.F0 + c)];
   mbar_wait(bar, phase);
   phase ^= 1;
   __syncthreads();
@@ -110,7 +110,7 @@ __device__ __forceinline__ const double* fwd_block(const DevPlan& P, const SBPla
   int* rq = reinterpret_cast<int*>(sm + O.q);
   int* pend = rq + nn;
   const int nleaf = lvl[1];
-  for (int t = tid; t < nn; t += SB_NT) {
+  for (int t = tid; t < nn; t += NT) {
     rq[t] = t < nleaf ? nodes[t] : -1;
     const SnInfo& It = Ss[K.s_lo + t];
     pend[t] = It.c1 - It.c0;
@@ -187,12 +187,12 @@ __device__ __forceinline__ void fwd_single_warp(const DevPlan& P, const SnInfo& 
 // Forward of one big supernode by the CTA (the per-node code of fwd_big_kernel): gather
 // v = [b(cols); 0] + children's u (fixed order), L11^-1 / blocked sweep, y -> Y, u -> uv.
 // v: [max_front] shared, tmp: [>= w] shared.
-template <bool BLK>
+template <bool BLK, int NT>
 __device__ __forceinline__ void fwd_big_cta(const DevPlan& P, const SnInfo& I, int s, int b, const double* Lb,
                                             const double* Dv, const double* bb, double* Y, double* uv,
                                             const double* Li_all, double* v, double* tmp, int* s_cR, int* s_cRel,
                                             int* s_cU, int tid) {
-  const int nt = SB_NT;
+  const int nt = NT;
   if (tid == 0) trace_stamp(P, 1, s, b, 0);
   const int r = I.r, w = I.w, R = r - w, nch = I.c1 - I.c0;
   const double* L = Lb + I.Lp;
@@ -265,8 +265,8 @@ __device__ __forceinline__ bool tree_arrive(int* cnt, int par, int nch) {
 // outside the blocks on warp 0, a big parent with the whole CTA.  No task ever waits.
 // BLK: some big supernode of the tree has no L11^-1 (the blocked substitution is compiled in;
 // it needs registers that cost occupancy, so the common case compiles without it)
-template <bool BLK>
-__global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_fwd_kernel(DevPlan P, SBPlan B, const double* __restrict__ Lx_all,
+template <bool BLK, int NT>
+__global__ void __launch_bounds__(NT, BLK ? 1 : sb_minb<NT>()) tree_fwd_kernel(DevPlan P, SBPlan B, const double* __restrict__ Lx_all,
                                                                  const double* __restrict__ Dv_all,
                                                                  const double* __restrict__ rhs, long long rs,
                                                                  double* Y_all, double* uv_all, int* cnt_all, int* ctl,
@@ -299,15 +299,15 @@ __global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_fwd_kernel(DevP
     const int code = __ldg(B.fwd_order + t / P.batch);
     if (code >= 0) {
       const SBlk K = B.blk[code];
-      const double* vr = fwd_block(P, B, K, b, Lb, Dv, bb, Y, sm, &bar, phase, s_qc, tid, lane, warp);
+      const double* vr = fwd_block<NT>(P, B, K, b, Lb, Dv, bb, Y, sm, &bar, phase, s_qc, tid, lane, warp);
       s = K.s_hi;
       I = P.sn[s];
       if (I.par >= 0)
-        for (int q = tid; q < I.r - I.w; q += SB_NT) uv[I.uvp + q] = vr[I.w + q];
+        for (int q = tid; q < I.r - I.w; q += NT) uv[I.uvp + q] = vr[I.w + q];
     } else {
       s = -code - 1;
       I = P.sn[s];
-      fwd_big_cta<BLK>(P, I, s, b, Lb, Dv, bb, Y, uv, Li_all, sm, sm + P.max_front, s_cR, s_cRel, s_cU, tid);
+      fwd_big_cta<BLK, NT>(P, I, s, b, Lb, Dv, bb, Y, uv, Li_all, sm, sm + P.max_front, s_cR, s_cRel, s_cU, tid);
     }
     // continuation up the tree
     for (;;) {
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_fwd_kernel(DevP
       s = nx;
       I = P.sn[s];
       if (I.big) {
-        fwd_big_cta<BLK>(P, I, s, b, Lb, Dv, bb, Y, uv, Li_all, sm, sm + P.max_front, s_cR, s_cRel, s_cU, tid);
+        fwd_big_cta<BLK, NT>(P, I, s, b, Lb, Dv, bb, Y, uv, Li_all, sm, sm + P.max_front, s_cR, s_cRel, s_cU, tid);
       } else if (warp == 0) {
         fwd_single_warp(P, I, s, b, Lb, Dv, bb, Y, uv, sm, sm + P.max_rw_small, lane);
       }
@@ -373,13 +373,13 @@ __device__ __forceinline__ void bwd_node_warp(const DevPlan& P, const SnInfo& I,
 }
 
 // Backward of one big supernode by the CTA (per-node code of bwd_big_kernel).
-template <bool BLK>
+template <bool BLK, int NT>
 __device__ __forceinline__ void bwd_big_cta(const DevPlan& P, const SnInfo& I, int s, int b,
                                             const double* __restrict__ Lx_all, const double* __restrict__ Dv_all,
                                             const double* __restrict__ Y_all, double* Xp_all, double* xout,
                                             long long xs, const double* __restrict__ Li_all, double* xa, double* part,
                                             int tid) {
-  const int nt = SB_NT;
+  const int nt = NT;
   if (tid == 0) trace_stamp(P, 2, s, b, 0);
   const int r = I.r, w = I.w;
   const double* L = Lx_all + (long long)b * P.nnzL_stored + I.Lp;
@@ -398,13 +398,14 @@ __device__ __forceinline__ void bwd_big_cta(const DevPlan& P, const SnInfo& I, i
   if (tid == 0) trace_stamp(P, 2, s, b, 1);
 }
 
-// Backward of one block: stage, y and the ancestors' x, levels root first.
+// Backward of one block: stage, y and the ancestors' x, then the block's ready queue.
+template <int NT>
 __device__ __forceinline__ void bwd_block(const DevPlan& P, const SBPlan& B, const SBlk& K, const SnInfo& I, int b,
                                           const double* Lb, const double* Dv, const double* Yb, double* Xp,
                                           double* xo, double* sm, uint64_t* bar, uint32_t& phase,
                                           int* qc, int tid, int lane, int warp) {
   const int nn = K.s_hi - K.s_lo + 1;
-  const SBLayout O = sb_layout(nn, K.nlev, K.nL, K.ncol, K.nr, K.nch, K.Rroot);
+  const SBLayout O = sb_layout(nn, K.nlev, K.nL, K.ncol, K.nr, K.nch, K.Rroot, NT / 32);
   const SBRange rL = sb_range(Lb + K.L0, K.nL), rD = sb_range(Dv + K.F0, K.ncol),
                 rS = sb_range(P.sn + K.s_lo, nn), rR = sb_range(B.lrow + K.RP0, K.nr),
                 rP = sb_range(P.perm + K.F0, K.ncol), rM = sb_range(B.meta + K.m0, K.nlev + 1 + nn),
@@ -422,8 +423,8 @@ __device__ __forceinline__ void bwd_block(const DevPlan& P, const SBPlan& B, con
   }
   // y of the block's columns and the ancestors' x of the root's update rows (generic loads)
   double* xl = sm + O.v;
-  for (int c = tid; c < K.ncol; c += SB_NT) xl[c] = ldcg(Yb + K.F0 + c);
-  for (int q = tid; q < K.Rroot; q += SB_NT) xl[K.ncol + q] = ldcg(Xp + __ldg(P.sn_rows + I.rp0 + I.w + q));
+  for (int c = tid; c < K.ncol; c += NT) xl[c] = ldcg(Yb + K.F0 + c);
+  for (int q = tid; q < K.Rroot; q += NT) xl[K.ncol + q] = ldcg(Xp + __ldg(P.sn_rows + I.rp0 + I.w + q));
   mbar_wait(bar, phase);
   phase ^= 1;
   __syncthreads();
@@ -438,7 +439,7 @@ __device__ __forceinline__ void bwd_block(const DevPlan& P, const SBPlan& B, con
   double* xa = sm + O.xa + warp * 64;
   // ready queue: the root, then every supernode pushes its children (tallest first)
   int* rq = reinterpret_cast<int*>(sm + O.q);
-  for (int t = tid; t < nn; t += SB_NT) rq[t] = t == 0 ? nn - 1 : -1;
+  for (int t = tid; t < nn; t += NT) rq[t] = t == 0 ? nn - 1 : -1;
   if (tid == 0) { qc[0] = 0; qc[1] = 1; }
   __syncthreads();
   volatile int* vrq = rq;
@@ -486,8 +487,8 @@ __device__ __forceinline__ void bwd_block(const DevPlan& P, const SBPlan& B, con
 // estimated start order (parents before children), taken by ticket; a task waits for its
 // parent's done flag (flag == this launch's epoch; no resets).  Every task waits only for a
 // task with a smaller ticket, held by a resident CTA: deadlock-free.
-template <bool BLK>
-__global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_bwd_kernel(DevPlan P, SBPlan B, const double* __restrict__ Lx_all,
+template <bool BLK, int NT>
+__global__ void __launch_bounds__(NT, BLK ? 1 : sb_minb<NT>()) tree_bwd_kernel(DevPlan P, SBPlan B, const double* __restrict__ Lx_all,
                                                                  const double* __restrict__ Dv_all,
                                                                  const double* __restrict__ Y_all, double* Xp_all,
                                                                  double* xout, long long xs, int* flags_all, int* ctl,
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_bwd_kernel(DevP
     const int bi = I.big ? -1 : __ldg(B.blk_of + s);
     __syncthreads();  // every thread reads the ancestors' x only after thread 0's acquire
     if (I.big) {
-      bwd_big_cta<BLK>(P, I, s, b, Lx_all, Dv_all, Y_all, Xp_all, xout, xs, Li_all, sm, sm + P.max_front, tid);
+      bwd_big_cta<BLK, NT>(P, I, s, b, Lx_all, Dv_all, Y_all, Xp_all, xout, xs, Li_all, sm, sm + P.max_front, tid);
       __threadfence();
       __syncthreads();
       if (tid == 0) st_release(flags + s, epoch);
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(SB_NT, BLK ? 1 : SB_MINB) tree_bwd_kernel(DevP
       }
     } else {
       const SBlk K = B.blk[bi];
-      bwd_block(P, B, K, I, b, Lx_all + (long long)b * P.nnzL_stored, Dv_all + (long long)b * P.n,
+      bwd_block<NT>(P, B, K, I, b, Lx_all + (long long)b * P.nnzL_stored, Dv_all + (long long)b * P.n,
                 Y_all + (long long)b * P.n, Xp_all + (long long)b * P.n, xout + (long long)b * xs, sm, &bar,
                 phase, s_qc, tid, lane, warp);
     }

@@ -35,11 +35,8 @@ struct SBLayout {
 #else
 #define SB_HD __host__ __device__ __forceinline__
 #endif
-#ifndef SB_NT_CFG
-#define SB_NT_CFG 256
-#endif
-constexpr int SB_NT = SB_NT_CFG;      // threads per CTA of the block kernels
-constexpr int SB_NW = SB_NT / 32;
+// CTA sizes of the tree kernels: 256 threads for latency-bound trees, 128 (more CTAs per SM,
+// smaller blocks) for throughput-bound ones; the layout's per-warp scratch depends on it
 SB_HD int sb_al(int d) { return (d + 1) & ~1; }            // doubles -> 16-byte multiple
 SB_HD int sb_ai(int i) { return ((i + 3) & ~3) / 2; }      // ints -> doubles, 16-byte multiple
 // fwd: L | v (sum r) | bcol (ncol) | D | sn | rel | ch | meta
@@ -47,12 +44,12 @@ SB_HD int sb_ai(int i) { return ((i + 3) & ~3) / 2; }      // ints -> doubles, 1
 // both: q = the block's ready queue and per-supernode pending-children counts (ints)
 // The TMA-filled sections (L, D, sn, rel, ch, perm, meta) hold the copied range rounded out to
 // 16 bytes; the generic-written ones (v / xl, bcol / xa) never share a 16-byte chunk with them.
-SB_HD SBLayout sb_layout(int nn, int nlev, long long nL, int ncol, int nr, int nch, int Rroot) {
+SB_HD SBLayout sb_layout(int nn, int nlev, long long nL, int ncol, int nr, int nch, int Rroot, int nw) {
   SBLayout o;
   int p = 0;
   o.L = p;    p += sb_al((int)nL + 2);
   o.v = p;    p += sb_al(nr > ncol + Rroot ? nr : ncol + Rroot);   // fwd v buffers / bwd xl (generic writes only)
-  o.bcol = p; p += sb_al(ncol > SB_NW * 64 ? ncol : SB_NW * 64);   // fwd bcol / bwd xa
+  o.bcol = p; p += sb_al(ncol > nw * 64 ? ncol : nw * 64);         // fwd bcol / bwd xa
   o.D = p;    p += sb_al(ncol + 2);
   o.sn = p;   p += nn * 8;
   o.rel = p;  p += sb_ai(nr + 4);
@@ -112,6 +109,6 @@ struct SBlockHost {
 };
 
 // Partition the small supernodes into maximal subtrees whose layout fits `cap` doubles.
-void build_sblocks(const Plan& P, int cap, SBlockHost& out);
+void build_sblocks(const Plan& P, int cap, int nw, SBlockHost& out);
 
 }  // namespace kkt

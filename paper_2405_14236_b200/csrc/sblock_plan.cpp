@@ -5,7 +5,7 @@
 
 namespace kkt {
 
-void build_sblocks(const Plan& P, int cap, SBlockHost& out) {
+void build_sblocks(const Plan& P, int cap, int nw, SBlockHost& out) {
   const int ns = P.ns;
   out = SBlockHost{};
   out.blk_of.assign(ns, -1);
@@ -32,7 +32,7 @@ void build_sblocks(const Plan& P, int cap, SBlockHost& out) {
     const int nch = P.sn_cp[s + 1] - P.sn_cp[a];
     const int R = (P.sn_rp[s + 1] - P.sn_rp[s]) - (P.sn_first[s + 1] - P.sn_first[s]);
     // the level count is the subtree height + 1 (levels by height within the subtree)
-    return sb_layout(nn, hgt[s] + 1, nL, ncol, nr, nch, R);
+    return sb_layout(nn, hgt[s] + 1, nL, ncol, nr, nch, R, nw);
   };
   std::vector<char> fits(ns, 0);
   for (int s = 0; s < ns; s++) {

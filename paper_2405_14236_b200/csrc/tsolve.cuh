@@ -288,24 +288,39 @@ __device__ void ts_fchain(const TSCtx& X, const TFront& F, int f, int k, double*
   tile_load_async(Xi, X.inv + X.T->ibase[f] + (long long)k * TBD);   // (L_kk^-1)^T
   if (k + 1 < F.nt) tile_load_async(Lo, ts_tile(X, F, k + 1, k));
   const int nk = tsize(F, k);
-  ts_wait(ts_gf(*X.S, X.cnt, F, f, k), 1);
-  ts_wait(ts_pc(*X.S, X.cnt, F, f, k), k);
+  if (threadIdx.x == 0) {  // the block's gather and its k partial products, one wait
+    const int* g = ts_gf(*X.S, X.cnt, F, f, k);
+    const int* pc = ts_pc(*X.S, X.cnt, F, f, k);
+    while (ld_volatile(g) < 1 || ld_volatile(pc) < k) { __nanosleep(32); }
+    fence_acq_rel();
+  }
+  __syncthreads();
   ts_ready(X);
   double* y = X.Y + I.f0 + k * TBS;
-  if (threadIdx.x < TBS) { w[threadIdx.x] = threadIdx.x < nk ? __ldcg(y + threadIdx.x) : 0.0; v[threadIdx.x] = 0.0; }
-  __syncthreads();
-  ts_sum_partials(X, F, f, k, k, w, r);
+  if (threadIdx.x < TBS) {  // r = v_k - sum_j P[k][j] (j ascending): all loads in one round trip
+    double a = threadIdx.x < nk ? __ldcg(y + threadIdx.x) : 0.0;
+    const double* p0 = ts_pslot(X, F, f, k, 0) + threadIdx.x;
+#pragma unroll 8
+    for (int j = 0; j < k; j++) a -= __ldcg(p0 + (long long)j * TBS);
+    r[threadIdx.x] = a;
+    v[threadIdx.x] = 0.0;
+    w[threadIdx.x] = 0.0;
+  }
   cp_async_wait_all();
   __syncthreads();
   ts_gemv_t(v, Xi, r);                              // v = -(L_kk^-1 r): y = -v
-  if (threadIdx.x < TBS) { v[threadIdx.x] = -v[threadIdx.x]; w[threadIdx.x] = 0.0; }
+  if (threadIdx.x < TBS) v[threadIdx.x] = -v[threadIdx.x];
   __syncthreads();
   if (threadIdx.x < nk) y[threadIdx.x] = v[threadIdx.x];
-  ts_publish(ts_yf(*X.S, X.cnt, F, f, k), 1);
-  if (k + 1 < F.nt) {
+  if (k + 1 < F.nt) {  // the next block's partial first: one fence publishes both (chain latency)
     ts_gemv_n(w, Lo, v);                            // w = -L_{k+1,k} y_k
     if (threadIdx.x < TBS) ts_pslot(X, F, f, k + 1, k)[threadIdx.x] = -w[threadIdx.x];
-    ts_publish_add(ts_pc(*X.S, X.cnt, F, f, k + 1));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(ts_yf(*X.S, X.cnt, F, f, k), 1);
+    if (k + 1 < F.nt) red_release_add(ts_pc(*X.S, X.cnt, F, f, k + 1), 1);
   }
 }
 
@@ -411,8 +426,12 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
     X.Xp[c] = v[threadIdx.x];
     X.xout[__ldg(P.perm + c)] = v[threadIdx.x];
   }
-  ts_publish(ts_xf(*X.S, X.cnt, F, f, k), 1);
-  ts_publish_add(ts_xdone(*X.S, X.cnt, F, f));
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one fence publishes x_k and the front's done count
+    __threadfence();
+    st_release(ts_xf(*X.S, X.cnt, F, f, k), 1);
+    red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+  }
 }
 
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, TilePlan T, TSolvePlan S,

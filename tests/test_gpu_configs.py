@@ -440,6 +440,7 @@ def test_warp_residual_variant(monkeypatch):
 
 
 SBLOCK_CASES = [("C2", {}), ("C2", {"KKT_SB_CAP": "1024", "KKT_FB_CAP": "2048"}), ("C1", {}), ("C5b8", {}),
+                ("C2", {"KKT_SB_NT": "128"}), ("C5b8", {"KKT_SB_NT": "128", "KKT_SB_CAP": "2048"}),
                 ("C5b8", {"KKT_SB_CAP": "1500", "KKT_FB_CAP": "3000"}), ("C2s", {"KKT_NO_PDL": "1"}),
                 ("C3L", {})]
 

@@ -36,6 +36,25 @@ __global__ void __launch_bounds__(256, 1) bench(int which, int reps, double* g, 
       __syncthreads();
     } else if (which == 6) {   // gemm into smem C
       tile_gemm_nt_smem(sm + 2 * TBD, sm, sm + TBD);
+    } else if (which == 7) {   // store a tile + panel copy + fence (publish cost)
+      tile_store(gt + 3 * TBD, sm);
+      TFront F{}; F.r = 700; F.w = 651; F.nbp = 11; F.nt = 11;
+      tile_to_panel(F, sm, g + (long long)gridDim.x * 4 * TBD + (long long)blockIdx.x * 64 * 700, 1, 0);
+      __syncthreads();
+      if (threadIdx.x == 0) __threadfence();
+      __syncthreads();
+    } else if (which == 8) {   // the whole CRIT body without waits
+      tile_load_async(sm, gt + TBD); tile_load_async(sm + TBD, gt + 2 * TBD); tile_load_async(sm + 2 * TBD, gt); cp_async_wait_all(); __syncthreads();
+      tile_trsm64(sm + TBD, sm, sm + 3 * TBD);
+      tile_store(gt + 3 * TBD, sm + TBD);
+      TFront F{}; F.r = 700; F.w = 651; F.nbp = 11; F.nt = 11;
+      tile_to_panel(F, sm + TBD, g + (long long)gridDim.x * 4 * TBD + (long long)blockIdx.x * 64 * 700, 1, 0);
+      __syncthreads(); if (threadIdx.x == 0) __threadfence(); __syncthreads();
+      tile_gemm_nt_smem(sm + 2 * TBD, sm + TBD, sm + TBD);
+      tile_potrf64(sm + 2 * TBD, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+      tile_store(gt + 3 * TBD, sm + 2 * TBD);
+      tile_to_panel(F, sm + 2 * TBD, g + (long long)gridDim.x * 4 * TBD + (long long)blockIdx.x * 64 * 700, 1, 1);
+      __syncthreads(); if (threadIdx.x == 0) __threadfence(); __syncthreads();
     }
   }
   long long t1 = clock64();
@@ -56,11 +75,12 @@ int main() {
     }
   }
   double *g, *dinv; long long* out;
-  cudaMalloc(&g, h.size() * 8); cudaMalloc(&dinv, nb * 64 * 8); cudaMalloc(&out, nb * 8);
+  cudaMalloc(&g, h.size() * 8 + (size_t)nb * 64 * 700 * 8 * 2); cudaMalloc(&dinv, nb * 64 * 8); cudaMalloc(&out, nb * 8);
   cudaMemcpy(g, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES);
-  const char* names[] = {"potrf64", "trsm64", "gemm_global", "load2tiles", "diag32", "rowsolve32x64", "gemm_smem"};
-  for (int w = 0; w < 7; w++) {
+  const char* names[] = {"potrf64", "trsm64", "gemm_global", "load2tiles", "diag32", "rowsolve32x64", "gemm_smem",
+                         "store+panel+fence", "crit_body"};
+  for (int w = 0; w < 9; w++) {
     for (int grid : {1, 148, 296}) {
       bench<<<grid, 256, TILE_SMEM_BYTES>>>(w, 20, g, dinv, out);
       cudaError_t e = cudaDeviceSynchronize();
