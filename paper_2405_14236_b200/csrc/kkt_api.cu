@@ -145,6 +145,7 @@ struct kkt_plan {
   long long* tile_trace = nullptr;  // KKT_TRACE: per-task stamps of the tile kernel
   // tile-task solves through the huge fronts (tsolve.cuh); KKT_TSOLVE=0: level kernel (hsolve.cuh)
   bool tsolve = false;
+  bool ts_chain = false;             // panel chains on one CTA (KKT_TS_CHAIN=1; default: per-step tasks)
   TSolvePlan tsp{};
   void* ts_mem = nullptr;
   size_t ts_cnt_bytes = 0;
@@ -890,6 +891,7 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       h->tile_cnt_bytes = align_up((B * (size_t)tph.ncnt + 1) * sizeof(int));
       CUDA_TRY(cudaMalloc(&h->tile_pool, poolb + invb + h->tile_cnt_bytes));
       TilePlan& T = h->tp;
+      T.panel = 1;
       T.fr = (const TFront*)base;
       T.tasks = (const int4*)(base + fb);
       T.hidx = (const int*)(base + fb + tkb);
@@ -908,9 +910,18 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       T.cnt = (int*)((char*)h->tile_pool + poolb + invb);
       T.trace = nullptr;
       h->tsolve = !h->huge_solve_cta && !(getenv("KKT_TSOLVE") && atoi(getenv("KKT_TSOLVE")) == 0);
+      // the tile solve reads L from the tile pool: the factorisation skips the panel copies
+      h->tp.panel = h->tsolve ? 0 : 1;
+      if (getenv("KKT_TILE_PANEL") && atoi(getenv("KKT_TILE_PANEL")) > 0) h->tp.panel = 1;
       if (h->tsolve) {
         TSolvePlanHost tsh;
-        build_tile_solve_plan(P, tph, h->g_tile, tsh);
+        // chain tasks (one CTA per front panel, tsolve.cuh FCH / BCH) unless a panel is too tall
+        int maxnbp = 0;
+        for (const auto& fr_ : tph.fr) maxnbp = std::max(maxnbp, fr_.nbp);
+        // opt-in (KKT_TS_CHAIN=1): measured slower on C4 (root panel 65 -> 126 us: the per-tile
+        // CTA barriers of the streamed GEMVs cost more than the per-step hand-offs they remove)
+        h->ts_chain = maxnbp <= TS_NBP_MAX && getenv("KKT_TS_CHAIN") && atoi(getenv("KKT_TS_CHAIN")) > 0;
+        build_tile_solve_plan(P, tph, h->g_tile, h->ts_chain, tsh);
         h->ts_est_us = tsh.est_us;
         std::vector<TTask> st;
         st.reserve(tsh.tasks.size() * B);
@@ -934,7 +945,7 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
         h->tsp.cbase2 = (const int*)(tb_ + sb);
         h->tsp.cnt = (int*)(tb_ + sb + cbb + pbb + partb);
         h->tsp.trace = nullptr;
-        CUDA_TRY(cudaFuncSetAttribute(tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES));
+        CUDA_TRY(cudaFuncSetAttribute(tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TS_SMEM_BYTES));
       }
       if (h->tsolve && getenv("KKT_TRACE") && atoi(getenv("KKT_TRACE")) > 0) {
         CUDA_TRY(cudaMalloc(&h->ts_trace, (size_t)h->tsp.ntask * 4 * sizeof(long long)));
@@ -1111,7 +1122,7 @@ static kkt_status launch_huge_solve(kkt_plan* h, const double* rhs, long long rs
     const int* dn = done;
     void* args[] = {&dp, &tp, &sp, &dv, &rh, &rs_, &y, &uv, &xp, &xo, &xs_, &dn};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)tile_solve_kernel, dim3(h->g_tile), dim3(TILE_THREADS), args,
-                                         (size_t)TILE_SMEM_BYTES, h->ls));
+                                         (size_t)TS_SMEM_BYTES, h->ls));
     h->launches++;
   } else if (!P.order_h.empty() && !cta_huge) {
     DevPlan dp = h->dp;

@@ -20,7 +20,7 @@ namespace kkt {
 
 namespace {
 constexpr int TB = 64;
-constexpr int TS_G = 0, TS_U = 1, TS_C = 2, TS_BU_ = 3, TS_BC_ = 4, TS_UF = 5;  // tsolve.cuh task types
+constexpr int TS_G = 0, TS_U = 1, TS_C = 2, TS_BU_ = 3, TS_BC_ = 4, TS_UF = 5, TS_FCH_ = 6, TS_BCH_ = 7;  // tsolve.cuh task types
 
 struct Task {
   int type, f, i, j, k;
@@ -259,7 +259,7 @@ void build_tile_plan(const Plan& P, int workers, TilePlanHost& out) {
 
 namespace kkt {
 
-void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, TSolvePlanHost& out) {
+void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, bool chains, TSolvePlanHost& out) {
   out = TSolvePlanHost();
   const int nf = (int)tp.fr.size();
   out.cbase2.resize(std::max(nf, 1));
@@ -305,13 +305,23 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
     }
     std::vector<std::vector<int>> prod(nt);     // producers of the partials P[t][.]
     fc[f].assign(nbp, -1);
-    for (int k = 0; k < nbp; k++) {
-      std::vector<int> p = {g[k]};
-      p.insert(p.end(), prod[k].begin(), prod[k].end());
-      const int c = add(TS_C, f, k + 1, k, d_c, p);
-      fc[f][k] = c;
-      if (k + 1 < nt) prod[k + 1].push_back(c);
-      for (int i = k + 2; i < nt; i++) prod[i].push_back(add(TS_U, f, i, k, d_u, {c}));
+    if (chains) {
+      // the panel on one CTA (tsolve.cuh FCH), then the update rows' products per (t, k)
+      std::vector<int> p(g.begin(), g.begin() + nbp);
+      const double dch = 1.0 + 1.2 * nbp + 0.4 * nbp * (nbp - 1) / 2;
+      const int c = add(TS_FCH_, f, 0, 0, dch, p);
+      for (int k = 0; k < nbp; k++) fc[f][k] = c;
+      for (int k = 0; k < nbp; k++)
+        for (int i = nbp; i < nt; i++) prod[i].push_back(add(TS_U, f, i, k, d_u, {c}));
+    } else {
+      for (int k = 0; k < nbp; k++) {
+        std::vector<int> p = {g[k]};
+        p.insert(p.end(), prod[k].begin(), prod[k].end());
+        const int c = add(TS_C, f, k + 1, k, d_c, p);
+        fc[f][k] = c;
+        if (k + 1 < nt) prod[k + 1].push_back(c);
+        for (int i = k + 2; i < nt; i++) prod[i].push_back(add(TS_U, f, i, k, d_u, {c}));
+      }
     }
     for (int t = nbp; t < nt; t++) {
       std::vector<int> p = {g[t]};
@@ -334,6 +344,13 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, T
         if (hp >= 0) p.push_back(xlast[hp]);
         q[k].push_back(add(TS_BU_, f, c0, k, d_u * std::min(UCH, nt - c0), p));
       }
+    if (chains) {
+      std::vector<int> p = {fc[f][0]};
+      for (int k = 0; k < nbp; k++) p.insert(p.end(), q[k].begin(), q[k].end());
+      const double dch = 1.0 + 1.2 * nbp + 0.4 * nbp * (nbp - 1) / 2;
+      xlast[f] = add(TS_BCH_, f, 0, 0, dch, p);
+      continue;
+    }
     int xprev = -1;
     for (int k = nbp - 1; k >= 0; k--) {
       std::vector<int> p = {fc[f][k]};

@@ -48,6 +48,7 @@ struct TSolvePlanHost {
   int ncnt = 1;
   double est_us = 0.0;
 };
-void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, TSolvePlanHost& out);
+// chains: the panel of every front as one forward and one backward task (tsolve.cuh FCH / BCH)
+void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, bool chains, TSolvePlanHost& out);
 
 }  // namespace kkt

@@ -64,6 +64,8 @@ struct TilePlan {
   double* inv;         // [batch][inv_doubles]: (L_kk^-1)^T of every diagonal panel tile (solves)
   long long inv_doubles;
   const long long* ibase;  // [nf] offset of a front's nbp inverse tiles
+  int panel;           // 1: also write final L tiles to the supernodal panel layout (read by the CTA-view
+                       // and level solves); 0 when the tile solve reads the pool (no copy on the chain)
 };
 
 __device__ __forceinline__ int tlin(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
@@ -611,7 +613,7 @@ __device__ void task_potrf0(const TileCtx& X, const TFront& F, double* sm) {
   if (SG) tile_potrf64_signed(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail, ssg, X.Sg + I.f0, s_kjj, X.cnt3);
   else tile_potrf64(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail);
   tile_store(tile_ptr(X, F, 0, 0), T0);
-  tile_to_panel(F, T0, X.Lx + I.Lp, 0, 0);
+  if (X.T->panel) tile_to_panel(F, T0, X.Lx + I.Lp, 0, 0);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + s_fail);
   publish_cnt(tile_cnt(X, F, 0, 0), 2);
 }
@@ -630,7 +632,7 @@ __device__ void task_trsm(const TileCtx& X, const TFront& F, int i, int k, doubl
   tile_trsm64<SG>(A, Lk, sinv, ssg);
   tile_store(tile_ptr(X, F, i, k), A);
   const SnInfo I = X.P->sn[F.s];
-  tile_to_panel(F, A, X.Lx + I.Lp, i, k);
+  if (X.T->panel) tile_to_panel(F, A, X.Lx + I.Lp, i, k);
   publish_cnt(tile_cnt(X, F, i, k), k + 2);
 }
 
@@ -642,12 +644,13 @@ __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) 
   if (SG) load_kjj(X, F, k + 1, s_kjj);
   const SnInfo I = X.P->sn[F.s];
   if (threadIdx.x == 0) s_fail = -1;
-  wait_cnt(tile_cnt(X, F, k, k), k + 2);
-  tile_load_async(Lk, tile_ptr(X, F, k, k));
+  // the updated tiles are ready before the previous step's diagonal tile: stage them first
   wait_cnt(tile_cnt(X, F, k + 1, k), k + 1);
   tile_load_async(A1, tile_ptr(X, F, k + 1, k));
   wait_cnt(tile_cnt(X, F, k + 1, k + 1), k + 1);
   tile_load_async(A2, tile_ptr(X, F, k + 1, k + 1));
+  wait_cnt(tile_cnt(X, F, k, k), k + 2);
+  tile_load_async(Lk, tile_ptr(X, F, k, k));
   load_sinv<SG>(X, F, k, sinv, ssg);
   stamp_ready(X);
   cp_async_wait_all();
@@ -655,7 +658,7 @@ __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) 
   // TRSM(k+1, k), published at once (the other updates of step k may start)
   tile_trsm64<SG>(A1, Lk, sinv, ssg);
   tile_store(tile_ptr(X, F, k + 1, k), A1);
-  tile_to_panel(F, A1, X.Lx + I.Lp, k + 1, k);
+  if (X.T->panel) tile_to_panel(F, A1, X.Lx + I.Lp, k + 1, k);
   publish_cnt(tile_cnt(X, F, k + 1, k), k + 2);
   // A2 -= L1 L1^T, Cholesky of A2
   tile_gemm_nt_smem<SG>(A2, A1, A1, ssg);
@@ -663,7 +666,7 @@ __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) 
                               X.Sg + I.f0 + (k + 1) * TBS, s_kjj, X.cnt3);
   else tile_potrf64(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail);
   tile_store(tile_ptr(X, F, k + 1, k + 1), A2);
-  tile_to_panel(F, A2, X.Lx + I.Lp, k + 1, k + 1);
+  if (X.T->panel) tile_to_panel(F, A2, X.Lx + I.Lp, k + 1, k + 1);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + (k + 1) * TBS + s_fail);
   publish_cnt(tile_cnt(X, F, k + 1, k + 1), k + 3);
 }

@@ -28,7 +28,12 @@
 
 namespace kkt {
 
-constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF = 5;
+constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF = 5, TS_FCH = 6, TS_BCH = 7;
+// chain tasks (FCH / BCH): the whole panel of one front on one CTA, tiles streamed through a
+// ring of TS_RING shared-memory slots (cp.async groups), working vectors in shared memory
+constexpr int TS_RING = 4;
+constexpr int TS_NBP_MAX = 40;   // panel row blocks per front the chain tasks support
+constexpr int TS_SMEM_BYTES = (TS_RING * TBD + 2 * TS_NBP_MAX * 64 + 2 * 64) * 8;
 constexpr int TS_UCHUNK = 2;   // update-row tiles per backward task (parallel chunks, one slot each)
 
 struct TSolvePlan {
@@ -434,6 +439,153 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
   }
 }
 
+// cp.async groups: at most N outstanding
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+// FCH(f): forward through the front's panel on one CTA, right-looking over the panel's column
+// blocks -- y_j = L_jj^-1 a_j (inverse tile), then a_k -= L_kj y_j for every panel row block
+// k > j -- with the tiles (Xi_j, L_{j+1,j}, ..., L_{nbp-1,j}, Xi_{j+1}, ...) streamed through the
+// ring.  a_k receives its products in j-ascending order and every product is the 4-thread
+// GEMV of ts_gemv_n, so the sums are those of the per-step tasks (FC / panel FU).  y_j is
+// published per block (the update-row FU tasks consume it); no waits inside the chain.
+__device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* sm) {
+  const SnInfo I = X.P->sn[F.s];
+  const int nbp = F.nbp;
+  double* av = sm + TS_RING * TBD;     // [nbp][64]
+  double* yv = av + TS_NBP_MAX * 64;   // [nbp][64], zero-padded
+  double* tmp = yv + TS_NBP_MAX * 64;  // [64]
+  const int ntile = nbp + nbp * (nbp - 1) / 2;
+  int ij = 0, ik = 0;                  // issue cursor: column j, position k (k == j: Xi_j)
+  auto issue = [&](int q) {
+    if (q < ntile) {
+      const double* g = (ik == ij) ? X.inv + X.T->ibase[f] + (long long)ij * TBD : ts_tile(X, F, ik, ij);
+      tile_load_async(sm + (q % TS_RING) * TBD, g);
+      if (++ik == nbp) { ij++; ik = ij; }
+    }
+    cp_async_commit();
+  };
+  for (int q = 0; q < TS_RING - 1; q++) issue(q);
+  if (threadIdx.x == 0) {  // every panel block gathered
+    for (int t = 0; t < nbp; t++)
+      while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
+    fence_acq_rel();
+  }
+  __syncthreads();
+  ts_ready(X);
+  for (int q = threadIdx.x; q < nbp * 64; q += TILE_THREADS) {
+    const int t = q >> 6, e = q & 63;
+    av[q] = e < tsize(F, t) ? __ldcg(X.Y + I.f0 + t * TBS + e) : 0.0;
+  }
+  int j = 0, k = 0;                    // consume cursor
+  for (int q = 0; q < ntile; q++) {
+    issue(q + TS_RING - 1);
+    cp_async_wait_n<TS_RING - 1>();
+    __syncthreads();
+    const double* T = sm + (q % TS_RING) * TBD;
+    if (k == j) {                      // y_j = -(gemv_t(0, Xi_j, a_j))
+      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
+      __syncthreads();
+      ts_gemv_t(tmp, T, av + j * 64);
+      const int nk = tsize(F, j);
+      if (threadIdx.x < TBS) {
+        const double y = -tmp[threadIdx.x];
+        yv[j * 64 + threadIdx.x] = threadIdx.x < nk ? y : 0.0;
+        if (threadIdx.x < nk) X.Y[I.f0 + j * TBS + threadIdx.x] = y;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) { __threadfence(); st_release(ts_yf(*X.S, X.cnt, F, f, j), 1); }
+    } else {                           // a_k -= L_kj y_j
+      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
+      __syncthreads();
+      ts_gemv_n(tmp, T, yv + j * 64);
+      if (threadIdx.x < TBS) av[k * 64 + threadIdx.x] -= -tmp[threadIdx.x];
+    }
+    if (++k == nbp) { j++; k = j; }
+    __syncthreads();                   // slot q is reused by the next issue
+  }
+  cp_async_wait_n<0>();
+}
+
+// BCH(f): backward through the panel on one CTA: a_k = y_k - (update-row chunks, last first),
+// then for i = nbp-1 .. 0: x_i = L_ii^-T a_i (inverse tile), a_k -= L_ik^T x_i for k < i
+// (tiles Xi_i, L_{i,i-1}, ..., L_{i,0} streamed).  a_k gets the panel products in i-descending
+// order, the one of k+1 last, as in the per-step tasks (BC / panel BU).
+__device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* sm) {
+  const DevPlan& P = *X.P;
+  const SnInfo I = P.sn[F.s];
+  const int nbp = F.nbp;
+  double* av = sm + TS_RING * TBD;
+  double* xs = av + TS_NBP_MAX * 64;
+  double* tmp = xs + TS_NBP_MAX * 64;
+  const int nchunk = (F.nt - F.nbp + TS_UCHUNK - 1) / TS_UCHUNK;
+  const int ntile = nbp + nbp * (nbp - 1) / 2;
+  int ii = nbp - 1, ik = nbp - 1;      // issue cursor: row block i, column k (k == i: Xi_i)
+  auto issue = [&](int q) {
+    if (q < ntile) {
+      const double* g = (ik == ii) ? X.inv + X.T->ibase[f] + (long long)ii * TBD : ts_tile(X, F, ii, ik);
+      tile_load_async(sm + (q % TS_RING) * TBD, g);
+      if (--ik < 0) { ii--; ik = ii; }
+    }
+    cp_async_commit();
+  };
+  for (int q = 0; q < TS_RING - 1; q++) issue(q);
+  if (threadIdx.x == 0) {  // the forward chain done, every update-row chunk product present
+    for (int t = 0; t < nbp; t++) {
+      while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
+      while (ld_volatile(ts_qc(*X.S, X.cnt, F, f, t)) < nchunk) { __nanosleep(32); }
+    }
+    fence_acq_rel();
+  }
+  __syncthreads();
+  ts_ready(X);
+  for (int q = threadIdx.x; q < nbp * 64; q += TILE_THREADS) {
+    const int t = q >> 6, e = q & 63;
+    double a = e < tsize(F, t) ? __ldcg(X.Y + I.f0 + t * TBS + e) : 0.0;
+    const double* q0 = ts_qslot(X, F, f, t, 0) + e;
+#pragma unroll 4
+    for (int c = nchunk - 1; c >= 0; c--) a -= __ldcg(q0 + (long long)(F.nbp + c) * TBS);
+    av[q] = a;
+  }
+  int i = nbp - 1, k = nbp - 1;        // consume cursor
+  for (int q = 0; q < ntile; q++) {
+    issue(q + TS_RING - 1);
+    cp_async_wait_n<TS_RING - 1>();
+    __syncthreads();
+    const double* T = sm + (q % TS_RING) * TBD;
+    if (k == i) {                      // x_i = -(gemv_n(0, Xi_i, a_i))
+      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
+      __syncthreads();
+      ts_gemv_n(tmp, T, av + i * 64);
+      const int nk = tsize(F, i);
+      if (threadIdx.x < TBS) {
+        const double x = -tmp[threadIdx.x];
+        xs[i * 64 + threadIdx.x] = threadIdx.x < nk ? x : 0.0;
+        if (threadIdx.x < nk) {
+          const int c = I.f0 + i * TBS + threadIdx.x;
+          X.Xp[c] = x;
+          X.xout[__ldg(P.perm + c)] = x;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(ts_xf(*X.S, X.cnt, F, f, i), 1);
+        red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+      }
+    } else {                           // a_k -= L_ik^T x_i
+      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
+      __syncthreads();
+      ts_gemv_t(tmp, T, xs + i * 64);
+      if (threadIdx.x < TBS) av[k * 64 + threadIdx.x] -= -tmp[threadIdx.x];
+    }
+    if (--k < 0) { i--; k = i; }
+    __syncthreads();
+  }
+  cp_async_wait_n<0>();
+}
+
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, TilePlan T, TSolvePlan S,
                                                                    const double* __restrict__ Dv_all,
                                                                    const double* __restrict__ rhs, long long rs,
@@ -474,6 +626,8 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, 
       case TS_FC: ts_fchain(X, F, tk.y, tk.w, tsm); break;
       case TS_BU: ts_bupdate(X, F, tk.y, tk.w, tk.z, tsm); break;
       case TS_UF: ts_ufinal(X, F, tk.y, tk.z, tsm); break;
+      case TS_FCH: ts_fchain_front(X, F, tk.y, tsm); break;
+      case TS_BCH: ts_bchain_front(X, F, tk.y, tsm); break;
       default: ts_bchain(X, F, tk.y, tk.w, tsm); break;
     }
     if (S.trace) {

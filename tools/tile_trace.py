@@ -33,14 +33,14 @@ t0 = tr[:, 0].min()
 st, rd, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
 rd = np.where(tr[:, 1] > 0, rd, st)      # no wait recorded -> ready at start
 typ = tasks[:, 0] & 15
-names = ["FG", "FU", "FC", "BU", "BC"] if SOLVE else ["ASM", "POTRF0", "TRSM", "CRIT", "UPD"]
+names = ["FG", "FU", "FC", "BU", "BC", "UF", "FCH", "BCH"] if SOLVE else ["ASM", "POTRF0", "TRSM", "CRIT", "UPD", "INV"]
 span = en.max()
 print(f"tasks {len(tasks)}  span {span:.1f} us  (list-schedule estimate {est:.1f} us)")
 busy = (en - st).sum()
 work = (en - rd).sum()
 nw = len(np.unique(tr[:, 3]))
 print(f"SMs used {nw}; sum(task time) {busy:.0f} us, sum(work after deps) {work:.0f} us, workers*span {nw*2*span:.0f} us")
-for t in range(5):
+for t in range(len(names)):
     m = typ == t
     if m.any():
         print(f"  {names[t]:6s} n={m.sum():6d}  work mean {np.mean(en[m]-rd[m]):7.2f} us  p90 {np.percentile(en[m]-rd[m],90):7.2f}"
