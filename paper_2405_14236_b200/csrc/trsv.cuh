@@ -375,60 +375,124 @@ __global__ void __launch_bounds__(KKT_BNT) linv_kernel(DevPlan P, const double* 
   }
 }
 
+// Row dot products of the big-supernode sweeps: acc = sum_k A[k * lda + i] x[k] for k < kend,
+// four accumulators (a_j takes k = j mod 4 while a full group of four fits, the tail goes to
+// a0), combined as (a0 + a1) + (a2 + a3).  The loads of 16 consecutive k are issued before
+// their FMAs (16 in flight per thread: the products are latency-bound, one row per thread).
+__device__ __forceinline__ double row_dot4(const double* __restrict__ A, long long lda, int i, const double* x,
+                                           int kend) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int k4 = kend & ~3;  // groups of four: k + 3 < kend
+  int k = 0;
+  for (; k + 16 <= k4; k += 16) {
+    double l[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) l[u] = __ldg(A + (long long)(k + u) * lda + i);
+#pragma unroll
+    for (int u = 0; u < 16; u += 4) {
+      a0 = fma(l[u], x[k + u], a0);
+      a1 = fma(l[u + 1], x[k + u + 1], a1);
+      a2 = fma(l[u + 2], x[k + u + 2], a2);
+      a3 = fma(l[u + 3], x[k + u + 3], a3);
+    }
+  }
+  {  // remaining groups of four (< 16 values), loads first
+    double l[12];
+    const int ng = (k4 - k) >> 2;
+#pragma unroll
+    for (int u = 0; u < 12; u++) l[u] = (u < 4 * ng) ? __ldg(A + (long long)(k + u) * lda + i) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 12; u += 4) {
+      if (u < 4 * ng) {
+        a0 = fma(l[u], x[k + u], a0);
+        a1 = fma(l[u + 1], x[k + u + 1], a1);
+        a2 = fma(l[u + 2], x[k + u + 2], a2);
+        a3 = fma(l[u + 3], x[k + u + 3], a3);
+      }
+    }
+    k += 4 * ng;
+  }
+  for (; k < kend; k++) a0 = fma(__ldg(A + (long long)k * lda + i), x[k], a0);
+  return (a0 + a1) + (a2 + a3);
+}
+
 // forward sweep of a big supernode with Li: v[0:r) in shared memory; tmp: >= w doubles
 __device__ __forceinline__ void cta_fwd_inv(const double* __restrict__ L, const double* __restrict__ Li, int r,
                                             int w, double* v, double* tmp, int tid, int nt) {
-  for (int i = tid; i < w; i += nt) {  // y1 = Li v[0:w) (lower triangular)
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int k = 0;
-    for (; k + 3 <= i; k += 4) {
-      a0 = fma(__ldg(Li + (long long)k * w + i), v[k], a0);
-      a1 = fma(__ldg(Li + (long long)(k + 1) * w + i), v[k + 1], a1);
-      a2 = fma(__ldg(Li + (long long)(k + 2) * w + i), v[k + 2], a2);
-      a3 = fma(__ldg(Li + (long long)(k + 3) * w + i), v[k + 3], a3);
-    }
-    for (; k <= i; k++) a0 = fma(__ldg(Li + (long long)k * w + i), v[k], a0);
-    tmp[i] = (a0 + a1) + (a2 + a3);
-  }
+  for (int i = tid; i < w; i += nt) tmp[i] = row_dot4(Li, w, i, v, i + 1);  // y1 = Li v[0:w) (lower)
   __syncthreads();
   for (int i = tid; i < w; i += nt) v[i] = tmp[i];
-  for (int i = w + tid; i < r; i += nt) {  // u = v[w:r) - L21 y1
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int k = 0;
-    for (; k + 3 < w; k += 4) {
-      a0 = fma(__ldg(L + (long long)k * r + i), tmp[k], a0);
-      a1 = fma(__ldg(L + (long long)(k + 1) * r + i), tmp[k + 1], a1);
-      a2 = fma(__ldg(L + (long long)(k + 2) * r + i), tmp[k + 2], a2);
-      a3 = fma(__ldg(L + (long long)(k + 3) * r + i), tmp[k + 3], a3);
-    }
-    for (; k < w; k++) a0 = fma(__ldg(L + (long long)k * r + i), tmp[k], a0);
-    v[i] -= (a0 + a1) + (a2 + a3);
-  }
+  for (int i = w + tid; i < r; i += nt) v[i] -= row_dot4(L, r, i, tmp, w);  // u = v[w:r) - L21 y1
   __syncthreads();
 }
 
 // backward sweep of a big supernode with Li: xa[0:w) = y1 on entry, xa[w:r) = ancestors' x;
 // on return xa[0:w) = x1.  Warp per column (lanes along the contiguous column), fixed-order
-// shuffle reductions.  tmp: >= w doubles.
+// shuffle reductions; a warp takes four columns at a time so that their loads are in flight
+// together (each column's sum keeps its own order).  tmp: >= w doubles.
 __device__ __forceinline__ void cta_bwd_inv(const double* __restrict__ L, const double* __restrict__ Li, int r,
                                             int w, double* xa, double* tmp, int tid, int nt) {
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int k = warp; k < w; k += nw) {  // z_k = y_k - L21(:,k)^T x(anc)
-    const double* Lk = L + (long long)k * r;
-    double a = 0.0;
-    for (int i = w + lane; i < r; i += 32) a = fma(__ldg(Lk + i), xa[i], a);
+  constexpr int CB = 4, RB = 4;  // columns per warp at once, row chunks of 32 with loads in flight
+  for (int k0 = warp; k0 < w; k0 += nw * CB) {  // z_k = y_k - L21(:,k)^T x(anc)
+    double a[CB];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) tmp[k] = xa[k] - a;
+    for (int c = 0; c < CB; c++) a[c] = 0.0;
+    for (int i0 = w + lane; i0 < r; i0 += 32 * RB) {
+      double l[CB][RB], xv[RB];
+#pragma unroll
+      for (int q = 0; q < RB; q++) xv[q] = (i0 + 32 * q < r) ? xa[i0 + 32 * q] : 0.0;
+#pragma unroll
+      for (int c = 0; c < CB; c++)
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+          const int k = k0 + c * nw, i = i0 + 32 * q;
+          l[c][q] = (k < w && i < r) ? __ldg(L + (long long)k * r + i) : 0.0;
+        }
+#pragma unroll
+      for (int c = 0; c < CB; c++)
+#pragma unroll
+        for (int q = 0; q < RB; q++)
+          if (i0 + 32 * q < r) a[c] = fma(l[c][q], xv[q], a[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CB; c++) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) a[c] += __shfl_xor_sync(0xffffffffu, a[c], o);
+      const int k = k0 + c * nw;
+      if (lane == 0 && k < w) tmp[k] = xa[k] - a[c];
+    }
   }
   __syncthreads();
-  for (int k = warp; k < w; k += nw) {  // x_k = sum_{i>=k} Li(i,k) z_i
-    const double* Lik = Li + (long long)k * w;
-    double a = 0.0;
-    for (int i = k + lane; i < w; i += 32) a = fma(__ldg(Lik + i), tmp[i], a);
+  for (int k0 = warp; k0 < w; k0 += nw * CB) {  // x_k = sum_{i>=k} Li(i,k) z_i
+    double a[CB];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) xa[k] = a;
+    for (int c = 0; c < CB; c++) a[c] = 0.0;
+    // column k's lane covers rows k + lane + 32 j (the per-column order of the sequential form)
+    for (int j0 = 0; k0 + j0 < w; j0 += 32 * RB) {
+      double l[CB][RB];
+#pragma unroll
+      for (int c = 0; c < CB; c++)
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+          const int k = k0 + c * nw, i = k + lane + j0 + 32 * q;
+          l[c][q] = (k < w && i < w) ? __ldg(Li + (long long)k * w + i) : 0.0;
+        }
+#pragma unroll
+      for (int c = 0; c < CB; c++)
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+          const int k = k0 + c * nw, i = k + lane + j0 + 32 * q;
+          if (k < w && i < w) a[c] = fma(l[c][q], tmp[i], a[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CB; c++) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) a[c] += __shfl_xor_sync(0xffffffffu, a[c], o);
+      const int k = k0 + c * nw;
+      if (lane == 0 && k < w) xa[k] = a[c];
+    }
   }
   __syncthreads();
 }
