@@ -276,6 +276,18 @@ kkt_status kkt_get_condensed(kkt_handle h, int inst, int *Kp, int *Ki, double *K
 kkt_status kkt_get_supernodes(kkt_handle h, int *nsuper, int *sn_first, int *sn_nrows,
                               int *sn_parent);
 
+/* Subtree blocks of the small supernodes (host plan of the block kernels; test export, needs only
+ * kkt_analyze).  kind 0 = the triangular solves (sblock.cuh), 1 = the block factorisation
+ * (fblock.cuh); cap = shared-memory budget per block in doubles; nwarps = warps per CTA.  Outputs
+ * (host, any may be NULL; call with NULLs first to learn the sizes): nblk, nmeta;
+ * blk[nblk][8] = {first supernode, root, levels, offset into meta, layout doubles, 0, 0, 0};
+ * blk_of[nsuper] = block index of a block root, -2 inside a block, -1 outside every block;
+ * meta[nmeta] = per block nlev + 1 level offsets then the local supernode ids by level;
+ * lrow[rows of all fronts] (kind 0) = backward row map; is_big[nsuper] = 1 for CTA-class
+ * supernodes.  Errors: KKT_ERR_ARG. */
+kkt_status kkt_get_blocks(kkt_handle h, int kind, int cap, int nwarps, int *nblk, int *nmeta, int *blk,
+                          int *blk_of, int *meta, int *lrow, int *is_big);
+
 /* Tracing (environment KKT_TRACE=1 at kkt_bind): [host] stamps[3][nsuper][8] = globaltimer
  * (ns) start, end and checkpoints 2..7 of every supernode task of instance 0 in the last factor (row 0), forward
  * (row 1) and backward (row 2) solve.  Blocking.  KKT_ERR_STATE when tracing is off. */

@@ -1944,6 +1944,49 @@ extern "C" kkt_status kkt_get_supernodes(kkt_handle h, int* nsuper, int* sn_firs
   return KKT_OK;
 }
 
+extern "C" kkt_status kkt_get_blocks(kkt_handle h, int kind, int cap, int nwarps, int* nblk, int* nmeta,
+                                     int* blk, int* blk_of, int* meta, int* lrow, int* is_big) {
+  if (!h || (kind != 0 && kind != 1) || cap <= 0 || nwarps <= 0) return KKT_ERR_ARG;
+  const Plan& P = h->P;
+  if (is_big)
+    for (int s = 0; s < P.ns; s++) is_big[s] = P.sn[s].big;
+  if (kind == 0) {
+    SBlockHost H;
+    build_sblocks(P, cap, nwarps, H);
+    if (nblk) *nblk = (int)H.blk.size();
+    if (nmeta) *nmeta = (int)H.meta.size();
+    for (size_t q = 0; blk && q < H.blk.size(); q++) {
+      const SBlk& B = H.blk[q];
+      const int v[8] = {B.s_lo, B.s_hi, B.nlev, B.m0, sb_layout(B.s_hi - B.s_lo + 1, B.nlev, B.nL, B.ncol, B.nr,
+                                                               B.nch, B.Rroot, nwarps).total, 0, 0, 0};
+      std::copy(v, v + 8, blk + 8 * q);
+    }
+    if (blk_of) std::copy(H.blk_of.begin(), H.blk_of.end(), blk_of);
+    if (meta) std::copy(H.meta.begin(), H.meta.end(), meta);
+    if (lrow) std::copy(H.lrow.begin(), H.lrow.end(), lrow);
+  } else {
+    FBlockHost H;
+    build_fblocks(P, cap, H);
+    if (nblk) *nblk = (int)H.blk.size();
+    if (nmeta) *nmeta = (int)H.meta.size();
+    for (size_t q = 0; blk && q < H.blk.size(); q++) {
+      const FBlk& B = H.blk[q];
+      const int v[8] = {B.s_lo, B.s_hi, B.nlev, B.m0, fb_layout(B.s_hi - B.s_lo + 1, B.nlev, B.nL, B.nU, B.nK, B.nr,
+                                                               B.nch).total, 0, 0, 0};
+      std::copy(v, v + 8, blk + 8 * q);
+    }
+    if (blk_of) {
+      std::fill(blk_of, blk_of + P.ns, -1);
+      for (size_t q = 0; q < H.blk.size(); q++) {
+        for (int t = H.blk[q].s_lo; t < H.blk[q].s_hi; t++) blk_of[t] = -2;
+        blk_of[H.blk[q].s_hi] = (int)q;
+      }
+    }
+    if (meta) std::copy(H.meta.begin(), H.meta.end(), meta);
+  }
+  return KKT_OK;
+}
+
 extern "C" kkt_status kkt_get_trace(kkt_handle h, long long* stamps) {
   if (!h || !stamps) return KKT_ERR_ARG;
   if (!h->trace_buf) { g_err = "tracing disabled: set KKT_TRACE=1 before kkt_bind"; return KKT_ERR_STATE; }

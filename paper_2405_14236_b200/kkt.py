@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
-           "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_trace", "kkt_launch_count",
+           "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_blocks", "kkt_get_trace", "kkt_launch_count",
            "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_tile_solve_trace", "kkt_last_error", "kkt_destroy"]
 
 
@@ -87,6 +87,7 @@ def lib(build_if_missing: bool = True):
             "kkt_recover_bounds": [P, P, P, P, P, D, P, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
+            "kkt_get_blocks": [P, I, I, I, P, P, P, P, P, P, P],
             "kkt_get_trace": [P, P],
             "kkt_factor_phase_ms": [P, P],
             "kkt_debug_steps": [P, P, I],
@@ -245,6 +246,22 @@ def kkt_get_supernodes(h):
     return f, r[:ns.value], p[:ns.value]
 
 
+def kkt_get_blocks(h, ns, nrows, kind=0, cap=6144, nwarps=8):
+    """Subtree blocks of the small supernodes (host plan; test export): (blk [nblk, 8], blk_of,
+    meta, lrow, is_big) -- see include/kkt.h."""
+    nb, nm = C.c_int(0), C.c_int(0)
+    _chk(lib().kkt_get_blocks(h, kind, cap, nwarps, C.byref(nb), C.byref(nm), None, None, None, None, None),
+         "kkt_get_blocks")
+    blk = np.zeros((max(nb.value, 1), 8), dtype=np.int32)
+    blk_of = np.zeros(ns, dtype=np.int32)
+    meta = np.zeros(max(nm.value, 1), dtype=np.int32)
+    lrow = np.zeros(max(nrows, 1), dtype=np.int32)
+    is_big = np.zeros(ns, dtype=np.int32)
+    _chk(lib().kkt_get_blocks(h, kind, cap, nwarps, C.byref(nb), C.byref(nm), _ptr(blk), _ptr(blk_of), _ptr(meta),
+                              _ptr(lrow) if kind == 0 else None, _ptr(is_big)), "kkt_get_blocks")
+    return blk[:nb.value], blk_of, meta[:nm.value], lrow[:nrows], is_big
+
+
 def kkt_get_trace(h, ns):
     t = np.zeros((3, max(ns, 1), 8), np.int64)
     _chk(lib().kkt_get_trace(h, t.ctypes.data), "kkt_get_trace")
@@ -356,6 +373,10 @@ class KKTSolver:
 
     def supernodes(self):
         return kkt_get_supernodes(self.h)
+
+    def blocks(self, kind=0, cap=6144, nwarps=8):
+        f, r, p = self.supernodes()
+        return kkt_get_blocks(self.h, len(r), int(r.sum()), kind, cap, nwarps)
 
     def trace(self):
         return kkt_get_trace(self.h, int(self.info["nsuper"]))

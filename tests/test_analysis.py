@@ -102,3 +102,57 @@ def test_state_errors_without_bind():
     assert K.KKT_STATUS[code] == "KKT_ERR_STATE"
     code = K.lib().kkt_condense(S.h, None, None, None, None, None, 0.0, 0.0, 0.0)
     assert K.KKT_STATUS[code] == "KKT_ERR_STATE"
+
+
+@pytest.mark.parametrize("cfg,kind,cap,nw", [("C2", 0, 6144, 8), ("C2", 0, 1024, 4), ("C5", 0, 4096, 4),
+                                             ("C2", 1, 6144, 4), ("C5", 1, 2048, 4), ("C1", 0, 2048, 8)])
+def test_subtree_block_plan(cfg, kind, cap, nw):
+    """Host plan of the block kernels (sblock.cuh / fblock.cuh): every block is a whole subtree of
+    small supernodes (a contiguous postorder range ending at its root), blocks are maximal and
+    disjoint, fit the budget, their level lists put every child below its parent, and the
+    backward row map sends own columns to their block-local column and every other row inside
+    the block's column range or the root's update rows."""
+    import paper_2405_14236_b200 as K
+    inst = make_config(cfg) if cfg != "C5" else make_config("C5", batch=1)
+    S = K.KKTSolver.from_instance(inst)
+    f, r, par = S.supernodes()
+    ns = len(r)
+    w = np.diff(f)
+    blk, blk_of, meta, lrow, big = S.blocks(kind, cap, nw)
+    assert len(blk) > 0
+    rp = np.concatenate([[0], np.cumsum(r)])
+    owner = -np.ones(ns, dtype=np.int64)
+    for b, (lo, hi, nlev, m0, total, *_rest) in enumerate(blk):
+        assert 0 <= lo <= hi < ns and blk_of[hi] == b and total <= cap
+        assert not big[lo:hi + 1].any()
+        assert (owner[lo:hi + 1] == -1).all()
+        owner[lo:hi + 1] = b
+        # whole subtree: every member's parent is in the range (except the root's), nothing
+        # outside the range has its parent inside
+        for t in range(lo, hi):
+            assert lo < par[t] <= hi and blk_of[t] == -2
+        inside = (par >= lo) & (par <= hi)
+        assert set(np.nonzero(inside)[0]) <= set(range(lo, hi + 1))
+        # maximal: the root's parent is big, absent, or outside every block
+        assert par[hi] < 0 or big[par[hi]] or blk_of[par[hi]] == -1
+        # level lists: a permutation, children strictly below their parent
+        nn = hi - lo + 1
+        lv = meta[m0:m0 + nlev + 1]
+        nodes = meta[m0 + nlev + 1:m0 + nlev + 1 + nn]
+        assert lv[0] == 0 and lv[-1] == nn and (np.diff(lv) >= 0).all()
+        assert sorted(nodes) == list(range(nn))
+        level = np.empty(nn, dtype=np.int64)
+        for l in range(nlev):
+            level[nodes[lv[l]:lv[l + 1]]] = l
+        for t in range(lo, hi):
+            assert level[t - lo] < level[par[t] - lo]
+        if kind == 0:  # backward row map
+            F0, ncol = f[lo], f[hi + 1] - f[lo]
+            Rroot = r[hi] - w[hi]
+            for t in range(lo, hi + 1):
+                lr = lrow[rp[t]:rp[t + 1]]
+                assert (lr[:w[t]] == f[t] - F0 + np.arange(w[t])).all()
+                assert ((lr >= 0) & (lr < ncol + Rroot)).all()
+    # small supernodes outside the blocks are exactly the blk_of == -1 non-big ones
+    assert ((owner >= 0) | big.astype(bool) | (blk_of == -1)).all()
+    assert (blk_of[big.astype(bool)] == -1).all()
