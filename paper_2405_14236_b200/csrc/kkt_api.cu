@@ -145,7 +145,7 @@ struct kkt_plan {
   long long* tile_trace = nullptr;  // KKT_TRACE: per-task stamps of the tile kernel
   // tile-task solves through the huge fronts (tsolve.cuh); KKT_TSOLVE=0: level kernel (hsolve.cuh)
   bool tsolve = false;
-  bool ts_chain = false;             // panel chains on one CTA (KKT_TS_CHAIN=1; default: per-step tasks)
+  bool ts_chain = false;             // panel chains on one CTA (KKT_TS_CHAIN=0: per-step tasks)
   TSolvePlan tsp{};
   void* ts_mem = nullptr;
   size_t ts_cnt_bytes = 0;
@@ -918,9 +918,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
         // chain tasks (one CTA per front panel, tsolve.cuh FCH / BCH) unless a panel is too tall
         int maxnbp = 0;
         for (const auto& fr_ : tph.fr) maxnbp = std::max(maxnbp, fr_.nbp);
-        // opt-in (KKT_TS_CHAIN=1): measured slower on C4 (root panel 65 -> 126 us: the per-tile
-        // CTA barriers of the streamed GEMVs cost more than the per-step hand-offs they remove)
-        h->ts_chain = maxnbp <= TS_NBP_MAX && getenv("KKT_TS_CHAIN") && atoi(getenv("KKT_TS_CHAIN")) > 0;
+        // measured: C4 solve 5.31 -> 4.73 ms, C3 15.8 -> 15.0 ms (KKT_TS_CHAIN=0: per-step tasks)
+        h->ts_chain = maxnbp <= TS_NBP_MAX && !(getenv("KKT_TS_CHAIN") && atoi(getenv("KKT_TS_CHAIN")) == 0);
         build_tile_solve_plan(P, tph, h->g_tile, h->ts_chain, tsh);
         h->ts_est_us = tsh.est_us;
         std::vector<TTask> st;

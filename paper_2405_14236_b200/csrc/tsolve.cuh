@@ -29,10 +29,11 @@
 namespace kkt {
 
 constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF = 5, TS_FCH = 6, TS_BCH = 7;
-// chain tasks (FCH / BCH): the whole panel of one front on one CTA, tiles streamed through a
-// ring of TS_RING shared-memory slots (cp.async groups), working vectors in shared memory
-constexpr int TS_RING = 4;
-constexpr int TS_NBP_MAX = 40;   // panel row blocks per front the chain tasks support
+// chain tasks (FCH / BCH): the whole panel of one front on one CTA, tiles streamed by TMA bulk
+// copies through a ring of TS_RING shared-memory slots (one mbarrier each, linear layout), one
+// warp per tile product, working vectors in shared memory
+constexpr int TS_RING = 6;
+constexpr int TS_NBP_MAX = 24;   // panel row blocks per front the chain tasks support
 constexpr int TS_SMEM_BYTES = (TS_RING * TBD + 2 * TS_NBP_MAX * 64 + 2 * 64) * 8;
 constexpr int TS_UCHUNK = 2;   // update-row tiles per backward task (parallel chunks, one slot each)
 
@@ -439,34 +440,75 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
   }
 }
 
-// cp.async groups: at most N outstanding
-template <int N>
-__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Per-warp products with a linear (column-major, unswizzled) 64 x 64 tile in shared memory.
+// gemv_n: o = A x, lane owns rows lane and lane + 32 (consecutive rows: conflict-free);
+// gemv_t: o = A^T x, lane owns columns lane and lane + 32, rows visited from r = lane on
+// (banks spread).  Two partial sums per output (even / odd steps), added at the end.
+__device__ __forceinline__ void ts_gemv_n_warp(const double* A, const double* x, double& o0, double& o1, int lane) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < 64; c += 2) {
+    const double x0 = x[c], x1 = x[c + 1];
+    a0 = fma(A[c * 64 + lane], x0, a0);
+    a1 = fma(A[c * 64 + lane + 32], x0, a1);
+    b0 = fma(A[(c + 1) * 64 + lane], x1, b0);
+    b1 = fma(A[(c + 1) * 64 + lane + 32], x1, b1);
+  }
+  o0 = a0 + b0;
+  o1 = a1 + b1;
+}
+__device__ __forceinline__ void ts_gemv_t_warp(const double* A, const double* x, double& o0, double& o1, int lane) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const double* A0 = A + lane * 64;
+  const double* A1 = A + (lane + 32) * 64;
+#pragma unroll 8
+  for (int s = 0; s < 64; s += 2) {
+    const int r0 = (s + lane) & 63, r1 = (s + 1 + lane) & 63;
+    const double x0 = x[r0], x1 = x[r1];
+    a0 = fma(A0[r0], x0, a0);
+    a1 = fma(A1[r0], x0, a1);
+    b0 = fma(A0[r1], x1, b0);
+    b1 = fma(A1[r1], x1, b1);
+  }
+  o0 = a0 + b0;
+  o1 = a1 + b1;
+}
+
+// Ring of TS_RING tile slots filled by TMA bulk copies (32 KB each); ph = parity bit per slot,
+// kept identical by every thread (each fill completes its slot's mbarrier phase once).
+struct TsRing {
+  double* slot;        // [TS_RING][TBD]
+  uint64_t* bar;       // [TS_RING] mbarriers
+};
+__device__ __forceinline__ void ts_ring_issue(const TsRing& R, int q, const double* g) {  // one thread
+  uint64_t* b = R.bar + (q % TS_RING);
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(b, TBD * 8);
+  bulk_g2s(R.slot + (q % TS_RING) * TBD, g, TBD * 8, b);
+}
+__device__ __forceinline__ void ts_ring_wait(const TsRing& R, int q, uint32_t ph) {
+  mbar_wait(R.bar + (q % TS_RING), (ph >> (q % TS_RING)) & 1u);
+}
 
 // FCH(f): forward through the front's panel on one CTA, right-looking over the panel's column
-// blocks -- y_j = L_jj^-1 a_j (inverse tile), then a_k -= L_kj y_j for every panel row block
-// k > j -- with the tiles (Xi_j, L_{j+1,j}, ..., L_{nbp-1,j}, Xi_{j+1}, ...) streamed through the
-// ring.  a_k receives its products in j-ascending order and every product is the 4-thread
-// GEMV of ts_gemv_n, so the sums are those of the per-step tasks (FC / panel FU).  y_j is
-// published per block (the update-row FU tasks consume it); no waits inside the chain.
-__device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* sm) {
+// blocks: y_j = L_jj^-1 a_j (the stored inverse tile (L_jj^-1)^T, transposed product on warp
+// 0), then a_k -= L_kj y_j for every panel row block k > j (one warp per tile); tiles streamed
+// in that order (Xi_j, L_{j+1,j}, ..., L_{nbp-1,j}, Xi_{j+1}, ...).  y_j is published per block
+// (the update-row FU tasks consume it).  Waits only on the front's gathers: deadlock-free.
+__device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* sm, const TsRing& R, uint32_t& ph) {
   const SnInfo I = X.P->sn[F.s];
-  const int nbp = F.nbp;
+  const int nbp = F.nbp, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* av = sm + TS_RING * TBD;     // [nbp][64]
   double* yv = av + TS_NBP_MAX * 64;   // [nbp][64], zero-padded
-  double* tmp = yv + TS_NBP_MAX * 64;  // [64]
   const int ntile = nbp + nbp * (nbp - 1) / 2;
-  int ij = 0, ik = 0;                  // issue cursor: column j, position k (k == j: Xi_j)
-  auto issue = [&](int q) {
-    if (q < ntile) {
-      const double* g = (ik == ij) ? X.inv + X.T->ibase[f] + (long long)ij * TBD : ts_tile(X, F, ik, ij);
-      tile_load_async(sm + (q % TS_RING) * TBD, g);
-      if (++ik == nbp) { ij++; ik = ij; }
-    }
-    cp_async_commit();
+  auto src = [&](int q) -> const double* {  // q-th tile of the stream
+    int j = 0, c = q;
+    while (c >= nbp - j) { c -= nbp - j; j++; }
+    return c == 0 ? X.inv + X.T->ibase[f] + (long long)j * TBD : ts_tile(X, F, j + c, j);
   };
-  for (int q = 0; q < TS_RING - 1; q++) issue(q);
+  __syncthreads();  // the previous task's shared-memory reads are done
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
   if (threadIdx.x == 0) {  // every panel block gathered
     for (int t = 0; t < nbp; t++)
       while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
@@ -478,59 +520,66 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
     const int t = q >> 6, e = q & 63;
     av[q] = e < tsize(F, t) ? __ldcg(X.Y + I.f0 + t * TBS + e) : 0.0;
   }
-  int j = 0, k = 0;                    // consume cursor
-  for (int q = 0; q < ntile; q++) {
-    issue(q + TS_RING - 1);
-    cp_async_wait_n<TS_RING - 1>();
+  __syncthreads();
+  int q = 0;  // consume cursor
+  for (int j = 0; j < nbp; j++) {
+    const int nk = tsize(F, j);
+    if (warp == 0) {  // y_j = (Xi_j)^T a_j
+      ts_ring_wait(R, q, ph);
+      double o0, o1;
+      ts_gemv_t_warp(R.slot + (q % TS_RING) * TBD, av + j * 64, o0, o1, lane);
+      yv[j * 64 + lane] = lane < nk ? o0 : 0.0;
+      yv[j * 64 + lane + 32] = lane + 32 < nk ? o1 : 0.0;
+      if (lane < nk) X.Y[I.f0 + j * TBS + lane] = o0;
+      if (lane + 32 < nk) X.Y[I.f0 + j * TBS + lane + 32] = o1;
+    }
     __syncthreads();
-    const double* T = sm + (q % TS_RING) * TBD;
-    if (k == j) {                      // y_j = -(gemv_t(0, Xi_j, a_j))
-      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
-      __syncthreads();
-      ts_gemv_t(tmp, T, av + j * 64);
-      const int nk = tsize(F, j);
-      if (threadIdx.x < TBS) {
-        const double y = -tmp[threadIdx.x];
-        yv[j * 64 + threadIdx.x] = threadIdx.x < nk ? y : 0.0;
-        if (threadIdx.x < nk) X.Y[I.f0 + j * TBS + threadIdx.x] = y;
+    ph ^= 1u << (q % TS_RING);
+    if (threadIdx.x == 0) {
+      if (q + TS_RING < ntile) ts_ring_issue(R, q + TS_RING, src(q + TS_RING));
+      __threadfence();
+      st_release(ts_yf(*X.S, X.cnt, F, f, j), 1);
+    }
+    q++;
+    for (int k0 = j + 1; k0 < nbp; k0 += TS_RING) {  // waves of at most TS_RING tiles
+      const int nw = min(TS_RING, nbp - k0);
+      if (warp < nw) {
+        const int qq = q + warp, k = k0 + warp;
+        ts_ring_wait(R, qq, ph);
+        double o0, o1;
+        ts_gemv_n_warp(R.slot + (qq % TS_RING) * TBD, yv + j * 64, o0, o1, lane);
+        av[k * 64 + lane] -= o0;
+        av[k * 64 + lane + 32] -= o1;
       }
       __syncthreads();
-      if (threadIdx.x == 0) { __threadfence(); st_release(ts_yf(*X.S, X.cnt, F, f, j), 1); }
-    } else {                           // a_k -= L_kj y_j
-      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
-      __syncthreads();
-      ts_gemv_n(tmp, T, yv + j * 64);
-      if (threadIdx.x < TBS) av[k * 64 + threadIdx.x] -= -tmp[threadIdx.x];
+      for (int u = 0; u < nw; u++) ph ^= 1u << ((q + u) % TS_RING);
+      if (threadIdx.x == 0)
+        for (int u = 0; u < nw; u++)
+          if (q + u + TS_RING < ntile) ts_ring_issue(R, q + u + TS_RING, src(q + u + TS_RING));
+      q += nw;
     }
-    if (++k == nbp) { j++; k = j; }
-    __syncthreads();                   // slot q is reused by the next issue
   }
-  cp_async_wait_n<0>();
 }
 
 // BCH(f): backward through the panel on one CTA: a_k = y_k - (update-row chunks, last first),
-// then for i = nbp-1 .. 0: x_i = L_ii^-T a_i (inverse tile), a_k -= L_ik^T x_i for k < i
-// (tiles Xi_i, L_{i,i-1}, ..., L_{i,0} streamed).  a_k gets the panel products in i-descending
-// order, the one of k+1 last, as in the per-step tasks (BC / panel BU).
-__device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* sm) {
+// then for i = nbp-1 .. 0: x_i = L_ii^-T a_i (inverse tile, warp 0), a_k -= L_ik^T x_i for
+// k < i (one warp per tile); tiles streamed as Xi_i, L_{i,i-1}, ..., L_{i,0}, Xi_{i-1}, ...
+__device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* sm, const TsRing& R, uint32_t& ph) {
   const DevPlan& P = *X.P;
   const SnInfo I = P.sn[F.s];
-  const int nbp = F.nbp;
+  const int nbp = F.nbp, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* av = sm + TS_RING * TBD;
   double* xs = av + TS_NBP_MAX * 64;
-  double* tmp = xs + TS_NBP_MAX * 64;
   const int nchunk = (F.nt - F.nbp + TS_UCHUNK - 1) / TS_UCHUNK;
   const int ntile = nbp + nbp * (nbp - 1) / 2;
-  int ii = nbp - 1, ik = nbp - 1;      // issue cursor: row block i, column k (k == i: Xi_i)
-  auto issue = [&](int q) {
-    if (q < ntile) {
-      const double* g = (ik == ii) ? X.inv + X.T->ibase[f] + (long long)ii * TBD : ts_tile(X, F, ii, ik);
-      tile_load_async(sm + (q % TS_RING) * TBD, g);
-      if (--ik < 0) { ii--; ik = ii; }
-    }
-    cp_async_commit();
+  auto src = [&](int q) -> const double* {  // q-th tile: row block i from the top, Xi_i then L(i, i-1 .. 0)
+    int i = nbp - 1, c = q;
+    while (c >= i + 1) { c -= i + 1; i--; }
+    return c == 0 ? X.inv + X.T->ibase[f] + (long long)i * TBD : ts_tile(X, F, i, i - c);
   };
-  for (int q = 0; q < TS_RING - 1; q++) issue(q);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
   if (threadIdx.x == 0) {  // the forward chain done, every update-row chunk product present
     for (int t = 0; t < nbp; t++) {
       while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
@@ -548,42 +597,54 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
     for (int c = nchunk - 1; c >= 0; c--) a -= __ldcg(q0 + (long long)(F.nbp + c) * TBS);
     av[q] = a;
   }
-  int i = nbp - 1, k = nbp - 1;        // consume cursor
-  for (int q = 0; q < ntile; q++) {
-    issue(q + TS_RING - 1);
-    cp_async_wait_n<TS_RING - 1>();
-    __syncthreads();
-    const double* T = sm + (q % TS_RING) * TBD;
-    if (k == i) {                      // x_i = -(gemv_n(0, Xi_i, a_i))
-      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
-      __syncthreads();
-      ts_gemv_n(tmp, T, av + i * 64);
-      const int nk = tsize(F, i);
-      if (threadIdx.x < TBS) {
-        const double x = -tmp[threadIdx.x];
-        xs[i * 64 + threadIdx.x] = threadIdx.x < nk ? x : 0.0;
-        if (threadIdx.x < nk) {
-          const int c = I.f0 + i * TBS + threadIdx.x;
-          X.Xp[c] = x;
-          X.xout[__ldg(P.perm + c)] = x;
-        }
+  __syncthreads();
+  int q = 0;
+  for (int i = nbp - 1; i >= 0; i--) {
+    const int nk = tsize(F, i);
+    if (warp == 0) {  // x_i = Xi_i a_i
+      ts_ring_wait(R, q, ph);
+      double o0, o1;
+      ts_gemv_n_warp(R.slot + (q % TS_RING) * TBD, av + i * 64, o0, o1, lane);
+      xs[i * 64 + lane] = lane < nk ? o0 : 0.0;
+      xs[i * 64 + lane + 32] = lane + 32 < nk ? o1 : 0.0;
+      if (lane < nk) {
+        const int c = I.f0 + i * TBS + lane;
+        X.Xp[c] = o0;
+        X.xout[__ldg(P.perm + c)] = o0;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        st_release(ts_xf(*X.S, X.cnt, F, f, i), 1);
-        red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+      if (lane + 32 < nk) {
+        const int c = I.f0 + i * TBS + lane + 32;
+        X.Xp[c] = o1;
+        X.xout[__ldg(P.perm + c)] = o1;
       }
-    } else {                           // a_k -= L_ik^T x_i
-      if (threadIdx.x < TBS) tmp[threadIdx.x] = 0.0;
-      __syncthreads();
-      ts_gemv_t(tmp, T, xs + i * 64);
-      if (threadIdx.x < TBS) av[k * 64 + threadIdx.x] -= -tmp[threadIdx.x];
     }
-    if (--k < 0) { i--; k = i; }
     __syncthreads();
+    ph ^= 1u << (q % TS_RING);
+    if (threadIdx.x == 0) {
+      if (q + TS_RING < ntile) ts_ring_issue(R, q + TS_RING, src(q + TS_RING));
+      __threadfence();
+      st_release(ts_xf(*X.S, X.cnt, F, f, i), 1);
+      red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+    }
+    q++;
+    for (int c0 = 0; c0 < i; c0 += TS_RING) {  // tiles L(i, i-1-c), waves of at most TS_RING
+      const int nw = min(TS_RING, i - c0);
+      if (warp < nw) {
+        const int qq = q + warp, k = i - 1 - (c0 + warp);
+        ts_ring_wait(R, qq, ph);
+        double o0, o1;
+        ts_gemv_t_warp(R.slot + (qq % TS_RING) * TBD, xs + i * 64, o0, o1, lane);
+        av[k * 64 + lane] -= o0;
+        av[k * 64 + lane + 32] -= o1;
+      }
+      __syncthreads();
+      for (int u = 0; u < nw; u++) ph ^= 1u << ((q + u) % TS_RING);
+      if (threadIdx.x == 0)
+        for (int u = 0; u < nw; u++)
+          if (q + u + TS_RING < ntile) ts_ring_issue(R, q + u + TS_RING, src(q + u + TS_RING));
+      q += nw;
+    }
   }
-  cp_async_wait_n<0>();
 }
 
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, TilePlan T, TSolvePlan S,
@@ -594,7 +655,12 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, 
                                                                    const int* __restrict__ done) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int s_task;
+  __shared__ __align__(8) uint64_t s_bar[TS_RING];
   if (done && done[P.batch] == 0) return;  // every instance has finished refining (grid-uniform)
+  if (threadIdx.x < TS_RING) mbar_init(s_bar + threadIdx.x, 1);
+  __syncthreads();
+  const TsRing ring{tsm, s_bar};
+  uint32_t ph = 0;
   int* ticket = S.cnt + (long long)P.batch * S.ncnt;
   for (;;) {
     __syncthreads();
@@ -626,8 +692,8 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_solve_kernel(DevPlan P, 
       case TS_FC: ts_fchain(X, F, tk.y, tk.w, tsm); break;
       case TS_BU: ts_bupdate(X, F, tk.y, tk.w, tk.z, tsm); break;
       case TS_UF: ts_ufinal(X, F, tk.y, tk.z, tsm); break;
-      case TS_FCH: ts_fchain_front(X, F, tk.y, tsm); break;
-      case TS_BCH: ts_bchain_front(X, F, tk.y, tsm); break;
+      case TS_FCH: ts_fchain_front(X, F, tk.y, tsm, ring, ph); break;
+      case TS_BCH: ts_bchain_front(X, F, tk.y, tsm, ring, ph); break;
       default: ts_bchain(X, F, tk.y, tk.w, tsm); break;
     }
     if (S.trace) {
