@@ -921,6 +921,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
         // measured: C4 solve 5.31 -> 4.73 ms, C3 15.8 -> 15.0 ms (KKT_TS_CHAIN=0: per-step tasks)
         h->ts_chain = maxnbp <= TS_NBP_MAX && !(getenv("KKT_TS_CHAIN") && atoi(getenv("KKT_TS_CHAIN")) == 0);
         build_tile_solve_plan(P, tph, h->g_tile, h->ts_chain, tsh);
+        h->tsp.wave = 4;  // measured C4 8.69 / 8.73 / 8.76 ms at 4 / 3 / 2
+        if (const char* e = getenv("KKT_TS_WAVE")) h->tsp.wave = std::min(std::min(TS_RING, TILE_THREADS / 64), std::max(1, atoi(e)));
         h->ts_est_us = tsh.est_us;
         std::vector<TTask> st;
         st.reserve(tsh.tasks.size() * B);

@@ -49,6 +49,7 @@ struct TSolvePlan {
   long long* trace;    // optional [ntask][4]
   double* part;        // [batch][part_doubles] partial products (one 64-slot per producer)
   long long part_doubles;
+  int wave;            // chain tasks: tiles per wave (<= min(TS_RING, 4): two warps per tile)
   const long long* pbase;  // [nf]: forward slots P[t][k] (nt x nbp x 64), then backward Q[k][s]
                            // (nbp x nt x 64; s = source panel block i, or nbp + c = update-row chunk c)
 };
@@ -440,38 +441,30 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
   }
 }
 
-// Per-warp products with a linear (column-major, unswizzled) 64 x 64 tile in shared memory.
-// gemv_n: o = A x, lane owns rows lane and lane + 32 (consecutive rows: conflict-free);
-// gemv_t: o = A^T x, lane owns columns lane and lane + 32, rows visited from r = lane on
-// (banks spread).  Two partial sums per output (even / odd steps), added at the end.
-__device__ __forceinline__ void ts_gemv_n_warp(const double* A, const double* x, double& o0, double& o1, int lane) {
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+// Products with a linear (column-major, unswizzled) 64 x 64 tile in shared memory, two warps
+// per tile: gemv_n gives row h * 32 + lane of A x (consecutive rows across the lanes:
+// conflict-free), gemv_t column h * 32 + lane of A^T x with the rows visited from r = lane on
+// (banks spread).  Two partial sums (even / odd steps) added at the end.
+__device__ __forceinline__ double ts_gemv_n_half(const double* A, const double* x, int h, int lane) {
+  double a = 0.0, b = 0.0;
+  const double* Ar = A + h * 32 + lane;
 #pragma unroll 8
   for (int c = 0; c < 64; c += 2) {
-    const double x0 = x[c], x1 = x[c + 1];
-    a0 = fma(A[c * 64 + lane], x0, a0);
-    a1 = fma(A[c * 64 + lane + 32], x0, a1);
-    b0 = fma(A[(c + 1) * 64 + lane], x1, b0);
-    b1 = fma(A[(c + 1) * 64 + lane + 32], x1, b1);
+    a = fma(Ar[c * 64], x[c], a);
+    b = fma(Ar[(c + 1) * 64], x[c + 1], b);
   }
-  o0 = a0 + b0;
-  o1 = a1 + b1;
+  return a + b;
 }
-__device__ __forceinline__ void ts_gemv_t_warp(const double* A, const double* x, double& o0, double& o1, int lane) {
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-  const double* A0 = A + lane * 64;
-  const double* A1 = A + (lane + 32) * 64;
+__device__ __forceinline__ double ts_gemv_t_half(const double* A, const double* x, int h, int lane) {
+  double a = 0.0, b = 0.0;
+  const double* Ac = A + (h * 32 + lane) * 64;
 #pragma unroll 8
   for (int s = 0; s < 64; s += 2) {
     const int r0 = (s + lane) & 63, r1 = (s + 1 + lane) & 63;
-    const double x0 = x[r0], x1 = x[r1];
-    a0 = fma(A0[r0], x0, a0);
-    a1 = fma(A1[r0], x0, a1);
-    b0 = fma(A0[r1], x1, b0);
-    b1 = fma(A1[r1], x1, b1);
+    a = fma(Ac[r0], x[r0], a);
+    b = fma(Ac[r1], x[r1], b);
   }
-  o0 = a0 + b0;
-  o1 = a1 + b1;
+  return a + b;
 }
 
 // Ring of TS_RING tile slots filled by TMA bulk copies (32 KB each); ph = parity bit per slot,
@@ -524,14 +517,12 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
   int q = 0;  // consume cursor
   for (int j = 0; j < nbp; j++) {
     const int nk = tsize(F, j);
-    if (warp == 0) {  // y_j = (Xi_j)^T a_j
+    if (warp < 2) {  // y_j = (Xi_j)^T a_j, column halves on warps 0 and 1
       ts_ring_wait(R, q, ph);
-      double o0, o1;
-      ts_gemv_t_warp(R.slot + (q % TS_RING) * TBD, av + j * 64, o0, o1, lane);
-      yv[j * 64 + lane] = lane < nk ? o0 : 0.0;
-      yv[j * 64 + lane + 32] = lane + 32 < nk ? o1 : 0.0;
-      if (lane < nk) X.Y[I.f0 + j * TBS + lane] = o0;
-      if (lane + 32 < nk) X.Y[I.f0 + j * TBS + lane + 32] = o1;
+      const int e = warp * 32 + lane;
+      const double o = ts_gemv_t_half(R.slot + (q % TS_RING) * TBD, av + j * 64, warp, lane);
+      yv[j * 64 + e] = e < nk ? o : 0.0;
+      if (e < nk) X.Y[I.f0 + j * TBS + e] = o;
     }
     __syncthreads();
     ph ^= 1u << (q % TS_RING);
@@ -541,15 +532,13 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
       st_release(ts_yf(*X.S, X.cnt, F, f, j), 1);
     }
     q++;
-    for (int k0 = j + 1; k0 < nbp; k0 += TS_RING) {  // waves of at most TS_RING tiles
-      const int nw = min(TS_RING, nbp - k0);
-      if (warp < nw) {
-        const int qq = q + warp, k = k0 + warp;
+    const int wv = X.S->wave;
+    for (int k0 = j + 1; k0 < nbp; k0 += wv) {  // waves of at most wv tiles (the ring holds the next ones)
+      const int nw = min(wv, nbp - k0);
+      if ((warp >> 1) < nw) {  // two warps per tile (row halves)
+        const int t = warp >> 1, hh = warp & 1, qq = q + t, k = k0 + t;
         ts_ring_wait(R, qq, ph);
-        double o0, o1;
-        ts_gemv_n_warp(R.slot + (qq % TS_RING) * TBD, yv + j * 64, o0, o1, lane);
-        av[k * 64 + lane] -= o0;
-        av[k * 64 + lane + 32] -= o1;
+        av[k * 64 + hh * 32 + lane] -= ts_gemv_n_half(R.slot + (qq % TS_RING) * TBD, yv + j * 64, hh, lane);
       }
       __syncthreads();
       for (int u = 0; u < nw; u++) ph ^= 1u << ((q + u) % TS_RING);
@@ -601,21 +590,15 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
   int q = 0;
   for (int i = nbp - 1; i >= 0; i--) {
     const int nk = tsize(F, i);
-    if (warp == 0) {  // x_i = Xi_i a_i
+    if (warp < 2) {  // x_i = Xi_i a_i, row halves on warps 0 and 1
       ts_ring_wait(R, q, ph);
-      double o0, o1;
-      ts_gemv_n_warp(R.slot + (q % TS_RING) * TBD, av + i * 64, o0, o1, lane);
-      xs[i * 64 + lane] = lane < nk ? o0 : 0.0;
-      xs[i * 64 + lane + 32] = lane + 32 < nk ? o1 : 0.0;
-      if (lane < nk) {
-        const int c = I.f0 + i * TBS + lane;
-        X.Xp[c] = o0;
-        X.xout[__ldg(P.perm + c)] = o0;
-      }
-      if (lane + 32 < nk) {
-        const int c = I.f0 + i * TBS + lane + 32;
-        X.Xp[c] = o1;
-        X.xout[__ldg(P.perm + c)] = o1;
+      const int e = warp * 32 + lane;
+      const double o = ts_gemv_n_half(R.slot + (q % TS_RING) * TBD, av + i * 64, warp, lane);
+      xs[i * 64 + e] = e < nk ? o : 0.0;
+      if (e < nk) {
+        const int c = I.f0 + i * TBS + e;
+        X.Xp[c] = o;
+        X.xout[__ldg(P.perm + c)] = o;
       }
     }
     __syncthreads();
@@ -627,15 +610,13 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
       red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
     }
     q++;
-    for (int c0 = 0; c0 < i; c0 += TS_RING) {  // tiles L(i, i-1-c), waves of at most TS_RING
-      const int nw = min(TS_RING, i - c0);
-      if (warp < nw) {
-        const int qq = q + warp, k = i - 1 - (c0 + warp);
+    const int wv = X.S->wave;
+    for (int c0 = 0; c0 < i; c0 += wv) {  // tiles L(i, i-1-c), waves of at most wv
+      const int nw = min(wv, i - c0);
+      if ((warp >> 1) < nw) {  // two warps per tile (column halves)
+        const int t = warp >> 1, hh = warp & 1, qq = q + t, k = i - 1 - (c0 + t);
         ts_ring_wait(R, qq, ph);
-        double o0, o1;
-        ts_gemv_t_warp(R.slot + (qq % TS_RING) * TBD, xs + i * 64, o0, o1, lane);
-        av[k * 64 + lane] -= o0;
-        av[k * 64 + lane + 32] -= o1;
+        av[k * 64 + hh * 32 + lane] -= ts_gemv_t_half(R.slot + (qq % TS_RING) * TBD, xs + i * 64, hh, lane);
       }
       __syncthreads();
       for (int u = 0; u < nw; u++) ph ^= 1u << ((q + u) % TS_RING);
