@@ -227,7 +227,7 @@ __device__ __forceinline__ void tile_diag32(double* T, int kb, int lane, double*
   for (int c = 0; c < 32; c++) {
     const bool b_ = pivot_bad(d);
     bad |= (b_ ? 1u : 0u) << c;
-    const double iv = b_ ? nan_d() : inv;
+    const double iv = inv;  // a bad pivot already gives a non-finite rsqrt (R6): the check stays off the chain
     if (lane == c) myinv = iv;
     const double l = (lane > c) ? a[c] * iv : (lane == c ? d * iv : 0.0);
     a[c] = l;
