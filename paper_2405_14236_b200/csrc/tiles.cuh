@@ -428,6 +428,59 @@ __device__ __forceinline__ void tile_potrf64(double* T, int kb, double* dinv, do
   __syncthreads();
 }
 
+// C(rb:rb+8, cb:cb+32) -= A(rb:rb+8, :) A(cb:cb+32, :)^T by one warp (the per-warp DMMA block of
+// tile_gemm_nt_smem, same k order: the same sums)
+__device__ __forceinline__ void tile_syrk_strip(double* C, const double* A, int rb, int cb) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double acc[4][2];
+#pragma unroll
+  for (int n = 0; n < 4; n++) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < TBS / 4; ks++) {
+    const int kk = 4 * ks + lc;
+    const double a = A[tsw(rb + lr, kk)];
+    double b[4];
+#pragma unroll
+    for (int n = 0; n < 4; n++) b[n] = A[tsw(cb + 8 * n + lr, kk)];
+#pragma unroll
+    for (int n = 0; n < 4; n++) dmma_nv(acc[n][0], acc[n][1], a, b[n]);
+  }
+#pragma unroll
+  for (int n = 0; n < 4; n++)
+#pragma unroll
+    for (int e = 0; e < 2; e++) C[tsw(rb + lr, cb + 8 * n + 2 * lc + e)] -= acc[n][e];
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// CRIT's diagonal step, A2 -= A1 A1^T then Cholesky of A2, with the update overlapped: warps 0-3
+// update the top-left 32 x 32 block while warps 4-7 update the bottom-left one; warp 0 then
+// factors the top-left block while warps 4-7 update the bottom-right one (the top-right block is
+// above the diagonal: never read).  Same products and factorisation as tile_gemm_nt_smem +
+// tile_potrf64.
+__device__ __forceinline__ void tile_syrk_potrf64(double* A2, const double* A1, int kb, double* dinv, double* sinv,
+                                                  double* L11s, int* fail_k) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kb0 = min(kb, 32), kb1 = max(kb - 32, 0);
+  tile_syrk_strip(A2, A1, warp < 4 ? 8 * warp : 32 + 8 * (warp - 4), 0);
+  if (warp < 4) named_bar(1, 128);  // the top-left block is complete for warp 0
+  if (warp == 0) tile_diag32<0>(A2, kb0, lane, dinv, sinv, L11s, fail_k);
+  else if (warp >= 4 && kb1 > 0) tile_syrk_strip(A2, A1, 32 + 8 * (warp - 4), 32);
+  __syncthreads();
+  if (kb1 > 0) {
+    tile_rowsolve32<0>(A2, 32, 32, A2, sinv);
+    __syncthreads();
+    tile_block_update(A2, 32, 32, A2, 0, 32);
+    __syncthreads();
+    if (warp == 0) tile_diag32<32>(A2, kb1, lane, dinv, sinv, L11s, fail_k);
+  } else if (warp == 0) {
+    for (int c = 0; c < 64; c++) A2[tsw(32 + lane, c)] = 0.0;
+    sinv[32 + lane] = 0.0;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------------------ tasks
 struct TileCtx {
   const DevPlan* P;
@@ -661,10 +714,13 @@ __device__ void task_crit(const TileCtx& X, const TFront& F, int k, double* sm) 
   if (X.T->panel) tile_to_panel(F, A1, X.Lx + I.Lp, k + 1, k);
   publish_cnt(tile_cnt(X, F, k + 1, k), k + 2);
   // A2 -= L1 L1^T, Cholesky of A2
-  tile_gemm_nt_smem<SG>(A2, A1, A1, ssg);
-  if (SG) tile_potrf64_signed(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail, ssg,
-                              X.Sg + I.f0 + (k + 1) * TBS, s_kjj, X.cnt3);
-  else tile_potrf64(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail);
+  if (SG) {
+    tile_gemm_nt_smem<SG>(A2, A1, A1, ssg);
+    tile_potrf64_signed(A2, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail, ssg,
+                        X.Sg + I.f0 + (k + 1) * TBS, s_kjj, X.cnt3);
+  } else {
+    tile_syrk_potrf64(A2, A1, tsize(F, k + 1), X.Dv + I.f0 + (k + 1) * TBS, sinv, L11s, &s_fail);
+  }
   tile_store(tile_ptr(X, F, k + 1, k + 1), A2);
   if (X.T->panel) tile_to_panel(F, A2, X.Lx + I.Lp, k + 1, k + 1);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + (k + 1) * TBS + s_fail);
