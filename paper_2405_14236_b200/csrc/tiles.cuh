@@ -211,9 +211,11 @@ __device__ __forceinline__ void tile_gemm_nt_smem(double* C, const double* A, co
 // dense.cuh ll_diag_warp: fma -> shuffle -> rsqrt -> mul per column, column broadcasts through the
 // 32 x 32 scratch L11s.  Writes L into T (zeros above the diagonal), the inverse pivots into
 // sinv[c0 ..] and dinv[c0 ..] and the first failing column (tile-local) into *fail_k.
-template <int c0>
+// PUB: also publish each finished column to another warp (tile_syrk_potrf64's row solve
+// follower): inverse pivot into sinv, then *pflag = c + 1 after the column is in L11s.
+template <int c0, bool PUB = false>
 __device__ __forceinline__ void tile_diag32(double* T, int kb, int lane, double* dinv, double* sinv,
-                                            double* L11s, int* fail_k) {
+                                            double* L11s, int* fail_k, volatile int* pflag = nullptr) {
   const int row = c0 + lane;
   double a[32];
 #pragma unroll
@@ -229,6 +231,7 @@ __device__ __forceinline__ void tile_diag32(double* T, int kb, int lane, double*
     bad |= (b_ ? 1u : 0u) << c;
     const double iv = inv;  // a bad pivot already gives a non-finite rsqrt (R6): the check stays off the chain
     if (lane == c) myinv = iv;
+    if (PUB && lane == c) sinv[c0 + c] = (c < kb) ? iv : 0.0;
     const double l = (lane > c) ? a[c] * iv : (lane == c ? d * iv : 0.0);
     a[c] = l;
     L11s[c * 32 + lane] = l;
@@ -237,6 +240,7 @@ __device__ __forceinline__ void tile_diag32(double* T, int kb, int lane, double*
       inv = rsqrt_fast(d);
     }
     warp_bar();
+    if (PUB && lane == 0) { __threadfence_block(); *pflag = c + 1; }
     const double2* col2 = reinterpret_cast<const double2*>(L11s + c * 32);
     if ((c + 1) & 1) a[c + 1] = fma(-l, L11s[c * 32 + c + 1], a[c + 1]);
 #pragma unroll
@@ -454,23 +458,44 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// CRIT's diagonal step, A2 -= A1 A1^T then Cholesky of A2, with the update overlapped: warps 0-3
+// CRIT's diagonal step (POTRF0: A1 = NULL, no update), A2 -= A1 A1^T then Cholesky of A2, with the update overlapped: warps 0-3
 // update the top-left 32 x 32 block while warps 4-7 update the bottom-left one; warp 0 then
 // factors the top-left block while warps 4-7 update the bottom-right one (the top-right block is
 // above the diagonal: never read).  Same products and factorisation as tile_gemm_nt_smem +
 // tile_potrf64.
 __device__ __forceinline__ void tile_syrk_potrf64(double* A2, const double* A1, int kb, double* dinv, double* sinv,
                                                   double* L11s, int* fail_k) {
+  __shared__ int s_col;  // columns of the top-left factor published to the row-solve follower
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kb0 = min(kb, 32), kb1 = max(kb - 32, 0);
-  tile_syrk_strip(A2, A1, warp < 4 ? 8 * warp : 32 + 8 * (warp - 4), 0);
-  if (warp < 4) named_bar(1, 128);  // the top-left block is complete for warp 0
-  if (warp == 0) tile_diag32<0>(A2, kb0, lane, dinv, sinv, L11s, fail_k);
-  else if (warp >= 4 && kb1 > 0) tile_syrk_strip(A2, A1, 32 + 8 * (warp - 4), 32);
+  if (threadIdx.x == 0) s_col = 0;
+  if (A1) tile_syrk_strip(A2, A1, warp < 4 ? 8 * warp : 32 + 8 * (warp - 4), 0);
+  __syncthreads();  // top-left and bottom-left blocks updated
+  if (warp == 0) {
+    tile_diag32<0, true>(A2, kb0, lane, dinv, sinv, L11s, fail_k, &s_col);
+  } else if (warp == 1 && kb1 > 0) {
+    // L21 = A21 L11^-T for rows 32..63, one column behind warp 0 (tile_rowsolve32's arithmetic,
+    // L11 read from the published columns)
+    const int row = 32 + lane;
+    double x[32];
+#pragma unroll
+    for (int c = 0; c < 32; c++) x[c] = A2[tsw(row, c)];
+    volatile int* vc = &s_col;
+#pragma unroll
+    for (int c = 0; c < 32; c++) {
+      while (*vc < c + 1) { }
+      __threadfence_block();
+      x[c] *= sinv[c];
+#pragma unroll
+      for (int cc = c + 1; cc < 32; cc++) x[cc] = fma(-x[c], L11s[c * 32 + cc], x[cc]);
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c++) A2[tsw(row, c)] = x[c];
+  } else if (A1 && warp >= 4 && kb1 > 0) {
+    tile_syrk_strip(A2, A1, 32 + 8 * (warp - 4), 32);
+  }
   __syncthreads();
   if (kb1 > 0) {
-    tile_rowsolve32<0>(A2, 32, 32, A2, sinv);
-    __syncthreads();
     tile_block_update(A2, 32, 32, A2, 0, 32);
     __syncthreads();
     if (warp == 0) tile_diag32<32>(A2, kb1, lane, dinv, sinv, L11s, fail_k);
@@ -664,7 +689,7 @@ __device__ void task_potrf0(const TileCtx& X, const TFront& F, double* sm) {
   __syncthreads();
   const SnInfo I = X.P->sn[F.s];
   if (SG) tile_potrf64_signed(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail, ssg, X.Sg + I.f0, s_kjj, X.cnt3);
-  else tile_potrf64(T0, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail);
+  else tile_syrk_potrf64(T0, nullptr, tsize(F, 0), X.Dv + I.f0, sinv, L11s, &s_fail);
   tile_store(tile_ptr(X, F, 0, 0), T0);
   if (X.T->panel) tile_to_panel(F, T0, X.Lx + I.Lp, 0, 0);
   if (threadIdx.x == 0 && s_fail >= 0) atomicMin(X.fail_all, I.f0 + s_fail);
