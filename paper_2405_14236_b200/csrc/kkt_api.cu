@@ -484,9 +484,29 @@ extern "C" kkt_status kkt_bind(kkt_handle h, int device, void* d_workspace, size
   return st;
 }
 
+// Factor start lists by the estimated longest path to the top of the small + big phases (the
+// critical chains first): small leaves (up_s) and the first big tasks (up_bf).  Estimated
+// durations (us, C4 traces): small supernode 6, big 12 + r w / 400; huge fronts belong to the
+// next kernel.  Scheduling only: every supernode's arithmetic is unchanged.
+static void order_factor_lists(Plan& P) {
+  const int ns = P.ns;
+  if (ns == 0) return;
+  std::vector<double> up(ns, 0.0);
+  for (int s = ns - 1; s >= 0; s--) {
+    const SnInfo& I = P.sn[s];
+    const double d = I.huge ? 0.0 : (I.big ? 12.0 + (double)I.r * I.w / 400.0 : 6.0);
+    const int par = P.sn_parent[s];
+    up[s] = d + ((par >= 0 && !P.sn[par].huge) ? up[par] : 0.0);
+  }
+  auto by_up = [&](int a, int b) { return up[a] != up[b] ? up[a] > up[b] : a < b; };
+  std::stable_sort(P.up_s.begin(), P.up_s.end(), by_up);
+  std::stable_sort(P.up_bf.begin(), P.up_bf.end(), by_up);
+}
+
 static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t bytes,
                             kkt_stream_t stream) {
   CUDA_TRY(cudaSetDevice(device));
+  if (!(getenv("KKT_FACTOR_ORDER") && atoi(getenv("KKT_FACTOR_ORDER")) == 0)) order_factor_lists(h->P);
   h->device = device;
   h->stream = (cudaStream_t)stream;
   h->ls = h->stream;
@@ -686,6 +706,16 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
   const long long ts = (long long)P.order_s.size() * P.batch, tb = (long long)P.order_b.size() * P.batch;
   if (h->fsmall_occ == 3) CUDA_TRY(grid_of(factor_small_kernel<3>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
   else CUDA_TRY(grid_of(factor_small_kernel<1>, KKT_WPB * 32, h->fsmall_smem, us, KKT_WPB, &h->g_fsmall));
+  {  // leave KKT_FBIG_RESERVE SMs to the (programmatically overlapped) big kernel so that the
+     // critical big chain starts while the throughput-bound small phase is still running
+    const int reserve = getenv("KKT_FBIG_RESERVE") ? atoi(getenv("KKT_FBIG_RESERVE")) : 0;
+    if (reserve > 0 && reserve < h->sms) {
+      int occ = 0;
+      if (h->fsmall_occ == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_small_kernel<3>, KKT_WPB * 32, h->fsmall_smem);
+      else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_small_kernel<1>, KKT_WPB * 32, h->fsmall_smem);
+      h->g_fsmall = std::max(1, std::min(h->g_fsmall, std::max(occ, 1) * (h->sms - reserve)));
+    }
+  }
   CUDA_TRY(grid_of(factor_big_kernel<false>, KKT_BNT, h->fbig_smem, ub, 1, &h->g_fbig));
   CUDA_TRY(grid_of(fwd_small_kernel, KKT_WPB * 32, h->tsmall_smem, us, KKT_WPB, &h->g_tsmall));
   CUDA_TRY(grid_of(fwd_big_kernel, KKT_BNT, h->tbig_smem,
