@@ -840,14 +840,10 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
       S.n_fwd = (int)fsorted.size();
       S.bwd_order = (const int2*)((char*)h->sb_mem2 + b5);
       S.n_bwd = (int)bord.size();
-      S.smem_doubles = std::max({H.max_smem, h->dp.max_rw_small + P.max_r_small + 2, P.max_front + 8 * 32 + 2});
+      S.smem_doubles = std::max({H.max_smem, h->dp.max_rw_small + P.max_r_small + 2, P.max_front + 8 * 32 + 32 * 33 + 2});
       h->sb_smem = S.smem_doubles * 8;
-      // every big supernode of the tree needs its L11^-1: the blocked substitution's registers
-      // would cost the small phase its occupancy, so such plans keep the per-node kernels
-      bool blk = !h->use_linv;
-      for (int s_ = 0; s_ < P.ns; s_++)
-        if (P.sn[s_].big && (!P.sn[s_].huge || vcta) && P.sn_Lip[s_] < 0) blk = true;
-      if (blk) h->sblock = false;
+      // supernodes without L11^-1 (the CTA view of the large fronts, or KKT_NO_LINV) take the
+      // register-light blocked sweeps (sblock.cuh cta_fwd_lite / cta_bwd_lite)
       auto fk = h->sb_nt == 128 ? tree_fwd_kernel<false, 128> : tree_fwd_kernel<false, 256>;
       auto bk = h->sb_nt == 128 ? tree_bwd_kernel<false, 128> : tree_bwd_kernel<false, 256>;
       CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sb_smem));

@@ -184,6 +184,106 @@ __device__ __forceinline__ void fwd_single_warp(const DevPlan& P, const SnInfo& 
   if (lane == 0) trace_stamp(P, 1, s, b, 1);
 }
 
+// Blocked sweeps of a supernode without L11^-1 inside the tree kernels (the CTA view of the
+// large fronts), with the arithmetic of cta_fwd_blocked / cta_bwd_blocked but few registers: the
+// 32 x 32 diagonal block is staged in shared memory (Ds, pitch 33) instead of registers, the rows
+// below take their 32 column values 8 at a time, and the backward partial sums run 8 columns at
+// a time (per column the same per-thread order and the same butterfly).  Ds: >= 32 * 33 doubles,
+// part: >= 8 * 32 doubles.
+template <int NT>
+__device__ __forceinline__ void cta_fwd_lite(const double* __restrict__ L, int r, int w, const double* __restrict__ dv,
+                                             double* v, double* Ds, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int c0 = 0; c0 < w; c0 += 32) {
+    const int kb = min(32, w - c0);
+    for (int q = tid; q < 32 * 32; q += NT) {  // diagonal block, column-major, pitch 33
+      const int k = q >> 5, i = q & 31;
+      Ds[k * 33 + i] = (i < kb && k < kb && k < i) ? __ldg(L + (long long)(c0 + k) * r + c0 + i) : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int row = c0 + lane;
+      double x = (lane < kb) ? v[row] : 0.0;
+      const double di = (lane < kb) ? __ldg(dv + row) : 0.0;
+      for (int k = 0; k < kb; k++) {
+        const double yk = __shfl_sync(0xffffffffu, x * di, k);
+        if (lane == k) x = yk;
+        else if (lane > k) x = fma(-Ds[k * 33 + lane], yk, x);
+      }
+      if (lane < kb) v[row] = x;
+    }
+    __syncthreads();
+    for (int i = c0 + kb + tid; i < r; i += NT) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int cb = 0; cb < 32; cb += 8) {
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) l[u] = (cb + u < kb) ? __ldg(L + (long long)(c0 + cb + u) * r + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          a0 = fma(l[u], (cb + u < kb) ? v[c0 + cb + u] : 0.0, a0);
+          a1 = fma(l[u + 1], (cb + u + 1 < kb) ? v[c0 + cb + u + 1] : 0.0, a1);
+        }
+      }
+      v[i] -= a0 + a1;
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void cta_bwd_lite(const double* __restrict__ L, int r, int w, const double* __restrict__ dv,
+                                             double* xa, double* Ds, double* part, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = NT / 32;
+  for (int c0 = ((w - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
+    const int kb = min(32, w - c0);
+    for (int q = tid; q < 32 * 32; q += NT) {  // diagonal block, column-major, pitch 33
+      const int k = q >> 5, i = q & 31;
+      Ds[k * 33 + i] = (i < kb && k < kb && k < i) ? __ldg(L + (long long)(c0 + k) * r + c0 + i) : 0.0;
+    }
+    double tot = 0.0;  // lane c (warp 0): sum of the warp partials of column c0 + c
+    for (int g = 0; g < 32; g += 8) {
+      double p[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) p[c] = 0.0;
+      for (int i = c0 + kb + tid; i < r; i += NT) {
+        const double xi = xa[i];
+#pragma unroll
+        for (int c = 0; c < 8; c++) p[c] = fma((g + c < kb) ? __ldg(L + (long long)(c0 + g + c) * r + i) : 0.0, xi, p[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) p[c] += __shfl_xor_sync(0xffffffffu, p[c], o);
+      }
+      if (lane < 8) {
+        double pv = p[0];
+#pragma unroll
+        for (int c = 1; c < 8; c++) pv = (lane == c) ? p[c] : pv;
+        part[warp * 32 + g + lane] = pv;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double a = (lane < kb) ? xa[c0 + lane] : 0.0;
+      const double di = (lane < kb) ? __ldg(dv + c0 + lane) : 0.0;
+      for (int q = 0; q < nw; q++) a -= part[q * 32 + lane];
+      (void)tot;
+      for (int k = 31; k >= 0; k--) {
+        if (k < kb) {
+          const double xk = __shfl_sync(0xffffffffu, a * di, k);
+          if (lane == k) a = xk;
+          else if (lane < k) a = fma(-Ds[lane * 33 + k], xk, a);
+        }
+      }
+      if (lane < kb) xa[c0 + lane] = a;
+    }
+    __syncthreads();
+  }
+}
+
 // Forward of one big supernode by the CTA (the per-node code of fwd_big_kernel): gather
 // v = [b(cols); 0] + children's u (fixed order), L11^-1 / blocked sweep, y -> Y, u -> uv.
 // v: [max_front] shared, tmp: [>= w] shared.
@@ -242,8 +342,9 @@ __device__ __forceinline__ void fwd_big_cta(const DevPlan& P, const SnInfo& I, i
     }
   }
   const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
-  if (!BLK || lip >= 0) cta_fwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, v, tmp, tid, nt);
-  else cta_fwd_blocked(L, r, w, Dv + I.f0, v, tid, nt);
+  if (lip >= 0) cta_fwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, v, tmp, tid, nt);
+  else if (BLK) cta_fwd_blocked(L, r, w, Dv + I.f0, v, tid, nt);
+  else cta_fwd_lite<NT>(L, r, w, Dv + I.f0, v, tmp, tid);
   for (int q = tid; q < w; q += nt) Y[I.f0 + q] = v[q];
   if (I.par >= 0)
     for (int q = tid; q < R; q += nt) uv[I.uvp + q] = v[w + q];
@@ -388,8 +489,9 @@ __device__ __forceinline__ void bwd_big_cta(const DevPlan& P, const SnInfo& I, i
   for (int q = tid; q < r; q += nt) xa[q] = (q < w) ? ldcg(Y + I.f0 + q) : ldcg(Xp + __ldg(P.sn_rows + I.rp0 + q));
   __syncthreads();
   const long long lip = Li_all ? __ldg(P.sn_Lip + s) : -1;
-  if (!BLK || lip >= 0) cta_bwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, xa, part, tid, nt);
-  else cta_bwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part, tid, nt);
+  if (lip >= 0) cta_bwd_inv(L, Li_all + (long long)b * P.linv_doubles + lip, r, w, xa, part, tid, nt);
+  else if (BLK) cta_bwd_blocked(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part, tid, nt);
+  else cta_bwd_lite<NT>(L, r, w, Dv_all + (long long)b * P.n + I.f0, xa, part + 8 * 32, part, tid);
   double* xo = xout + (long long)b * xs;
   for (int q = tid; q < w; q += nt) {
     Xp[I.f0 + q] = xa[q];

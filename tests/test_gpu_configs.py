@@ -442,7 +442,7 @@ def test_warp_residual_variant(monkeypatch):
 SBLOCK_CASES = [("C2", {}), ("C2", {"KKT_SB_CAP": "1024", "KKT_FB_CAP": "2048"}), ("C1", {}), ("C5b8", {}),
                 ("C2", {"KKT_SB_NT": "128"}), ("C5b8", {"KKT_SB_NT": "128", "KKT_SB_CAP": "2048"}),
                 ("C5b8", {"KKT_SB_CAP": "1500", "KKT_FB_CAP": "3000"}), ("C2s", {"KKT_NO_PDL": "1"}),
-                ("C3L", {})]
+                ("C3L", {}), ("C3L", {"KKT_HUGE_SOLVE": "0"})]
 
 
 @pytest.mark.parametrize("switch", ["KKT_SBLOCK", "KKT_FBLOCK"])
@@ -457,7 +457,8 @@ def test_subtree_block_kernels_bitwise(case, env, switch, monkeypatch):
     from kkt_gpu import run_lifted, relerr
     if case == "C5b8":
         inst = make_config("C5", batch=8)
-    elif case == "C3L":  # the C3 pattern as LiftedKKT: huge fronts solved by the tile path
+    elif case == "C3L":  # the C3 pattern as LiftedKKT: large fronts by the tile solve or (KKT_HUGE_SOLVE=0)
+        # as CTA supernodes of the tree kernels without L11^-1 (cta_fwd_lite / cta_bwd_lite)
         inst = acopf(10000, 3000, name="acopf10000-lifted")
     else:
         inst = make_config(case)
