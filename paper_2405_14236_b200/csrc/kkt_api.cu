@@ -776,7 +776,8 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
     // the small phase is throughput-bound (>= 50k small supernode tasks: C4, C5, C6; measured)
     h->sb_nt = ((long long)P.order_s.size() * P.batch >= 50000) ? 128 : 256;
     if (const char* e = getenv("KKT_SB_NT")) h->sb_nt = atoi(e) == 128 ? 128 : 256;
-    const int cap = getenv("KKT_SB_CAP") ? std::max(1024, atoi(getenv("KKT_SB_CAP"))) : (h->sb_nt == 128 ? 4096 : 6144);
+    // measured: 256-thread trees (C1-C3) best at 12288-double blocks, 128-thread ones at 4096
+    const int cap = getenv("KKT_SB_CAP") ? std::max(1024, atoi(getenv("KKT_SB_CAP"))) : (h->sb_nt == 128 ? 4096 : 12288);
     SBlockHost H;
     build_sblocks(P, cap, h->sb_nt / 32, H);
     if (H.blk.empty()) {
