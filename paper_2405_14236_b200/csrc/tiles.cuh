@@ -463,6 +463,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // factors the top-left block while warps 4-7 update the bottom-right one (the top-right block is
 // above the diagonal: never read).  Same products and factorisation as tile_gemm_nt_smem +
 // tile_potrf64.
+template <bool FOLLOW = true>
 __device__ __forceinline__ void tile_syrk_potrf64(double* A2, const double* A1, int kb, double* dinv, double* sinv,
                                                   double* L11s, int* fail_k) {
   __shared__ int s_col;  // columns of the top-left factor published to the row-solve follower
@@ -472,8 +473,8 @@ __device__ __forceinline__ void tile_syrk_potrf64(double* A2, const double* A1, 
   if (A1) tile_syrk_strip(A2, A1, warp < 4 ? 8 * warp : 32 + 8 * (warp - 4), 0);
   __syncthreads();  // top-left and bottom-left blocks updated
   if (warp == 0) {
-    tile_diag32<0, true>(A2, kb0, lane, dinv, sinv, L11s, fail_k, &s_col);
-  } else if (warp == 1 && kb1 > 0) {
+    tile_diag32<0, FOLLOW>(A2, kb0, lane, dinv, sinv, L11s, fail_k, &s_col);
+  } else if (FOLLOW && warp == 1 && kb1 > 0) {
     // L21 = A21 L11^-T for rows 32..63, one column behind warp 0 (tile_rowsolve32's arithmetic,
     // L11 read from the published columns)
     const int row = 32 + lane;
@@ -496,6 +497,10 @@ __device__ __forceinline__ void tile_syrk_potrf64(double* A2, const double* A1, 
   }
   __syncthreads();
   if (kb1 > 0) {
+    if (!FOLLOW) {
+      tile_rowsolve32<0>(A2, 32, 32, A2, sinv);
+      __syncthreads();
+    }
     tile_block_update(A2, 32, 32, A2, 0, 32);
     __syncthreads();
     if (warp == 0) tile_diag32<32>(A2, kb1, lane, dinv, sinv, L11s, fail_k);

@@ -43,6 +43,27 @@ __global__ void __launch_bounds__(256, 1) bench(int which, int reps, double* g, 
       __syncthreads();
       if (threadIdx.x == 0) __threadfence();
       __syncthreads();
+    } else if (which == 10 || which == 11) {   // syrk+potrf: 10 = separate (gemm_smem + potrf64), 11 = fused, no follower
+      tile_load_async(sm + 2 * TBD, gt); cp_async_wait_all(); __syncthreads();
+      if (which == 10) { tile_gemm_nt_smem(sm + 2 * TBD, sm + TBD, sm + TBD); tile_potrf64(sm + 2 * TBD, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf); }
+      else tile_syrk_potrf64<false>(sm + 2 * TBD, sm + TBD, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+    } else if (which == 12) {  // fused with the follower
+      tile_load_async(sm + 2 * TBD, gt); cp_async_wait_all(); __syncthreads();
+      tile_syrk_potrf64<true>(sm + 2 * TBD, sm + TBD, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+    } else if (which == 9) {   // current CRIT body: trsm + store + fence + fused syrk/potrf + store + fence
+      tile_load_async(sm, gt + TBD); tile_load_async(sm + TBD, gt + 2 * TBD); tile_load_async(sm + 2 * TBD, gt); cp_async_wait_all(); __syncthreads();
+      long long c0 = clock64();
+      tile_trsm64(sm + TBD, sm, sm + 3 * TBD);
+      __syncthreads(); long long c1 = clock64();
+      tile_store(gt + 3 * TBD, sm + TBD);
+      __syncthreads(); if (threadIdx.x == 0) __threadfence(); __syncthreads();
+      long long c2 = clock64();
+      tile_syrk_potrf64(sm + 2 * TBD, sm + TBD, 64, dinv + blockIdx.x * 64, sm + 3 * TBD, sm + 3 * TBD + 64, &sf);
+      long long c3 = clock64();
+      tile_store(gt + 3 * TBD, sm + 2 * TBD);
+      __syncthreads(); if (threadIdx.x == 0) __threadfence(); __syncthreads();
+      long long c4 = clock64();
+      if (threadIdx.x == 0 && blockIdx.x == 0 && r == reps - 1) printf("crit parts: trsm %lld store+fence %lld syrk+potrf %lld store+fence %lld\n", c1 - c0, c2 - c1, c3 - c2, c4 - c3);
     } else if (which == 8) {   // the whole CRIT body without waits
       tile_load_async(sm, gt + TBD); tile_load_async(sm + TBD, gt + 2 * TBD); tile_load_async(sm + 2 * TBD, gt); cp_async_wait_all(); __syncthreads();
       tile_trsm64(sm + TBD, sm, sm + 3 * TBD);
@@ -79,8 +100,8 @@ int main() {
   cudaMemcpy(g, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_BYTES);
   const char* names[] = {"potrf64", "trsm64", "gemm_global", "load2tiles", "diag32", "rowsolve32x64", "gemm_smem",
-                         "store+panel+fence", "crit_body"};
-  for (int w = 0; w < 9; w++) {
+                         "store+panel+fence", "crit_body", "crit_now", "syrk_potrf_sep", "syrk_potrf_fused", "syrk_potrf_follow"};
+  for (int w = 0; w < 13; w++) {
     for (int grid : {1, 148, 296}) {
       bench<<<grid, 256, TILE_SMEM_BYTES>>>(w, 20, g, dinv, out);
       cudaError_t e = cudaDeviceSynchronize();
