@@ -476,3 +476,23 @@ def test_subtree_block_kernels_bitwise(case, env, switch, monkeypatch):
     if case in ("C2", "C1"):
         R = oracle.reference_solve(inst)
         assert relerr(x, R["x"]) <= 1e-8
+
+
+@pytest.mark.parametrize("env", [{"KKT_TS_CHAIN": "0"}, {"KKT_TS_CHAIN": "1", "KKT_TS_WAVE": "1"},
+                                 {"KKT_TS_CHAIN": "1", "KKT_TS_WAVE": "4"}])
+def test_tile_solve_chain_variants(env, monkeypatch):
+    """Tile solve of the large fronts: per-step chain tasks (FC / BC) and the panel chain tasks
+    (FCH / BCH: TMA tile ring, two warps per tile, waves of 1 or 4 tiles) against the oracle on a
+    pattern with large fronts (forced into the tile path with KKT_HUGE_SOLVE=1)."""
+    from kkt_gpu import run_lifted, relerr
+    monkeypatch.setenv("KKT_HUGE_SOLVE", "1")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inst = acopf(10000, 3000, name="acopf10000-lifted")
+    R = oracle.reference_solve(inst)
+    x, info, S = run_lifted(inst, max_refine=10)
+    S.close()
+    assert info["status"] == 0, info
+    assert relerr(x, R["x"]) <= 1e-8, relerr(x, R["x"])
+    eta, _ = oracle.backward_error(inst, R["K"], inst.b, x)
+    assert eta <= 1e-10
