@@ -245,19 +245,27 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------------------ ours
-def algorithmic_work(info, inst, refine_iters):
-    """SURVEY §8(d) algorithmic work per instance."""
+def algorithmic_work(info, inst, refine_iters, cg_iters=0):
+    """SURVEY §8(d) algorithmic work per instance.  HyKKT (m_eq > 0): every pass
+    runs cg_iters + 2 trsv pairs (z = K_gamma^-1 s, one per CG iteration, the final dx); the
+    G / G^T products are not counted (a lower bound); refine_iters = outer passes after the first,
+    each preceded by one dd residual.  cg_iters is the first pass's count, used for every pass."""
     n, m, nnzW, nnzJ = inst.n, inst.m, inst.nnzW, inst.nnzJ
     nnzK, nnzL = int(info["nnzK"]), int(info["nnzL"])
     condense_bytes = 8 * (nnzW + nnzJ + n + m) + 8 * nnzK
     trsv_bytes = 16 * nnzL + 24 * n
     resid_bytes = 24 * nnzW + 24 * nnzJ + 8 * (2 * n + m)
-    pairs = 1 + refine_iters
-    solve_bytes = pairs * trsv_bytes + (refine_iters + 1) * resid_bytes
+    if inst.m_eq > 0:
+        pairs = (1 + refine_iters) * (cg_iters + 2)
+        resid_passes = refine_iters
+    else:
+        pairs = 1 + refine_iters
+        resid_passes = refine_iters + 1
+    solve_bytes = pairs * trsv_bytes + resid_passes * resid_bytes
     return dict(condense_bytes=condense_bytes, factor_flops=float(info["flops"]),
                 factor_flops_large=float(info["flops_huge"]),
                 trsv_bytes=trsv_bytes, resid_bytes=resid_bytes, solve_bytes=solve_bytes,
-                trsv_pairs=pairs)
+                trsv_pairs=pairs, resid_passes=resid_passes)
 
 
 def run_ours(args, rank, world):
@@ -395,7 +403,7 @@ def run_ours(args, rank, world):
         d2h = 8 * B * inst.n
     # ---------------- roofline ----------------
     ph_mean = ph.mean(0)
-    work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0))
+    work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0), max(info["cg_iters"], 0))
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     pk = json.load(open(pk_path)) if os.path.exists(pk_path) else {}
     fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
@@ -429,7 +437,9 @@ def run_ours(args, rank, world):
                       "peak": hbm_peak, "unit": "GB/s", "traffic": None,
                       "kernel": ("hykkt_solve" if hykkt else "kkt_solve") + " (fwd/bwd trsv kernels + dd residual)",
                       "work": f"B x [{work['trsv_pairs']} trsv pairs x (16 nnz(L) + 24 n) + "
-                              f"{work['trsv_pairs']} dd residual passes] bytes",
+                              f"{work['resid_passes']} dd residual passes] bytes"
+                              + (" (HyKKT: (cg_iters + 2) pairs per pass; G, G^T products not counted)"
+                                 if hykkt else ""),
                       "peak_note": hbm_note}
     for r_ in roofs.values():
         r_["frac"] = r_["achieved"] / r_["peak"]

@@ -230,7 +230,7 @@ kkt_status kkt_factor_inertia_correct(kkt_handle h, const double *W_vals, const 
 /* Block the host until the handle's stream is idle; report and clear the device status.
  * Any out pointer may be NULL.  status: a kkt_status value; fail_col: original column of
  * the first non-SPD pivot or -1; refine_iters: sweeps run by the last solve (max over the
- * batch); cg_iters: CG iterations of the first HyKKT pass (max over the batch); bwd_err:
+ * batch; after hykkt_solve: the outer correction passes run after the first); cg_iters: CG iterations of the first HyKKT pass (max over the batch); bwd_err:
  * componentwise backward error omega after the last solve (max over the batch). */
 kkt_status kkt_sync_info(kkt_handle h, int *status, int *fail_col, int *refine_iters,
                          int *cg_iters, double *bwd_err);

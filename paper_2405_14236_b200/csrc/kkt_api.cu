@@ -91,6 +91,7 @@ struct kkt_plan {
   int hy_maxit = -1, hy_outer = -1, hy_krylov = -1;
   long long hy_fixed = 0, hy_body = 0;   // launches outside / per execution of the Krylov body
   bool hy_pending = false;               // last call was a HyKKT graph (launch count unread)
+  bool last_hykkt = false;               // last solve was HyKKT: kkt_sync_info reports outer passes
   const void *hy_W = nullptr, *hy_J = nullptr, *hy_Sx = nullptr;
   TaskQueue TQ{}, TQs{};  // work queues of bwd_big / bwd_small (separate: the two may overlap)
   double* Li = nullptr;   // [batch][linv_doubles] L11^-1 of the big (CTA) supernodes (solve operator)
@@ -1041,6 +1042,7 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
   h->launches = 0;
   h->graph_solve_pending = false;
   h->hy_pending = false;
+  h->last_hykkt = false;
   if (P.m > 0) {
     dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
@@ -1447,6 +1449,7 @@ extern "C" kkt_status kkt_solve(kkt_handle h, const double* b, double* x, int ma
   h->launches = 0;
   h->graph_solve_pending = false;
   h->hy_pending = false;
+  h->last_hykkt = false;
   if (!h->use_graph) return enqueue_solve(h, b, x, max_refine, tol_bwd);
   // one CUDA graph per (max_refine, tol, value pointers, delta_w), recorded on a private stream
   const bool stale = !h->solve_exec || h->g_max_refine != max_refine || h->g_tol != tol_bwd ||
@@ -1671,6 +1674,7 @@ extern "C" kkt_status hykkt_solve_krylov(kkt_handle h, const double* rbar1, cons
   h->launches = 0;
   h->graph_solve_pending = false;
   h->hy_pending = false;
+  h->last_hykkt = false;
   if (P.m_eq == 0) return kkt_solve(h, rbar1, dx, max_outer_refine, 0.0);
   const bool stale = !h->hy_exec || h->hy_rtol != cg_rtol || h->hy_maxit != cg_maxit ||
                      h->hy_outer != max_outer_refine || h->hy_krylov != krylov || h->hy_W != h->Wv ||
@@ -1693,6 +1697,7 @@ extern "C" kkt_status hykkt_solve_krylov(kkt_handle h, const double* rbar1, cons
   CUDA_TRY(cudaMemcpyAsync(dy, h->g_dy, mb, cudaMemcpyDeviceToDevice, h->stream));
   h->launches = h->hy_fixed;
   h->hy_pending = true;
+  h->last_hykkt = true;
   return KKT_OK;
 }
 
@@ -1761,6 +1766,7 @@ extern "C" kkt_status kkt_solve_unreduced(kkt_handle h, const double* x, const d
   h->launches = launches + 1;
   h->graph_solve_pending = false;
   h->hy_pending = false;
+  h->last_hykkt = false;
   return KKT_OK;
 }
 
@@ -1779,7 +1785,8 @@ extern "C" kkt_status kkt_sync_info(kkt_handle h, int* status, int* fail_col, in
   std::vector<double> om(P.batch);
   CUDA_TRY(cudaMemcpyAsync(&st, h->status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaMemcpyAsync(&fl, h->fail, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaMemcpyAsync(it.data(), h->C.refine_iters, P.batch * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(it.data(), h->last_hykkt ? h->C.opass : h->C.refine_iters, P.batch * sizeof(int),
+                           cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaMemcpyAsync(cg.data(), h->C.cg_iters_first, P.batch * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaMemcpyAsync(om.data(), h->C.omega_last, P.batch * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
