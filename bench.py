@@ -377,11 +377,29 @@ def run_ours(args, rank, world):
     pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
     e2e_ms = None
     h2d = d2h = 0
-    if not hykkt:
-        hW, hJ, hSx, hSs, hb = (pin(v0.W_vals), pin(v0.J_vals), pin(v0.Sigma_x), pin(v0.Sigma_s), pin(v0.b))
+    if True:
+        hW, hJ, hSx, hSs = (pin(v0.W_vals), pin(v0.J_vals), pin(v0.Sigma_x), pin(v0.Sigma_s))
         hx = torch.zeros(tuple(x.shape), dtype=torch.float64).pin_memory()
-        call = lambda: K.kkt_step_host(S.h, hW, hJ, hSx, hSs, None, inst.delta_w, inst.delta_c,
-                                       inst.gamma, hb, hx, args.max_refine, 0.0)
+        if not hykkt:
+            hb = pin(v0.b)
+            call = lambda: K.kkt_step_host(S.h, hW, hJ, hSx, hSs, None, inst.delta_w, inst.delta_c,
+                                           inst.gamma, hb, hx, args.max_refine, 0.0)
+        else:
+            # HyKKT has no host-buffer entry point: the public calls on device buffers, with the
+            # pinned-host copies of the step's inputs and of (dx, dy) on the handle's stream
+            hr1, hr2 = pin(v0.rbar1), pin(v0.rbar2)
+            hdy = torch.zeros(tuple(dy.shape), dtype=torch.float64).pin_memory()
+            dev_in = [torch.empty_like(t_, device=dev) for t_ in (hW, hJ, hSx, hSs, hr1, hr2)]
+
+            def call():
+                for dd_, hh_ in zip(dev_in, (hW, hJ, hSx, hSs, hr1, hr2)):
+                    dd_.copy_(hh_, non_blocking=True)
+                S.condense(dev_in[0], dev_in[1], dev_in[2], dev_in[3], None, inst.delta_w, inst.delta_c,
+                           inst.gamma)
+                S.factor()
+                S.hykkt_solve(dev_in[4], dev_in[5], x, dy, 1e-12, 0, 2)
+                hx.copy_(x, non_blocking=True)
+                hdy.copy_(dy, non_blocking=True)
         for _ in range(2):
             call()
         e0, e1 = ev(), ev()
@@ -399,8 +417,12 @@ def run_ours(args, rank, world):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
         e2e_ms = e2e_tot / args.steps
-        h2d = 8 * B * (inst.nnzW + inst.nnzJ + inst.n + (inst.m - inst.m_eq) + inst.n)
-        d2h = 8 * B * inst.n
+        if not hykkt:
+            h2d = 8 * B * (inst.nnzW + inst.nnzJ + inst.n + (inst.m - inst.m_eq) + inst.n)
+            d2h = 8 * B * inst.n
+        else:
+            h2d = sum(8 * t_.numel() for t_ in (hW, hJ, hSx, hSs, hr1, hr2))
+            d2h = 8 * (hx.numel() + hdy.numel())
     # ---------------- roofline ----------------
     ph_mean = ph.mean(0)
     work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0), max(info["cg_iters"], 0))
