@@ -412,8 +412,7 @@ __global__ void __launch_bounds__(NT, BLK ? 1 : sb_minb<NT>()) tree_fwd_kernel(D
     }
     // continuation up the tree
     for (;;) {
-      __threadfence();
-      __syncthreads();  // every thread's u entries are written before the arrival
+      __syncthreads();  // every thread's u entries are written before the arrival (acq_rel atomic: cumulative)
       if (tid == 0) {
         int nx = -1;
         if (I.par >= 0) {
@@ -623,14 +622,13 @@ __global__ void __launch_bounds__(NT, BLK ? 1 : sb_minb<NT>()) tree_bwd_kernel(D
     __syncthreads();  // every thread reads the ancestors' x only after thread 0's acquire
     if (I.big) {
       bwd_big_cta<BLK, NT>(P, I, s, b, Lx_all, Dv_all, Y_all, Xp_all, xout, xs, Li_all, sm, sm + P.max_front, tid);
-      __threadfence();
       __syncthreads();
-      if (tid == 0) st_release(flags + s, epoch);
+      if (tid == 0) st_release(flags + s, epoch);   // release: cumulative over the barrier
     } else if (bi < 0) {  // single small supernode: warp 0
       if (warp == 0) {
         bwd_node_warp(P, I, s, b, Lx_all, Dv_all, Y_all, Xp_all, xout, xs, sm, sm + P.max_rw_small, lane);
         __syncwarp();  // lanes' x writes are ordered before lane 0's release
-        if (lane == 0) { __threadfence(); st_release(flags + s, epoch); }
+        if (lane == 0) st_release(flags + s, epoch);
       }
     } else {
       const SBlk K = B.blk[bi];

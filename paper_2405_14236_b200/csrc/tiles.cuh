@@ -26,6 +26,9 @@
 // deadlock-free.  Final L tiles are also written to the supernodal panel layout (r x w,
 // column-major) that the triangular solves read.
 #pragma once
+#ifndef TILE_SLEEP
+#define TILE_SLEEP 32   // spin back-off (ns) of the dependency waits
+#endif
 #include "dense.cuh"
 #include "ldlt.cuh"
 
@@ -107,7 +110,7 @@ __device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double
 
 __device__ __forceinline__ void wait_cnt(const int* c, int target) {
   if (threadIdx.x == 0) {
-    while (ld_volatile(c) < target) { __nanosleep(32); }
+    while (ld_volatile(c) < target) { __nanosleep(TILE_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
@@ -115,7 +118,7 @@ __device__ __forceinline__ void wait_cnt(const int* c, int target) {
 // publish: every thread's global writes -> barrier -> one gpu-scope release by thread 0
 __device__ __forceinline__ void publish_cnt(int* c, int value) {
   __syncthreads();
-  if (threadIdx.x == 0) { __threadfence(); st_release(c, value); }
+  if (threadIdx.x == 0) st_release(c, value);   // release: cumulative over the barrier
 }
 
 // Final panel tile (i, k) -> supernodal panel layout Lx (r x w column-major); diagonal tiles

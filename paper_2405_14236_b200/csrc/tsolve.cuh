@@ -24,6 +24,9 @@
 // the list-schedule order (tile_plan.cpp), all workers resident: deadlock-free.  Every sum has a
 // fixed order (no floating-point atomics): deterministic, bitwise identical run to run.
 #pragma once
+#ifndef TS_SLEEP
+#define TS_SLEEP 32   // spin back-off (ns) of the dependency waits
+#endif
 #include "tiles.cuh"
 
 namespace kkt {
@@ -97,18 +100,18 @@ __device__ __forceinline__ double* ts_qslot(const TSCtx& X, const TFront& F, int
 
 __device__ __forceinline__ void ts_wait(const int* c, int target) {
   if (threadIdx.x == 0) {
-    while (ld_volatile(c) < target) { __nanosleep(32); }
+    while (ld_volatile(c) < target) { __nanosleep(TS_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
 }
 __device__ __forceinline__ void ts_publish(int* c, int v) {
   __syncthreads();
-  if (threadIdx.x == 0) { __threadfence(); st_release(c, v); }
+  if (threadIdx.x == 0) st_release(c, v);   // release: cumulative over the barrier
 }
 __device__ __forceinline__ void ts_publish_add(int* c) {
   __syncthreads();
-  if (threadIdx.x == 0) { __threadfence(); red_release_add(c, 1); }
+  if (threadIdx.x == 0) red_release_add(c, 1);
 }
 
 // r (64, shared) -= A (swizzled tile) x (64, shared): 4 threads per row, 16 columns each
@@ -204,10 +207,95 @@ __device__ __forceinline__ const double* ts_tile(const TSCtx& X, const TFront& F
 // FG(f, t): gather of row block t (children in fixed order) -> the block's working vector; gf = 1.
 // A huge child's update entries are finalised here: u_e = v_e - sum_k P_child[t_c][k] (k ascending)
 // once the child's blocks t_c covering them have all their partial products (no separate task).
+// Latency: everything that does not depend on the huge children's flags -- the right-hand side
+// through perm, every child's record, cut and row map, the final u entries of non-huge children
+// -- is loaded before the wait, one warp per child, into a per-child table in shared memory
+// (child q's entries land on distinct rows); after the wait only the huge children's u entries
+// and partials remain, then the table is summed into the block child by child (q ascending:
+// the same order and operations as the per-child loop, bitwise the same result).
+constexpr int TS_GMAX = 160;   // children staged per gather (more: per-child loop)
 __device__ void ts_gather(const TSCtx& X, const TFront& F, int f, int t, double* sv) {
   const DevPlan& P = *X.P;
   const SnInfo I = P.sn[F.s];
   const int r0 = trow0(F, t), nr = tsize(F, t);
+  const int nch = F.nch;
+  if (nch <= TS_GMAX) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* cval = sv + 64;                                           // [nch][64]
+    int* crow = reinterpret_cast<int*>(cval + (long long)nch * 64);   // [nch][64] target row or -1
+    int4* cmeta = reinterpret_cast<int4*>(crow + nch * 64);           // [nch] {hc, a, b, uvp}
+    __syncthreads();  // the previous task's shared-memory reads are done
+    if (threadIdx.x < TBS)
+      sv[threadIdx.x] = (t < F.nbp && threadIdx.x < nr) ? __ldg(X.rhs + __ldg(P.perm + I.f0 + r0 + threadIdx.x)) : 0.0;
+    for (int q = warp; q < nch; q += TILE_THREADS / 32) {
+      const int2 cr = X.T->tch[F.ch0 + q];
+      const int* cut = X.T->tcut + cr.y;
+      const int a = __ldg(cut + t), b = __ldg(cut + t + 1);
+      const int hc = __ldg(X.T->hidx + cr.x);
+      int uvp = 0;
+      if (b > a) {
+        const SnInfo C = P.sn[cr.x];
+        uvp = C.uvp;
+        const int* rel = P.sn_rel + C.rp0 + C.w;
+        const double* u = X.uvb + C.uvp;
+        for (int e0 = 0; e0 < b - a; e0 += 32) {
+          const int e = a + e0 + lane;
+          if (e < b) {
+            crow[q * 64 + e0 + lane] = __ldg(rel + e) - r0;
+            if (hc < 0) cval[q * 64 + e0 + lane] = __ldcg(u + e);
+          }
+        }
+      }
+      if (lane == 0) cmeta[q] = make_int4(hc, a, b, uvp);
+    }
+    if (threadIdx.x < nch) {  // huge children: the blocks feeding this one must be complete
+      const int2 cr = X.T->tch[F.ch0 + threadIdx.x];
+      const int hc = __ldg(X.T->hidx + cr.x);
+      const int* cut = X.T->tcut + cr.y;
+      const int a = __ldg(cut + t), b = __ldg(cut + t + 1);
+      if (hc >= 0 && b > a) {
+        const TFront C = X.T->fr[hc];
+        for (int tc = C.nbp + (a >> 6); tc <= C.nbp + ((b - 1) >> 6); tc++) {
+          const int* g = ts_gf(*X.S, X.cnt, C, hc, tc);
+          const int* pc = ts_pc(*X.S, X.cnt, C, hc, tc);
+          while (ld_volatile(g) < 1) { __nanosleep(TS_SLEEP); }
+          while (ld_volatile(pc) < C.nbp) { __nanosleep(TS_SLEEP); }
+        }
+        fence_acq_rel();
+      }
+    }
+    __syncthreads();
+    ts_ready(X);
+    for (int q = warp; q < nch; q += TILE_THREADS / 32) {
+      const int4 m = cmeta[q];
+      if (m.x < 0 || m.z <= m.y) continue;
+      const TFront Cf = X.T->fr[m.x];
+      const double* u = X.uvb + m.w;
+      for (int e0 = 0; e0 < m.z - m.y; e0 += 32) {
+        const int e = m.y + e0 + lane;
+        if (e < m.z) {
+          double val = __ldcg(u + e);
+          const double* p0 = X.part + X.S->pbase[m.x] + ((long long)(Cf.nbp + (e >> 6)) * Cf.nbp) * TBS + (e & 63);
+#pragma unroll 8
+          for (int k = 0; k < Cf.nbp; k++) val -= __ldcg(p0 + (long long)k * TBS);
+          cval[q * 64 + e0 + lane] = val;
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // child by child, q ascending
+      for (int q = 0; q < nch; q++) {
+        const int4 m = cmeta[q];
+        for (int e = lane; e < m.z - m.y; e += 32) sv[crow[q * 64 + e]] += cval[q * 64 + e];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    double* v = ts_vec(F, I, X.Y, X.uvb, t);
+    if (threadIdx.x < nr) v[threadIdx.x] = sv[threadIdx.x];
+    ts_publish(ts_gf(*X.S, X.cnt, F, f, t), 1);
+    return;
+  }
   if (threadIdx.x < F.nch) {  // huge children: the blocks feeding this one must be complete
     const int2 cr = X.T->tch[F.ch0 + threadIdx.x];
     const int hc = __ldg(X.T->hidx + cr.x);
@@ -218,8 +306,8 @@ __device__ void ts_gather(const TSCtx& X, const TFront& F, int f, int t, double*
       for (int tc = C.nbp + (a >> 6); tc <= C.nbp + ((b - 1) >> 6); tc++) {
         const int* g = ts_gf(*X.S, X.cnt, C, hc, tc);
         const int* pc = ts_pc(*X.S, X.cnt, C, hc, tc);
-        while (ld_volatile(g) < 1) { __nanosleep(32); }
-        while (ld_volatile(pc) < C.nbp) { __nanosleep(32); }
+        while (ld_volatile(g) < 1) { __nanosleep(TS_SLEEP); }
+        while (ld_volatile(pc) < C.nbp) { __nanosleep(TS_SLEEP); }
       }
       fence_acq_rel();
     }
@@ -298,7 +386,7 @@ __device__ void ts_fchain(const TSCtx& X, const TFront& F, int f, int k, double*
   if (threadIdx.x == 0) {  // the block's gather and its k partial products, one wait
     const int* g = ts_gf(*X.S, X.cnt, F, f, k);
     const int* pc = ts_pc(*X.S, X.cnt, F, f, k);
-    while (ld_volatile(g) < 1 || ld_volatile(pc) < k) { __nanosleep(32); }
+    while (ld_volatile(g) < 1 || ld_volatile(pc) < k) { __nanosleep(TS_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
@@ -325,9 +413,9 @@ __device__ void ts_fchain(const TSCtx& X, const TFront& F, int f, int k, double*
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(ts_yf(*X.S, X.cnt, F, f, k), 1);
-    if (k + 1 < F.nt) red_release_add(ts_pc(*X.S, X.cnt, F, f, k + 1), 1);
+    fence_acq_rel();   // one release fence for both flags
+    st_relaxed(ts_yf(*X.S, X.cnt, F, f, k), 1);
+    if (k + 1 < F.nt) red_relaxed_add(ts_pc(*X.S, X.cnt, F, f, k + 1), 1);
   }
 }
 
@@ -357,12 +445,23 @@ __device__ __forceinline__ double ts_xanc(const TSCtx& X, const SnInfo& I, const
 // done; i < nbp: one panel row block (after x_i; slot s = i)
 __device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i, double* sm) {
   const SnInfo I = X.P->sn[F.s];
-  double *A0 = sm, *A1 = sm + TBD, *xv = sm + 3 * TBD, *zv = xv + 64;
+  double *A0 = sm, *A1 = sm + TBD, *xv = sm + 3 * TBD, *zv = xv + 2 * 64;
   const bool urows = (i >= F.nbp);
   const int chunk = urows ? (i - F.nbp) / TS_UCHUNK : 0;
   const int i_lo = urows ? F.nbp + chunk * TS_UCHUNK : i;
   const int i_hi = urows ? min(F.nt - 1, i_lo + TS_UCHUNK - 1) : i;
+  static_assert(TS_UCHUNK <= 2, "ts_bupdate stages at most two tiles");
+  // every tile of the chunk and the row indices of its x entries are fetched before the wait;
+  // after it only the x values remain (one round trip)
   tile_load_async(A0, ts_tile(X, F, i_hi, k));
+  if (i_hi > i_lo) tile_load_async(A1, ts_tile(X, F, i_lo, k));
+  const int tq = threadIdx.x & 63, which = threadIdx.x >> 6;   // (entry, tile of the chunk)
+  const int ii_x = i_hi - which;
+  int xidx = -1;
+  if (which <= i_hi - i_lo && tq < tsize(F, ii_x)) {
+    const int row = trow0(F, ii_x) + tq;
+    xidx = urows ? __ldg(X.P->sn_rows + I.rp0 + row) : I.f0 + row;
+  }
   if (urows) {
     if (I.par >= 0) {
       const int hp = __ldg(X.T->hidx + I.par);
@@ -373,20 +472,12 @@ __device__ void ts_bupdate(const TSCtx& X, const TFront& F, int f, int k, int i,
     ts_wait(ts_xf(*X.S, X.cnt, F, f, i), 1);
   }
   ts_ready(X);
+  if (which <= i_hi - i_lo) xv[which * 64 + tq] = xidx >= 0 ? __ldcg(X.Xp + xidx) : 0.0;
   if (threadIdx.x < TBS) zv[threadIdx.x] = 0.0;
-  for (int ii = i_hi; ii >= i_lo; ii--) {
-    double* cur = ((i_hi - ii) & 1) ? A1 : A0;
-    double* nxt = ((i_hi - ii) & 1) ? A0 : A1;
-    const int nr = tsize(F, ii), r0 = trow0(F, ii);
-    if (threadIdx.x < TBS) {
-      const int q = threadIdx.x;
-      xv[q] = q < nr ? (urows ? ts_xanc(X, I, F, r0 + q) : __ldcg(X.Xp + I.f0 + r0 + q)) : 0.0;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (ii > i_lo) tile_load_async(nxt, ts_tile(X, F, ii - 1, k));  // next tile in flight
-    ts_gemv_t(zv, cur, xv);                                          // zv -= L^T x
-  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int ii = i_hi; ii >= i_lo; ii--)
+    ts_gemv_t(zv, ii == i_hi ? A0 : A1, xv + (i_hi - ii) * 64);   // zv -= L^T x (ii descending)
   if (threadIdx.x < TBS) ts_qslot(X, F, f, k, urows ? F.nbp + chunk : i)[threadIdx.x] = -zv[threadIdx.x];
   ts_publish_add(ts_qc(*X.S, X.cnt, F, f, k));
 }
@@ -435,9 +526,9 @@ __device__ void ts_bchain(const TSCtx& X, const TFront& F, int f, int k, double*
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // one fence publishes x_k and the front's done count
-    __threadfence();
-    st_release(ts_xf(*X.S, X.cnt, F, f, k), 1);
-    red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+    fence_acq_rel();
+    st_relaxed(ts_xf(*X.S, X.cnt, F, f, k), 1);
+    red_relaxed_add(ts_xdone(*X.S, X.cnt, F, f), 1);
   }
 }
 
@@ -504,7 +595,7 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
     for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
   if (threadIdx.x == 0) {  // every panel block gathered
     for (int t = 0; t < nbp; t++)
-      while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
+      while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(TS_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
@@ -528,8 +619,7 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
     ph ^= 1u << (q % TS_RING);
     if (threadIdx.x == 0) {
       if (q + TS_RING < ntile) ts_ring_issue(R, q + TS_RING, src(q + TS_RING));
-      __threadfence();
-      st_release(ts_yf(*X.S, X.cnt, F, f, j), 1);
+      st_release(ts_yf(*X.S, X.cnt, F, f, j), 1);   // cumulative over the barrier
     }
     q++;
     const int wv = X.S->wave;
@@ -571,8 +661,8 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
     for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
   if (threadIdx.x == 0) {  // the forward chain done, every update-row chunk product present
     for (int t = 0; t < nbp; t++) {
-      while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(32); }
-      while (ld_volatile(ts_qc(*X.S, X.cnt, F, f, t)) < nchunk) { __nanosleep(32); }
+      while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(TS_SLEEP); }
+      while (ld_volatile(ts_qc(*X.S, X.cnt, F, f, t)) < nchunk) { __nanosleep(TS_SLEEP); }
     }
     fence_acq_rel();
   }
@@ -605,9 +695,9 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
     ph ^= 1u << (q % TS_RING);
     if (threadIdx.x == 0) {
       if (q + TS_RING < ntile) ts_ring_issue(R, q + TS_RING, src(q + TS_RING));
-      __threadfence();
-      st_release(ts_xf(*X.S, X.cnt, F, f, i), 1);
-      red_release_add(ts_xdone(*X.S, X.cnt, F, f), 1);
+      fence_acq_rel();
+      st_relaxed(ts_xf(*X.S, X.cnt, F, f, i), 1);
+      red_relaxed_add(ts_xdone(*X.S, X.cnt, F, f), 1);
     }
     q++;
     const int wv = X.S->wave;

@@ -47,3 +47,12 @@ for t in range(len(names)):
               f"  wait mean {np.mean(rd[m]-st[m]):7.2f} us  total work {np.sum(en[m]-rd[m]):9.0f} us")
 if "--save" in sys.argv:
     np.savez(sys.argv[sys.argv.index("--save") + 1], tasks=tasks, trace=tr, est=est)
+if SOLVE and "--chains" in sys.argv:  # chain tasks in start order: front, start, ready, end (us)
+    for i in np.argsort(st):
+        if typ[i] in (6, 7):
+            print(f"  {names[typ[i]]} front {tasks[i, 1]:4d}  start {st[i]:8.1f}  ready {rd[i]:8.1f}  end {en[i]:8.1f}"
+                  f"  work {en[i] - rd[i]:6.1f}")
+if SOLVE and "--all" in sys.argv:  # every task in ticket order: type, front, z, w, start, ready, end (us)
+    for i in range(len(tasks)):
+        print(f"  T{i:5d} {names[typ[i]]:4s} f {tasks[i, 1]:4d} z {tasks[i, 2]:3d} w {tasks[i, 3]:3d}  start {st[i]:8.1f}"
+              f"  ready {rd[i]:8.1f}  end {en[i]:8.1f}  sm {int(tr[i, 3])}")
