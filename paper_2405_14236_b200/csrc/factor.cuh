@@ -245,8 +245,7 @@ __global__ void __launch_bounds__(KKT_BNT) factor_big_kernel(DevPlan P, const do
       if (tid == 0 && s_fail >= 0) atomicMin(fail_all, I.f0 + s_fail);
       if (tid == 0) trace_stamp(P, 0, s, b, 1);
       if (I.par < 0) break;
-      __threadfence();
-      __syncthreads();
+      __syncthreads();  // every thread's panel / U writes precede thread 0's release (cumulative)
       if (tid == 0) {
         const SnInfo Ip = s_Ip;
         if (Ip.huge) {            // the whole-GPU phase takes it from here
