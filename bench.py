@@ -247,16 +247,16 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------------------ ours
 def algorithmic_work(info, inst, refine_iters, cg_iters=0):
     """SURVEY §8(d) algorithmic work per instance.  HyKKT (m_eq > 0): every pass
-    runs cg_iters + 2 trsv pairs (z = K_gamma^-1 s, one per CG iteration, the final dx); the
-    G / G^T products are not counted (a lower bound); refine_iters = outer passes after the first,
-    each preceded by one dd residual.  cg_iters is the first pass's count, used for every pass."""
+    runs 2 trsv pairs (z = K_gamma^-1 s, the final dx) plus one per Krylov iteration; cg_iters is
+    the Krylov total over all passes (kkt_hykkt_stats); the G / G^T products are not counted (a
+    lower bound); refine_iters = outer passes after the first, each preceded by one dd residual."""
     n, m, nnzW, nnzJ = inst.n, inst.m, inst.nnzW, inst.nnzJ
     nnzK, nnzL = int(info["nnzK"]), int(info["nnzL"])
     condense_bytes = 8 * (nnzW + nnzJ + n + m) + 8 * nnzK
     trsv_bytes = 16 * nnzL + 24 * n
     resid_bytes = 24 * nnzW + 24 * nnzJ + 8 * (2 * n + m)
     if inst.m_eq > 0:
-        pairs = (1 + refine_iters) * (cg_iters + 2)
+        pairs = 2 * (1 + refine_iters) + cg_iters
         resid_passes = refine_iters
     else:
         pairs = 1 + refine_iters
@@ -425,7 +425,8 @@ def run_ours(args, rank, world):
             d2h = 8 * (hx.numel() + hdy.numel())
     # ---------------- roofline ----------------
     ph_mean = ph.mean(0)
-    work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0), max(info["cg_iters"], 0))
+    krylov_total = S.hykkt_stats()["krylov_total"] if hykkt else 0
+    work = algorithmic_work(S.info, inst, max(info["refine_iters"], 0), krylov_total)
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     pk = json.load(open(pk_path)) if os.path.exists(pk_path) else {}
     fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
@@ -460,7 +461,7 @@ def run_ours(args, rank, world):
                       "kernel": ("hykkt_solve" if hykkt else "kkt_solve") + " (fwd/bwd trsv kernels + dd residual)",
                       "work": f"B x [{work['trsv_pairs']} trsv pairs x (16 nnz(L) + 24 n) + "
                               f"{work['resid_passes']} dd residual passes] bytes"
-                              + (" (HyKKT: (cg_iters + 2) pairs per pass; G, G^T products not counted)"
+                              + (f" (HyKKT: {krylov_total} Krylov iterations over all passes + 2 pairs per pass; G, G^T products not counted)"
                                  if hykkt else ""),
                       "peak_note": hbm_note}
     for r_ in roofs.values():
@@ -489,6 +490,7 @@ def run_ours(args, rank, world):
            "factor_split_ms": {"small_big": float(fl_ms[0]), "large": float(fl_ms[1])},
            "instances_per_s": (C5_TOTAL if batched else world) / (value * 1e-3),
            "refine_iters": info["refine_iters"], "cg_iters": info["cg_iters"],
+           **({"krylov_iters_total": krylov_total} if hykkt else {}),
            "bwd_err": info["bwd_err"], "wall_s_timed": t_wall,
            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
            "gpu_launches": launches,

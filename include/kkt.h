@@ -302,6 +302,13 @@ kkt_status kkt_factor_phase_ms(kkt_handle h, double *ms);
 /* Number of kernel launches the last per-iteration call enqueued (evidence counter). */
 kkt_status kkt_launch_count(kkt_handle h, long long *launches);
 
+/* Work counts of the last hykkt_solve / hykkt_solve_krylov (§3.2): [host]
+ * *krylov_total = Krylov iterations (graph WHILE-body executions) summed over the first pass
+ * and the outer correction passes (each body = one K_gamma trsv pair for CG, one for CR);
+ * *outer_passes = correction passes run after the first (max over the batch).  Either pointer
+ * may be NULL.  Blocking (one stream sync).  KKT_ERR_STATE if the last solve was not HyKKT. */
+kkt_status kkt_hykkt_stats(kkt_handle h, int *krylov_total, int *outer_passes);
+
 /* Debug export (KKT_TRACE=2 at kkt_bind): copies up to n stamps [host] out[n] of the root
  * front's per-step globaltimer record of the whole-GPU factorization (8 per 32-column step).
  * Returns 0 on success, -1 when the record is off, -2 on a CUDA error.  Blocking. */

@@ -93,7 +93,16 @@ __global__ void gt_kernel(DevPlan P, const double* __restrict__ Jv, const double
     const double* J = Jv + (long long)b * P.nnzJ;
     const double* yb = y + (long long)b * P.m_eq;
     double acc = 0.0;
-    for (int p = P.Jt_p[i]; p < P.Gt_end[i]; p++) acc = fma(J[P.Jt_k[p]], yb[P.Jt_r[p]], acc);
+    int p = P.Jt_p[i];
+    const int pe = P.Gt_end[i];
+    for (; p + 4 <= pe; p += 4) {  // four terms' loads in flight, the same fma order
+      const int k0 = P.Jt_k[p], k1 = P.Jt_k[p + 1], k2 = P.Jt_k[p + 2], k3 = P.Jt_k[p + 3];
+      const int r0 = P.Jt_r[p], r1 = P.Jt_r[p + 1], r2 = P.Jt_r[p + 2], r3 = P.Jt_r[p + 3];
+      const double j0 = J[k0], j1 = J[k1], j2 = J[k2], j3 = J[k3];
+      const double y0 = yb[r0], y1 = yb[r1], y2 = yb[r2], y3 = yb[r3];
+      acc = fma(j0, y0, acc); acc = fma(j1, y1, acc); acc = fma(j2, y2, acc); acc = fma(j3, y3, acc);
+    }
+    for (; p < pe; p++) acc = fma(J[P.Jt_k[p]], yb[P.Jt_r[p]], acc);
     out[idx] = base ? fma(alpha, acc, base[idx]) : alpha * acc;
   }
 }
@@ -163,8 +172,8 @@ __global__ void cg_init_kernel(int batch, DevCtrl C, int use_odone) {
 // mode 1 (CG step):     q = G z ; alpha = rr / p.q
 // mode 2 (CR start):    s = q = G z (= S r0) ; rs = r.s ; qq = s.s ; alpha = rs / qq
 // mode 3 (CR step):     s = G z (= S r) ; beta = r.s / rs ; rs = r.s
-// grid (KKT_NPART, batch)
-__global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ z,
+// grid (KKT_NPART, batch), KKT_CGT threads
+__global__ void __launch_bounds__(KKT_CGT) g_kernel(DevPlan P, const double* __restrict__ Jv, const double* __restrict__ z,
                          const double* __restrict__ sub, double* out, double* p, double* dy,
                          DevCtrl C, int mode, int first, double* q) {
   __shared__ double red[32];
@@ -176,7 +185,15 @@ __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double*
   double part[2] = {0.0, 0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < me; r += KKT_NPART * blockDim.x) {
     double acc = 0.0;
-    for (int t = P.Jrp[r]; t < P.Jrp[r + 1]; t++) acc = fma(J[t], zb[P.Jci[t]], acc);
+    int t = P.Jrp[r];
+    const int te = P.Jrp[r + 1];
+    for (; t + 4 <= te; t += 4) {  // four terms' loads in flight, the same fma order
+      const int c0 = P.Jci[t], c1 = P.Jci[t + 1], c2 = P.Jci[t + 2], c3 = P.Jci[t + 3];
+      const double j0 = J[t], j1 = J[t + 1], j2 = J[t + 2], j3 = J[t + 3];
+      const double z0 = zb[c0], z1 = zb[c1], z2 = zb[c2], z3 = zb[c3];
+      acc = fma(j0, z0, acc); acc = fma(j1, z1, acc); acc = fma(j2, z2, acc); acc = fma(j3, z3, acc);
+    }
+    for (; t < te; t++) acc = fma(J[t], zb[P.Jci[t]], acc);
     const long long o = (long long)b * me + r;
     if (mode == 0) {
       acc -= sub[o];
@@ -225,7 +242,7 @@ __global__ void g_kernel(DevPlan P, const double* __restrict__ Jv, const double*
 // Correction passes of the outer refinement (first == 0) stop at the absolute level
 // rtol ||r0 of the first pass|| -- the correction only has to be accurate relative to the
 // solution it corrects, not relative to its own (small) right-hand side.
-__global__ void cg_update_kernel(int batch, int me, double* dy, double* r, const double* __restrict__ p,
+__global__ void __launch_bounds__(KKT_CGT) cg_update_kernel(int batch, int me, double* dy, double* r, const double* __restrict__ p,
                                  const double* __restrict__ q, DevCtrl C, double rtol, int* status, int first,
                                  int maxit) {
   __shared__ double red[32];
@@ -268,7 +285,7 @@ __global__ void cg_p_kernel(int batch, int me, double* p, const double* __restri
 }
 
 // CR: p = r + beta p ; q = s + beta q ; qq = q.q ; alpha = rs / qq.  grid (KKT_NPART, batch)
-__global__ void cr_pq_kernel(int batch, int me, double* p, double* q, const double* __restrict__ r,
+__global__ void __launch_bounds__(KKT_CGT) cr_pq_kernel(int batch, int me, double* p, double* q, const double* __restrict__ r,
                              const double* __restrict__ sv, DevCtrl C) {
   __shared__ double red[32];
   const int b = blockIdx.y;

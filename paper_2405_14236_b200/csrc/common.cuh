@@ -19,6 +19,7 @@ namespace kkt {
 
 #define KKT_NT 128          // threads per CTA of the persistent kernels
 #define KKT_NPART 64        // reduction partials per instance
+#define KKT_CGT 1024        // threads per block of the per-instance Krylov reductions (G z, updates)
 
 // ------------------------------------------------------------------ memory-model helpers
 __device__ __forceinline__ int ld_acquire(const int* p) {

@@ -973,6 +973,10 @@ static kkt_status bind_impl(kkt_handle h, int device, void* d_workspace, size_t 
         h->tsp.ncnt = tsh.ncnt;
         h->tsp.cbase2 = (const int*)(tb_ + sb);
         h->tsp.cnt = (int*)(tb_ + sb + cbb + pbb + partb);
+        if (h->sblock) {  // zeroed by tree_fwd_kernel, the kernel before the tile solve
+          h->sbp.zbuf = h->tsp.cnt;
+          h->sbp.zn = (int)(h->ts_cnt_bytes / sizeof(int));
+        }
         h->tsp.trace = nullptr;
         CUDA_TRY(cudaFuncSetAttribute(tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TS_SMEM_BYTES));
       }
@@ -1042,7 +1046,6 @@ extern "C" kkt_status kkt_condense(kkt_handle h, const double* W_vals, const dou
   h->launches = 0;
   h->graph_solve_pending = false;
   h->hy_pending = false;
-  h->last_hykkt = false;
   if (P.m > 0) {
     dweights_kernel<<<grid_for((long long)P.batch * P.m, 256, h->sms), 256, 0, h->ls>>>(
         h->dp, Sigma_s, D, delta_w, delta_c, gamma, h->Dh, h->Dl);
@@ -1142,7 +1145,7 @@ static kkt_status launch_huge_solve(kkt_plan* h, const double* rhs, long long rs
   const Plan& P = h->P;
   const bool cta_huge = h->huge_solve_cta;
   if (!P.order_h.empty() && !cta_huge && h->tsolve) {
-    CUDA_TRY(cudaMemsetAsync(h->tsp.cnt, 0, h->ts_cnt_bytes, h->ls));
+    if (!(h->sblock && h->sbp.zbuf)) CUDA_TRY(cudaMemsetAsync(h->tsp.cnt, 0, h->ts_cnt_bytes, h->ls));
     DevPlan dp = h->dp;
     TilePlan tp = h->tp;
     TSolvePlan sp = h->tsp;
@@ -1551,14 +1554,14 @@ static kkt_status hykkt_pass(kkt_plan* h, cudaGraph_t g, cudaGraphConditionalHan
     gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, r2, h->gamma, r1, h->sg, skip);
     LAUNCH_CHECK();
     TRY(launch_solve(h, h->sg, P.n, h->zv, P.n, skip));
-    g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0, first ? 1 : 0, nullptr);
+    g_kernel<<<gg, KKT_CGT, 0, h->ls>>>(h->dp, h->Jv, h->zv, r2, h->cr, h->cp, dyo, h->C, 0, first ? 1 : 0, nullptr);
     LAUNCH_CHECK();
     h->launches += 3;
     if (krylov == 1) {  // s0 = q0 = S r0 (p0 = r0)
       gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
       LAUNCH_CHECK();
       TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cs, h->cp, nullptr, h->C, 2, 0, h->cq);
+      g_kernel<<<gg, KKT_CGT, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cs, h->cp, nullptr, h->C, 2, 0, h->cq);
       LAUNCH_CHECK();
       h->launches += 2;
     }
@@ -1573,24 +1576,24 @@ static kkt_status hykkt_pass(kkt_plan* h, cudaGraph_t g, cudaGraphConditionalHan
       gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cp, 1.0, nullptr, h->wv, h->C.cg_done);
       LAUNCH_CHECK();
       TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1, 0, nullptr);
+      g_kernel<<<gg, KKT_CGT, 0, h->ls>>>(h->dp, h->Jv, h->zv, nullptr, h->cq, h->cp, nullptr, h->C, 1, 0, nullptr);
       LAUNCH_CHECK();
-      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+      cg_update_kernel<<<gg, KKT_CGT, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
                                                rtol, h->status, first ? 1 : 0, maxit);
       LAUNCH_CHECK();
       cg_p_kernel<<<dim3(std::max(1, std::min((P.m_eq + 255) / 256, 64)), P.batch), 256, 0, h->ls>>>(
           P.batch, P.m_eq, h->cp, h->cr, h->C);
       LAUNCH_CHECK();
     } else {
-      cg_update_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
+      cg_update_kernel<<<gg, KKT_CGT, 0, h->ls>>>(P.batch, P.m_eq, dyo, h->cr, h->cp, h->cq, h->C,
                                                rtol, h->status, first ? 1 : 0, maxit);
       LAUNCH_CHECK();
       gt_kernel<<<gs, 256, 0, h->ls>>>(h->dp, h->Jv, h->cr, 1.0, nullptr, h->wv, h->C.cg_done);
       LAUNCH_CHECK();
       TRY(launch_solve(h, h->wv, P.n, h->zv, P.n, h->C.cg_done));
-      g_kernel<<<gg, 256, 0, h->ls>>>(h->dp, h->Jv, h->zv, h->cr, h->cs, nullptr, nullptr, h->C, 3, 0, nullptr);
+      g_kernel<<<gg, KKT_CGT, 0, h->ls>>>(h->dp, h->Jv, h->zv, h->cr, h->cs, nullptr, nullptr, h->C, 3, 0, nullptr);
       LAUNCH_CHECK();
-      cr_pq_kernel<<<gg, 256, 0, h->ls>>>(P.batch, P.m_eq, h->cp, h->cq, h->cr, h->cs, h->C);
+      cr_pq_kernel<<<gg, KKT_CGT, 0, h->ls>>>(P.batch, P.m_eq, h->cp, h->cq, h->cr, h->cs, h->C);
       LAUNCH_CHECK();
     }
     cg_cond_kernel<<<1, 1, 0, h->ls>>>(P.batch, h->C, hc, 1);
@@ -2048,6 +2051,20 @@ extern "C" kkt_status kkt_launch_count(kkt_handle h, long long* launches) {
     h->hy_pending = false;
   }
   *launches = h->launches;
+  return KKT_OK;
+}
+
+extern "C" kkt_status kkt_hykkt_stats(kkt_handle h, int* krylov_total, int* outer_passes) {
+  if (!h) return KKT_ERR_ARG;
+  if (!h->last_hykkt) { g_err = "the last solve was not hykkt_solve"; return KKT_ERR_STATE; }
+  const Plan& P = h->P;
+  int runs = 0;
+  std::vector<int> op(P.batch);
+  CUDA_TRY(cudaMemcpyAsync(&runs, h->C.cg_runs, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(op.data(), h->C.opass, P.batch * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (krylov_total) *krylov_total = runs;
+  if (outer_passes) *outer_passes = *std::max_element(op.begin(), op.end());
   return KKT_OK;
 }
 

@@ -48,6 +48,8 @@ struct SBPlan {
   int n_fwd;            //   longest estimated path to the top first
   const int2* bwd_order;// backward tasks {supernode, supernode to wait for or -1} in estimated
   int n_bwd;            //   start order (topological: parents first)
+  int* zbuf;            // the tile solve's dependency counters, zeroed by the forward kernel
+  int zn;               //   (the next kernel in the stream; no separate memset node) or null
 };
 
 // one contiguous range staged by TMA: shift = elements between the 16-byte-aligned start and
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(NT, BLK ? 1 : sb_minb<NT>()) tree_fwd_kernel(D
   if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
   pdl_launch_dependents();
+  for (int q = blockIdx.x * NT + tid; q < B.zn; q += gridDim.x * NT) B.zbuf[q] = 0;
   if (done && done[P.batch] == 0) return;  // every instance has finished refining
   uint32_t phase = 0;
   const int ntask = B.n_fwd * P.batch;

@@ -21,7 +21,7 @@ KKT_STATUS = {0: "KKT_OK", 1: "KKT_ERR_ARG", 2: "KKT_ERR_PATTERN", 3: "KKT_ERR_N
 
 EXPORTS = ["kkt_default_options", "kkt_analyze", "kkt_get_symbolic", "kkt_workspace_size",
            "kkt_bind", "kkt_condense", "kkt_factor", "kkt_solve", "hykkt_solve", "hykkt_solve_krylov",
-           "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_blocks", "kkt_get_trace", "kkt_launch_count",
+           "kkt_sync_info", "kkt_inertia", "kkt_factor_inertia_correct", "kkt_solve_unreduced", "kkt_recover", "kkt_recover_bounds", "kkt_step_host", "kkt_get_condensed", "kkt_get_supernodes", "kkt_get_blocks", "kkt_get_trace", "kkt_launch_count", "kkt_hykkt_stats",
            "kkt_factor_phase_ms", "kkt_debug_steps", "kkt_tile_trace", "kkt_tile_solve_trace", "kkt_last_error", "kkt_destroy"]
 
 
@@ -86,6 +86,7 @@ def lib(build_if_missing: bool = True):
             "kkt_solve_unreduced": [P] + [P] * 4 + [P] * 6 + [P] * 6 + [I, D],
             "kkt_recover_bounds": [P, P, P, P, P, D, P, P, P, P],
             "kkt_launch_count": [P, C.POINTER(C.c_longlong)],
+            "kkt_hykkt_stats": [P, C.POINTER(C.c_int), C.POINTER(C.c_int)],
             "kkt_get_supernodes": [P, C.POINTER(I), P, P, P],
             "kkt_get_blocks": [P, I, I, I, P, P, P, P, P, P, P],
             "kkt_get_trace": [P, P],
@@ -268,6 +269,12 @@ def kkt_get_trace(h, ns):
     return t[:, :ns]
 
 
+def kkt_hykkt_stats(h):
+    kr, op = C.c_int(0), C.c_int(0)
+    _chk(lib().kkt_hykkt_stats(h, C.byref(kr), C.byref(op)), "kkt_hykkt_stats")
+    return {"krylov_total": kr.value, "outer_passes": op.value}
+
+
 def kkt_launch_count(h):
     v = C.c_longlong()
     _chk(lib().kkt_launch_count(h, C.byref(v)), "kkt_launch_count")
@@ -383,6 +390,9 @@ class KKTSolver:
 
     def launch_count(self):
         return kkt_launch_count(self.h)
+
+    def hykkt_stats(self):
+        return kkt_hykkt_stats(self.h)
 
     def factor_phase_ms(self):
         return kkt_factor_phase_ms(self.h)

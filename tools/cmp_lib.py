@@ -1,7 +1,8 @@
 """Bitwise comparison of two builds of libkkt on one config (KKT_LIB selects the library).
 
-usage: python tools/cmp_lib.py CFG other.so   -> runs the config with the default library and with
-other.so in a subprocess, compares x (and dx, dy for HyKKT) bit for bit.
+usage: python tools/cmp_lib.py CFG other.so|other_checkout_dir   -> runs the config with the default
+library and with the other library (or another checkout's binding + library) in a subprocess,
+compares x (and dx, dy for HyKKT) bit for bit.
 """
 import os, sys, subprocess, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -30,7 +31,12 @@ if len(sys.argv) > 3 and sys.argv[2] == "--dump":
 import numpy as np
 env = dict(os.environ)
 subprocess.run([sys.executable, __file__, cfg, "--dump", "/tmp/cmp_a.npy"], check=True, env=env)
-env["KKT_LIB"] = os.path.abspath(sys.argv[2])
-subprocess.run([sys.executable, __file__, cfg, "--dump", "/tmp/cmp_b.npy"], check=True, env=env)
+other = os.path.abspath(sys.argv[2])
+if os.path.isdir(other):  # another checkout (its own binding and library)
+    subprocess.run([sys.executable, os.path.join(other, "tools", "cmp_lib.py"), cfg, "--dump", "/tmp/cmp_b.npy"],
+                   check=True, env=env, cwd=other)
+else:
+    env["KKT_LIB"] = other
+    subprocess.run([sys.executable, __file__, cfg, "--dump", "/tmp/cmp_b.npy"], check=True, env=env)
 a, b = np.load("/tmp/cmp_a.npy"), np.load("/tmp/cmp_b.npy")
 print(cfg, "bitwise equal" if np.array_equal(a, b) else f"DIFFER max {np.abs(a - b).max():.3e}")
