@@ -28,7 +28,18 @@ __global__ void resid_rows_kernel(DevPlan P, const double* __restrict__ Jv, cons
     int p0 = P.Jrp[r], p1 = P.Jrp[r + 1];
     dd acc = {0.0, 0.0};
     double aa = 0.0;
-    for (int p = p0; p < p1; p++) {
+    int p = p0;
+    for (; p + 4 <= p1; p += 4) {  // four terms' loads in flight; the same summation order
+      const int c0 = P.Jci[p], c1 = P.Jci[p + 1], c2 = P.Jci[p + 2], c3 = P.Jci[p + 3];
+      const double jv[4] = {J[p], J[p + 1], J[p + 2], J[p + 3]};
+      const double xv[4] = {xb[c0], xb[c1], xb[c2], xb[c3]};
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        acc = dd_add(acc, two_prod(jv[u], xv[u]));
+        aa = fma(fabs(jv[u]), fabs(xv[u]), aa);
+      }
+    }
+    for (; p < p1; p++) {
       double jv = J[p], xv = xb[P.Jci[p]];
       acc = dd_add(acc, two_prod(jv, xv));
       aa = fma(fabs(jv), fabs(xv), aa);
@@ -67,12 +78,40 @@ __global__ void resid_cols_kernel(DevPlan P, const double* __restrict__ Wv, cons
     dd s = two_sum(Sx[idx], dw);
     dd y = dd_mul_d(s, xi);
     double den = fabs(s.hi) * fabs(xi);
-    for (int p = P.Wf_p[i]; p < P.Wf_p[i + 1]; p++) {
+    // loads of four terms in flight per step; the summation order is the sequential one
+    int p = P.Wf_p[i];
+    const int pw = P.Wf_p[i + 1];
+    for (; p + 4 <= pw; p += 4) {
+      const int k0 = P.Wf_k[p], k1 = P.Wf_k[p + 1], k2 = P.Wf_k[p + 2], k3 = P.Wf_k[p + 3];
+      const int c0 = P.Wf_c[p], c1 = P.Wf_c[p + 1], c2 = P.Wf_c[p + 2], c3 = P.Wf_c[p + 3];
+      const double wv[4] = {W[k0], W[k1], W[k2], W[k3]};
+      const double xv[4] = {xb[c0], xb[c1], xb[c2], xb[c3]};
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        y = dd_add(y, two_prod(wv[u], xv[u]));
+        den = fma(fabs(wv[u]), fabs(xv[u]), den);
+      }
+    }
+    for (; p < pw; p++) {
       double wv = W[P.Wf_k[p]], xv = xb[P.Wf_c[p]];
       y = dd_add(y, two_prod(wv, xv));
       den = fma(fabs(wv), fabs(xv), den);
     }
-    for (int p = P.Jt_p[i]; p < P.Jt_p[i + 1]; p++) {
+    p = P.Jt_p[i];
+    const int pj = P.Jt_p[i + 1];
+    for (; p + 4 <= pj; p += 4) {
+      const int r0 = P.Jt_r[p], r1 = P.Jt_r[p + 1], r2 = P.Jt_r[p + 2], r3 = P.Jt_r[p + 3];
+      const int k0 = P.Jt_k[p], k1 = P.Jt_k[p + 1], k2 = P.Jt_k[p + 2], k3 = P.Jt_k[p + 3];
+      const double jv[4] = {J[k0], J[k1], J[k2], J[k3]};
+      const double2 t[4] = {Tb[r0], Tb[r1], Tb[r2], Tb[r3]};
+      const double av[4] = {Ab[r0], Ab[r1], Ab[r2], Ab[r3]};
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        y = dd_add(y, dd_mul_d(dd{t[u].x, t[u].y}, jv[u]));
+        den = fma(fabs(jv[u]), av[u], den);
+      }
+    }
+    for (; p < pj; p++) {
       int r = P.Jt_r[p];
       double jv = J[P.Jt_k[p]];
       double2 t = Tb[r];
