@@ -593,9 +593,8 @@ __device__ void ts_fchain_front(const TSCtx& X, const TFront& F, int f, double* 
   __syncthreads();  // the previous task's shared-memory reads are done
   if (threadIdx.x == 0)
     for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
-  if (threadIdx.x == 0) {  // every panel block gathered
-    for (int t = 0; t < nbp; t++)
-      while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(TS_SLEEP); }
+  if (threadIdx.x < nbp) {  // every panel block gathered (one flag per thread: polled in parallel)
+    while (ld_volatile(ts_gf(*X.S, X.cnt, F, f, threadIdx.x)) < 1) { __nanosleep(TS_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
@@ -659,11 +658,9 @@ __device__ void ts_bchain_front(const TSCtx& X, const TFront& F, int f, double* 
   __syncthreads();
   if (threadIdx.x == 0)
     for (int q = 0; q < min(TS_RING, ntile); q++) ts_ring_issue(R, q, src(q));
-  if (threadIdx.x == 0) {  // the forward chain done, every update-row chunk product present
-    for (int t = 0; t < nbp; t++) {
-      while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, t)) < 1) { __nanosleep(TS_SLEEP); }
-      while (ld_volatile(ts_qc(*X.S, X.cnt, F, f, t)) < nchunk) { __nanosleep(TS_SLEEP); }
-    }
+  if (threadIdx.x < nbp) {  // the forward chain done, every update-row chunk product present
+    while (ld_volatile(ts_yf(*X.S, X.cnt, F, f, threadIdx.x)) < 1) { __nanosleep(TS_SLEEP); }
+    while (ld_volatile(ts_qc(*X.S, X.cnt, F, f, threadIdx.x)) < nchunk) { __nanosleep(TS_SLEEP); }
     fence_acq_rel();
   }
   __syncthreads();
