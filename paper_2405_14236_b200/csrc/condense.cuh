@@ -54,8 +54,21 @@ __global__ void __launch_bounds__(256) condense_kernel(DevPlan P, const double* 
     int w = __ldg(P.kw + k), dg = __ldg(P.kdiag + k);
     double v = (w >= 0) ? __ldg(W + w) : 0.0;
     if (dg >= 0) v += __ldg(Sx + (long long)b * P.n + dg) + dw;
-    int q0 = __ldg(P.pptr + k), q1 = __ldg(P.pptr + k + 1);
-    for (int q = q0; q < q1; q++) {
+    int q = __ldg(P.pptr + k);
+    const int q1 = __ldg(P.pptr + k + 1);
+    for (; q + 4 <= q1; q += 4) {  // four products' loads in flight, the same fma order
+      int a[4], c[4], r[4];
+      double ja[4], jc[4], d[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) { a[u] = __ldg(P.pa + q + u); c[u] = __ldg(P.pb + q + u); }
+#pragma unroll
+      for (int u = 0; u < 4; u++) { r[u] = __ldg(P.jrow + a[u]); ja[u] = __ldg(J + a[u]); jc[u] = __ldg(J + c[u]); }
+#pragma unroll
+      for (int u = 0; u < 4; u++) d[u] = __ldg(D + r[u]);
+#pragma unroll
+      for (int u = 0; u < 4; u++) v = fma(d[u] * ja[u], jc[u], v);
+    }
+    for (; q < q1; q++) {
       int a = __ldg(P.pa + q), c = __ldg(P.pb + q);
       v = fma(__ldg(D + __ldg(P.jrow + a)) * __ldg(J + a), __ldg(J + c), v);
     }

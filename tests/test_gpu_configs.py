@@ -243,6 +243,12 @@ def test_hykkt_is_graph_launched_without_host_sync():
     dx, dy, info, S = run_hykkt(inst, max_outer=2)
     n1 = S.launch_count()
     assert n1 > 10 * max(info["cg_iters"], 1)
+    # work counts: the Krylov total covers every pass (at least the first pass's count), the
+    # outer passes match kkt_sync_info's report, and the launch count is consistent with them
+    st = S.hykkt_stats()
+    assert st["krylov_total"] >= info["cg_iters"] >= 1, (st, info)
+    assert st["outer_passes"] == info["refine_iters"] and 0 <= st["outer_passes"] <= 2, (st, info)
+    assert n1 >= 5 * st["krylov_total"], (n1, st)
     dx2, dy2, info2, _ = run_hykkt(inst, max_outer=2, solver=S)
     assert np.array_equal(dx, dx2) and np.array_equal(dy, dy2)     # deterministic
     S.close()
