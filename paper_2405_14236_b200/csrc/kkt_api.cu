@@ -112,6 +112,8 @@ struct kkt_plan {
   // host-buffer path (kkt_step_host)
   double *hW = nullptr, *hJ = nullptr, *hSx = nullptr, *hSs = nullptr, *hD = nullptr,
          *hb = nullptr, *hx = nullptr;
+  cudaStream_t hcopy = nullptr;          // copy stream: b's upload overlaps condense + factor
+  cudaEvent_t hev[2] = {nullptr, nullptr};
   int* pinned_flags = nullptr;
   long long* trace_buf = nullptr;
   long long* dbg_buf = nullptr;  // KKT_TRACE=2: per-step stamps of the root front (huge path)
@@ -459,6 +461,9 @@ static void release_device(kkt_plan* h) {
   h->extra_exec.clear();
   if (h->cap) cudaStreamDestroy(h->cap);
   h->cap = nullptr;
+  if (h->hcopy) cudaStreamDestroy(h->hcopy);
+  h->hcopy = nullptr;
+  for (auto& e : h->hev) { if (e) cudaEventDestroy(e); e = nullptr; }
   for (auto& e : h->fev) { if (e) cudaEventDestroy(e); e = nullptr; }
   h->fev_valid = false;
   h->bound = false;
@@ -1885,6 +1890,10 @@ extern "C" kkt_status kkt_step_host(kkt_handle h, const double* W_vals, const do
     CUDA_TRY(cudaMalloc(&h->hb, B * P.n * 8));
     CUDA_TRY(cudaMalloc(&h->hx, B * P.n * 8));
   }
+  if (!h->hcopy) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->hcopy, cudaStreamNonBlocking));
+    for (auto& e : h->hev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   cudaStream_t s = h->stream;
   if (P.nnzW) CUDA_TRY(cudaMemcpyAsync(h->hW, W_vals, B * P.nnzW * 8, cudaMemcpyHostToDevice, s));
   if (P.nnzJ) CUDA_TRY(cudaMemcpyAsync(h->hJ, J_vals, B * P.nnzJ * 8, cudaMemcpyHostToDevice, s));
@@ -1892,9 +1901,15 @@ extern "C" kkt_status kkt_step_host(kkt_handle h, const double* W_vals, const do
   if (Sigma_s && P.m > P.m_eq)
     CUDA_TRY(cudaMemcpyAsync(h->hSs, Sigma_s, B * (P.m - P.m_eq) * 8, cudaMemcpyHostToDevice, s));
   if (D && P.m) CUDA_TRY(cudaMemcpyAsync(h->hD, D, B * P.m * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(h->hb, b, B * P.n * 8, cudaMemcpyHostToDevice, s));
+  // b is needed only by the solve: its upload runs on the copy stream while the handle's stream
+  // condenses and factorises (after the matrix uploads, so it does not share the link with them)
+  CUDA_TRY(cudaEventRecord(h->hev[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(h->hcopy, h->hev[0], 0));
+  CUDA_TRY(cudaMemcpyAsync(h->hb, b, B * P.n * 8, cudaMemcpyHostToDevice, h->hcopy));
+  CUDA_TRY(cudaEventRecord(h->hev[1], h->hcopy));
   TRY(kkt_condense(h, h->hW, h->hJ, h->hSx, Sigma_s ? h->hSs : nullptr, D ? h->hD : nullptr, delta_w, delta_c, gamma));
   TRY(kkt_factor(h));
+  CUDA_TRY(cudaStreamWaitEvent(s, h->hev[1], 0));
   TRY(kkt_solve(h, h->hb, h->hx, max_refine, tol_bwd));
   CUDA_TRY(cudaMemcpyAsync(x, h->hx, B * P.n * 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
