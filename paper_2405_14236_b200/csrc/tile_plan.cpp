@@ -337,7 +337,10 @@ void build_tile_solve_plan(const Plan& P, const TilePlanHost& tp, int workers, b
     const int par = P.sn_parent[F.s];
     const int hp = par >= 0 ? tp.hidx[par] : -1;
     std::vector<std::vector<int>> q(nbp);       // producers of Q[k][.]
-    const int UCH = 2;   // tsolve.cuh TS_UCHUNK
+#ifndef TS_UCHUNK_N
+#define TS_UCHUNK_N 1
+#endif
+    const int UCH = TS_UCHUNK_N;   // tsolve.cuh TS_UCHUNK
     for (int k = 0; k < nbp; k++)       // update rows in chunks of UCH tiles, parallel
       for (int c0 = nbp; c0 < nt; c0 += UCH) {
         std::vector<int> p;

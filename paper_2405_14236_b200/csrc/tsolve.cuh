@@ -38,7 +38,10 @@ constexpr int TS_GATHER = 0, TS_FU = 1, TS_FC = 2, TS_BU = 3, TS_BC = 4, TS_UF =
 constexpr int TS_RING = 6;
 constexpr int TS_NBP_MAX = 24;   // panel row blocks per front the chain tasks support
 constexpr int TS_SMEM_BYTES = (TS_RING * TBD + 2 * TS_NBP_MAX * 64 + 2 * 64) * 8;
-constexpr int TS_UCHUNK = 2;   // update-row tiles per backward task (parallel chunks, one slot each)
+#ifndef TS_UCHUNK_N
+#define TS_UCHUNK_N 1   // (shared with tile_plan.cpp; 1 measured faster than 2 on C3/C4)
+#endif
+constexpr int TS_UCHUNK = TS_UCHUNK_N;   // update-row tiles per backward task (parallel chunks, one slot each)
 
 struct TSolvePlan {
   const int4* tasks;   // x = type | (instance << 4), y = front, z = i, w = k
